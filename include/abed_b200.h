@@ -1,0 +1,272 @@
+/* abed_b200.h -- C ABI of the B200-native ABED convolution library
+ * (libabed_b200.so).  Plain C: pointers, sizes and POD structs only.
+ *
+ * Every entry point replaces one function of the reference's header-only C++
+ * API (/root/reference/proj/include/abed/*.hpp); the reference file:line is
+ * cited beside each declaration.  Tensors keep the reference layouts (NCHW
+ * activations, KCRS filters, N x K x P x Q ConvOut, 1 x C x R x S checksums;
+ * tensor.hpp:68-70) and are passed as DEVICE pointers unless stated otherwise;
+ * `stream` is a cudaStream_t (NULL = legacy default stream).
+ *
+ * Error convention (mirrors the reference's exceptions):
+ *   ABED_OK                    success
+ *   ABED_ERR_INVALID_ARGUMENT  reference throws std::invalid_argument
+ *   ABED_ERR_OUT_OF_RANGE      reference throws std::out_of_range
+ *   ABED_ERR_RUNTIME           reference throws std::runtime_error
+ *   ABED_ERR_CUDA              CUDA failure (no reference counterpart)
+ *   ABED_ERR_NO_DEVICE         no usable sm_100 device: the library never falls
+ *                              back to host computation
+ * A checksum mismatch is NOT an error: it is abed_verify_outcome.status = 1.
+ * abed_last_error() returns the message of the last failing call (thread-local).
+ */
+#ifndef ABED_B200_H
+#define ABED_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  ABED_OK = 0,
+  ABED_ERR_INVALID_ARGUMENT = 1,
+  ABED_ERR_OUT_OF_RANGE = 2,
+  ABED_ERR_RUNTIME = 3,
+  ABED_ERR_CUDA = 4,
+  ABED_ERR_NO_DEVICE = 5
+};
+
+/* element kinds, tensor.hpp:20 (ElemKind : uint8_t {I8, I32, I64, F32}) */
+enum { ABED_I8 = 0, ABED_I32 = 1, ABED_I64 = 2, ABED_F32 = 3 };
+/* convolution.hpp:342 Activation */
+enum { ABED_RELU = 0, ABED_IDENTITY = 1 };
+/* checksum.hpp:15 Scheme */
+enum { ABED_FC = 0, ABED_IC = 1, ABED_ICBATCH = 2, ABED_FIC = 3 };
+/* faults.hpp:17 InjectionTarget, :28 Classification, :71 DataMode */
+enum { ABED_TARGET_INPUT = 0, ABED_TARGET_FILTER = 1, ABED_TARGET_CONVOUT = 2 };
+enum { ABED_DETECTED = 0, ABED_SDC = 1, ABED_MASKED = 2, ABED_DETECTED_BENIGN = 3 };
+enum { ABED_DATA_ONES = 0, ABED_DATA_RANDOM_I8 = 1 };
+
+/* tensor.hpp:58-66 Dims4 */
+typedef struct abed_dims4 {
+  int64_t d0, d1, d2, d3;
+} abed_dims4;
+
+/* tensor.hpp:171-203 LayerShape (same field order) */
+typedef struct abed_layer_shape {
+  int64_t n, c, h, w, k, r, s, stride_h, stride_w, pad_h, pad_w, p, q;
+} abed_layer_shape;
+
+/* convolution.hpp:346-351 EpilogParams; bias = DEVICE pointer, K floats */
+typedef struct abed_epilog_params {
+  float scale;
+  const float* bias;
+  int64_t bias_len;
+  int32_t activation;  /* ABED_RELU / ABED_IDENTITY */
+  int32_t output_kind; /* ABED_I8 / ABED_F32 */
+} abed_epilog_params;
+
+/* checksum.hpp:30-51 VerifyOutcome (+ error_count: number of mismatching loci) */
+typedef struct abed_verify_outcome {
+  int32_t status;    /* 0 = Pass, 1 = Mismatch */
+  int32_t has_locus; /* locus present */
+  int64_t locus[3];
+  int64_t lhs, rhs;
+  double lhs_f, rhs_f;
+  int64_t error_count;
+} abed_verify_outcome;
+
+/* checksum.hpp:429-441 PrecisionPlan */
+typedef struct abed_precision_plan {
+  int32_t operand_bits, bits_output_fmap, bits_reduced_fc, bits_reduced_fic;
+  int32_t bits_filter_checksum, bits_input_checksum;
+  int32_t output_fmap_kind, reduced_fc_kind, reduced_fic_kind;
+  int32_t filter_checksum_kind, input_checksum_kind;
+} abed_precision_plan;
+
+/* faults.hpp:77-86 CampaignConfig (epilog bias is HOST memory here, may be NULL = zeros) */
+typedef struct abed_campaign_config {
+  abed_layer_shape shape;
+  int32_t scheme, target;
+  int64_t trials;
+  uint64_t root_seed;
+  int32_t mode;
+  float scale;
+  const float* bias_host;
+  int64_t bias_len;
+  int32_t activation, output_kind;
+  int32_t jobs; /* accepted for API parity; the GPU batches trials itself */
+} abed_campaign_config;
+
+/* faults.hpp:88-107 CampaignReport */
+typedef struct abed_campaign_report {
+  int32_t scheme, target;
+  int64_t trials, detected, detected_benign, sdc, masked;
+  uint64_t seed;
+} abed_campaign_report;
+
+/* faults.hpp:40-51 TrialOutcome (FlipSpec folded in) */
+typedef struct abed_trial_outcome {
+  int32_t classification;
+  int32_t target;
+  int64_t flat_index;
+  int32_t bit;
+  int32_t final_output_differs;
+  abed_verify_outcome verify;
+} abed_trial_outcome;
+
+/* ------------------------------------------------------------ library / device */
+const char* abed_last_error(void);
+int abed_device_check(void); /* ABED_OK iff an sm_100 device is present */
+int abed_version(void);
+int abed_malloc(void** dptr, size_t bytes);
+int abed_free(void* dptr);
+int abed_memcpy_h2d(void* dst, const void* src, size_t bytes);
+int abed_memcpy_d2h(void* dst, const void* src, size_t bytes);
+int abed_memset(void* dptr, int value, size_t bytes);
+int abed_synchronize(void);
+
+/* ------------------------------------------------------------ L0 data / rng */
+/* tensor.hpp:178-193 LayerShape::make (validation + derived p, q) */
+int abed_layer_shape_make(int64_t n, int64_t c, int64_t h, int64_t w, int64_t k, int64_t r,
+                          int64_t s, int64_t stride_h, int64_t stride_w, int64_t pad_h,
+                          int64_t pad_w, abed_layer_shape* out);
+/* rng.hpp:11-37 SplitMix64 stream element i = mix(seed + (i+1)*golden): index-parallel fill.
+ * fill_random_i8 (rng.hpp:46) continuing a stream already advanced by `offset` draws. */
+int abed_fill_random_i8(int8_t* data, int64_t count, uint64_t seed, uint64_t offset, void* stream);
+/* rng.hpp:51 fill_random_extreme */
+int abed_fill_random_extreme(int8_t* data, int64_t count, uint64_t seed, uint64_t offset, void* stream);
+/* rng.hpp:41-44 derive_seed (host) */
+uint64_t abed_derive_seed(uint64_t root, uint64_t index);
+
+/* ------------------------------------------------------------ L1 convolution */
+/* convolution.hpp:237 conv_direct / :224 detail::conv_fast_i8: int8 x int8 -> int32 ConvOut.
+ * ABED_ERR_INVALID_ARGUMENT when CRS > 65536 (:239-240).  tcgen05 implicit GEMM. */
+int abed_conv_i8(const int8_t* input, const int8_t* filters, const abed_layer_shape* shape,
+                 int32_t* convout, void* stream);
+/* convolution.hpp:245 conv_direct_f32 (f32 operands and accumulation) */
+int abed_conv_f32(const float* input, const float* filters, const abed_layer_shape* shape,
+                  float* convout, void* stream);
+/* convolution.hpp:353-387 epilog: out is int8 or f32 per params->output_kind */
+int abed_epilog(const int32_t* convout, abed_dims4 dims, const abed_epilog_params* params,
+                void* out, void* stream);
+
+/* ------------------------------------------------------------ L2 ABED schemes */
+/* checksum.hpp:75-90 gen_filter_checksum: sums[c,r,s] (i32).  filters dims K x C x R x S */
+int abed_gen_filter_checksum(const int8_t* filters, abed_dims4 fdims, int32_t* sums, void* stream);
+/* checksum.hpp:108-122 decompose_checksum_filters: planes = 4 x count raw LE bytes */
+int abed_decompose_checksum_filters(const int32_t* sums, int64_t count, int8_t* planes, void* stream);
+/* checksum.hpp:134-176 conv_checksum_planes: extra = 4 x (N*P*Q) i32 (planes 0-2 unsigned, 3 signed) */
+int abed_conv_checksum_planes(const int8_t* input, const abed_layer_shape* shape,
+                              const int8_t* planes, int32_t* extra, void* stream);
+/* checksum.hpp:179-196 recombine_extra_fmaps: out[i] = e0 + e1<<8 + e2<<16 + e3<<24 (i64) */
+int abed_recombine_extra_fmaps(const int32_t* extra, int64_t count, int64_t* out, void* stream);
+/* checksum.hpp:201-206 conv_filter_checksum: direct i64 route (input conv i32 sums) */
+int abed_conv_filter_checksum(const int8_t* input, const abed_layer_shape* shape,
+                              const int32_t* sums, int64_t* out, void* stream);
+/* checksum.hpp:211-236 fc_verify (synchronous; outcome in host memory) */
+int abed_fc_verify(const int32_t* convout, abed_dims4 dims, const int64_t* extra,
+                   int64_t original_k, abed_verify_outcome* outcome);
+/* checksum.hpp:248-266 gen_input_checksum: sums[c,r,s] (i32) */
+int abed_gen_input_checksum(const int8_t* input, const abed_layer_shape* shape, int32_t* sums,
+                            void* stream);
+/* checksum.hpp:268-272 reduce_all_i64 (result in host memory) */
+int abed_reduce_all_i64(const int32_t* convout, int64_t count, int64_t* result);
+/* checksum.hpp:299-303 reduce_all_wrap32 */
+int abed_reduce_all_wrap32(const int32_t* convout, int64_t count, int32_t* result);
+/* checksum.hpp:275-285 fic_dot */
+int abed_fic_dot(const int32_t* fc_sums, const int32_t* ic_sums, int64_t count, int64_t* result);
+/* checksum.hpp:287-294 fic_verify / :305-312 fic_verify_forced32 */
+int abed_fic_verify(const int32_t* convout, int64_t count, int64_t expected, abed_verify_outcome* outcome);
+int abed_fic_verify_forced32(const int32_t* convout, int64_t count, int64_t expected,
+                             abed_verify_outcome* outcome);
+/* checksum.hpp:319-347 ic_verify_k */
+int abed_ic_verify_k(const int32_t* convout, abed_dims4 dims, const int8_t* filters, abed_dims4 fdims,
+                     const int32_t* ic_sums, abed_verify_outcome* outcome);
+/* checksum.hpp:350-362 ic_batch_checksum: 1 x C x H x W i32 */
+int abed_ic_batch_checksum(const int8_t* input, abed_dims4 dims, int32_t* batch, void* stream);
+/* checksum.hpp:367-396 conv_batch_checksum: 1 x K x P x Q i64 */
+int abed_conv_batch_checksum(const int32_t* batch, const int8_t* filters, const abed_layer_shape* shape,
+                             int64_t* out, void* stream);
+/* checksum.hpp:398-421 ic_batch_verify */
+int abed_ic_batch_verify(const int32_t* convout, abed_dims4 dims, const int64_t* extra,
+                         abed_verify_outcome* outcome);
+/* checksum.hpp:451-468 plan_precision (host only) */
+int abed_plan_precision(const abed_layer_shape* shape, int32_t operand_bits, abed_precision_plan* out);
+
+/* float mode, checksum.hpp:474-595 (f32 tensors, f64 checksum vectors, absolute tau) */
+int abed_float_verify(double lhs, double rhs, double tau, abed_verify_outcome* outcome);
+int abed_filter_checksum_f64(const float* filters, abed_dims4 fdims, double* sums, void* stream);
+int abed_input_checksum_f64(const float* input, const abed_layer_shape* shape, double* sums, void* stream);
+int abed_reduce_all_f64(const float* convout, int64_t count, double* result);
+int abed_fic_dot_f64(const double* a, const double* b, int64_t count, double* result);
+int abed_fic_verify_f32(const float* convout, int64_t count, double expected, double tau,
+                        abed_verify_outcome* outcome);
+int abed_fc_verify_f32(const float* convout, abed_dims4 dims, const float* extra, double tau,
+                       abed_verify_outcome* outcome);
+int abed_ic_verify_k_f32(const float* convout, abed_dims4 dims, const float* filters, abed_dims4 fdims,
+                         const double* ic_sums, double tau, abed_verify_outcome* outcome);
+
+/* checksum.hpp:605-631 fused_conv_epilog.  out: int8/f32 per params.  Taps:
+ * out_checksum (host int64*, NULL = tap off) is the pre-epilog ConvOut sum;
+ * next_shape (NULL = tap off) requests the next layer's input checksum into
+ * next_ic (device i32, 1 x C' x R' x S'), needs an int8 epilog. */
+int abed_fused_conv_epilog(const int8_t* input, const int8_t* filters, const abed_layer_shape* shape,
+                           const abed_epilog_params* params, void* out, int64_t* out_checksum,
+                           const abed_layer_shape* next_shape, int32_t* next_ic, void* stream);
+
+/* ------------------------------------------------------------ L3 faults */
+/* faults.hpp:53-62 flip_bit_inplace on a device tensor of `kind` with `count` elements */
+int abed_flip_bit(void* data, int32_t kind, int64_t count, int64_t flat_index, int32_t bit, void* stream);
+/* faults.hpp:268-274 run_trial: input/filters DEVICE tensors, bias HOST (may be NULL) */
+int abed_run_trial(const abed_layer_shape* shape, const int8_t* input, const int8_t* filters,
+                   int32_t scheme, int32_t target, float scale, const float* bias_host,
+                   int64_t bias_len, int32_t activation, int32_t output_kind, uint64_t seed,
+                   abed_trial_outcome* outcome);
+/* faults.hpp:276-333 run_campaign (deterministic; identical for any jobs / GPU count).
+ * trial_begin/trial_end select a sub-range of trials (batch sharding across GPUs);
+ * pass 0, config->trials for the whole campaign. */
+int abed_run_campaign(const abed_campaign_config* config, int64_t trial_begin, int64_t trial_end,
+                      abed_campaign_report* report);
+
+/* ------------------------------------------------------------ protected conv (hot path)
+ * A plan holds the packed filters (+ FC checksum-digit rows), the filter checksum
+ * and the per-tile verification workspace of one layer.  The activations live in
+ * the packed strip-plane layout; abed_pack_input converts a
+ * reference NCHW tensor, and a previous layer can write it directly
+ * (ABED_OUT_I8_PACKED).  Scheme bits: ABED_CHECK_FC | ABED_CHECK_FIC | ABED_CHECK_IC. */
+enum { ABED_CHECK_FC = 1, ABED_CHECK_FIC = 2, ABED_CHECK_IC = 4 };
+enum {
+  ABED_OUT_NONE = 0, ABED_OUT_I32_NCHW = 1, ABED_OUT_I8_NCHW = 2, ABED_OUT_F32_NCHW = 3,
+  ABED_OUT_I8_PACKED = 4, ABED_OUT_I8_COMPARE = 5
+};
+typedef struct abed_conv_plan abed_conv_plan;
+typedef struct abed_plan_info {
+  int64_t packed_input_bytes;   /* bytes of the packed activation buffer */
+  int32_t block_n, n_tiles, m_tiles, gps, b_resident, n_phase, Hl, Wl;
+  int64_t smem_bytes;
+} abed_plan_info;
+int abed_conv_plan_create(const abed_layer_shape* shape, const int8_t* filters, int32_t checks,
+                          int32_t force_block_n, abed_conv_plan** plan);
+int abed_conv_plan_destroy(abed_conv_plan* plan);
+int abed_conv_plan_info(const abed_conv_plan* plan, abed_plan_info* info);
+int abed_pack_input(const abed_conv_plan* plan, const int8_t* input_nchw, int8_t* packed, void* stream);
+/* Runs the fused kernel (and, with ABED_CHECK_FIC, the input-checksum kernels)
+ * asynchronously.  `next` (may be NULL) gives the consumer layer's plan when
+ * out_mode == ABED_OUT_I8_PACKED.  fault_key/fault_bit: ConvOut single-bit
+ * fault hook (faults.hpp:230-233), fault_key < 0 = none. */
+int abed_conv_plan_run(abed_conv_plan* plan, const int8_t* packed_input, const abed_epilog_params* params,
+                       int32_t out_mode, void* out, const abed_conv_plan* next, int64_t fault_key,
+                       int32_t fault_bit, void* stream);
+/* Reduces the run's per-tile records into reference VerifyOutcomes (device side),
+ * asynchronously; outcome_dev points to 3 device abed_verify_outcome {FC, FIC, IC}. */
+int abed_conv_plan_finalize(abed_conv_plan* plan, abed_verify_outcome* outcome_dev, void* stream);
+/* duplication baseline: mismatch count of the last OUT_I8_COMPARE run (synchronous) */
+int abed_conv_plan_compare_count(abed_conv_plan* plan, int64_t* count);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ABED_B200_H */

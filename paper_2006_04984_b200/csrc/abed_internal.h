@@ -1,0 +1,71 @@
+// Internal declarations shared by the .cu translation units of libabed_b200.so.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include "../../include/abed_b200.h"
+#include "conv_tc.cuh"
+
+namespace abed_host {
+
+// exceptions carrying the reference's exception class as a status code
+struct AbedError : std::runtime_error {
+  int code;
+  AbedError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] inline void throw_invalid(const std::string& m) { throw AbedError(ABED_ERR_INVALID_ARGUMENT, m); }
+[[noreturn]] inline void throw_range(const std::string& m) { throw AbedError(ABED_ERR_OUT_OF_RANGE, m); }
+inline void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw AbedError(ABED_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// plan.cu
+abed_dev::ActGeom make_geom(const abed_layer_shape& s);
+int geom_strip_pix(const abed_dev::ActGeom& g);
+int64_t geom_packed_bytes(const abed_dev::ActGeom& g);
+bool choose_tiling(const abed_dev::ActGeom& g, bool fc, int force_block_n, abed_dev::ConvTcParams& p);
+int num_sms();
+
+__global__ void pack_input_kernel(const int8_t* x, abed_dev::ActGeom g, int8_t* out);
+__global__ void pack_filters_kernel(const int8_t* f, abed_dev::ActGeom g, int block_n, int block_n_tot,
+                                    int n_tiles, int gps, int k_stages, int fc, int8_t* out);
+__global__ void filter_sum_kernel(const int8_t* f, int64_t K, int64_t crs, int32_t* sums);
+__global__ void batch_sum_packed_kernel(const int8_t* act, abed_dev::ActGeom g, int32_t* bsum);
+__global__ void box_sum_dot_kernel(const int32_t* bsum, abed_dev::ActGeom g, const int32_t* fsum,
+                                   int32_t* ic_out, unsigned long long* fic_rhs);
+__global__ void fc_finalize_rec_kernel(const int64_t* rec, int m_tiles, int P, int Q, abed_verify_outcome* out);
+__global__ void fc_finalize_part_kernel(const int64_t* part, abed_dev::ActGeom g, int n_tiles,
+                                        unsigned long long* scratch);
+__global__ void fc_finalize_part2_kernel(const int64_t* part, abed_dev::ActGeom g, int n_tiles,
+                                         const unsigned long long* scratch, abed_verify_outcome* out);
+__global__ void fic_finalize_kernel(const int64_t* part, int n, const unsigned long long* rhs_p,
+                                    abed_verify_outcome* out);
+__global__ void ic_finalize_kernel(const unsigned long long* ksum, const int8_t* f, const int32_t* ic, int64_t K,
+                                   int64_t crs, abed_verify_outcome* out);
+
+// conv_tc.cu
+uint32_t conv_tc_smem_bytes(const abed_dev::ConvTcParams& p);
+cudaError_t conv_tc_launch(const abed_dev::ConvTcParams& p, int num_sms, cudaStream_t stream);
+
+}  // namespace abed_host
+
+// opaque plan (C ABI handle)
+struct abed_conv_plan {
+  abed_layer_shape shape;
+  abed_dev::ActGeom g;
+  abed_dev::ConvTcParams base;  // tiling + tap tables; pointers filled per run
+  int checks;
+  int8_t* d_wpk = nullptr;      // packed B blocks
+  int8_t* d_filters = nullptr;  // KCRS copy (IC verify reads filter storage)
+  int32_t* d_fsum = nullptr;    // filter checksum (c,r,s) order, i32
+  int32_t* d_ic = nullptr;      // input checksum of the last run (c,r,s)
+  int32_t* d_bsum = nullptr;    // batch-sum image [phase][c16*16][Hl*Wl]
+  int64_t* d_fc_rec = nullptr;
+  int64_t* d_fc_part = nullptr;
+  int64_t* d_fic_part = nullptr;
+  unsigned long long* d_acc = nullptr;  // [0]=fic rhs, [1]=cmp count, [2..3]=fc scratch, [4..4+K) ic sums
+  float* d_zero_bias = nullptr;
+};

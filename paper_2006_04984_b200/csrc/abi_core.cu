@@ -1,0 +1,327 @@
+// C ABI: library utilities, the protected-conv plan (hot path) and the
+// reference-facing convolution entry points built on it.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "abed_internal.h"
+
+using namespace abed_host;
+using abed_dev::ActGeom;
+using abed_dev::ConvTcParams;
+
+namespace abed_host {
+thread_local std::string g_last_error;
+
+int set_error(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+template <typename Fn>
+int guarded(Fn&& fn) {
+  try {
+    fn();
+    return ABED_OK;
+  } catch (const AbedError& e) {
+    return set_error(e.code, e.what());
+  } catch (const std::exception& e) {
+    return set_error(ABED_ERR_RUNTIME, e.what());
+  }
+}
+
+void require_device() {
+  static int ok = -1;
+  if (ok < 0) {
+    int dev = 0, n = 0;
+    ok = 0;
+    if (cudaGetDeviceCount(&n) == cudaSuccess && n > 0 && cudaGetDevice(&dev) == cudaSuccess) {
+      int major = 0;
+      cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+      ok = major == 10 ? 1 : 0;
+    }
+  }
+  if (!ok) throw AbedError(ABED_ERR_NO_DEVICE, "abed: no sm_100 (B200) device available; the library has no host fallback");
+}
+
+int grid_for(int64_t n, int threads = 256) {
+  int64_t g = (n + threads - 1) / threads;
+  const int cap = num_sms() * 16;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+void validate_shape(const abed_layer_shape& s) {
+  if (s.n < 1 || s.c < 1 || s.h < 1 || s.w < 1 || s.k < 1 || s.r < 1 || s.s < 1)
+    throw_invalid("LayerShape: extents must be >= 1");
+  if (s.stride_h < 1 || s.stride_w < 1) throw_invalid("LayerShape: strides must be >= 1");
+  if (s.pad_h < 0 || s.pad_w < 0) throw_invalid("LayerShape: pads must be >= 0");
+  if (s.r > s.h + 2 * s.pad_h || s.s > s.w + 2 * s.pad_w)
+    throw_invalid("LayerShape: filter exceeds padded input");
+  if (s.p != (s.h + 2 * s.pad_h - s.r) / s.stride_h + 1 || s.q != (s.w + 2 * s.pad_w - s.s) / s.stride_w + 1)
+    throw_invalid("LayerShape: p/q inconsistent with extents");
+}
+
+// ---------------------------------------------------------------- plan
+abed_conv_plan* plan_create(const abed_layer_shape& shape, const int8_t* filters, int checks, int force_bn) {
+  require_device();
+  validate_shape(shape);
+  if (shape.c * shape.r * shape.s > 65536)
+    throw_invalid("conv: CRS > 65536 exceeds the int32 accumulator plan");
+  if (shape.r * shape.s > abed_dev::kMaxTaps) throw_invalid("conv: filters with more than 64 taps are not supported");
+  if (shape.k > (int64_t(1) << 24)) throw_invalid("gen_filter_checksum: K too large for i32 checksums");
+  auto* pl = new abed_conv_plan();
+  try {
+    pl->shape = shape;
+    pl->checks = checks;
+    pl->g = make_geom(shape);
+    const ActGeom& g = pl->g;
+    ConvTcParams& p = pl->base;
+    std::memset(&p, 0, sizeof(p));
+    if (!choose_tiling(g, (checks & ABED_CHECK_FC) != 0, force_bn, p))
+      throw_invalid("conv: no tiling fits shared memory for this layer");
+    p.plane_len = g.plane_len;
+    p.n_phase = g.n_phase;
+    p.c16 = g.c16;
+    p.strip_pix = geom_strip_pix(g);
+    p.ntaps = g.r * g.s;
+    for (int r = 0; r < g.r; ++r)
+      for (int s = 0; s < g.s; ++s) {
+        const int t = r * g.s + s;
+        p.tap_phase[t] = (r % g.sh) * g.nph_w + (s % g.sw);
+        p.tap_shift[t] = (r / g.sh) * g.Wl + (s / g.sw);
+      }
+    p.m_total = g.m_total;
+    p.m_tiles = g.m_tiles;
+    p.Hl = g.Hl; p.Wl = g.Wl; p.P = g.p; p.Q = g.q; p.N = g.n; p.K = g.k;
+    p.fault_key = -1;
+
+    const int64_t crs = shape.c * shape.r * shape.s;
+    const size_t wpk_bytes = (size_t)p.n_tiles * p.k_stages * p.b_stage_bytes;
+    cuda_check(cudaMalloc(&pl->d_wpk, wpk_bytes), "cudaMalloc(wpk)");
+    cuda_check(cudaMalloc(&pl->d_filters, (size_t)(shape.k * crs)), "cudaMalloc(filters)");
+    cuda_check(cudaMemcpy(pl->d_filters, filters, (size_t)(shape.k * crs), cudaMemcpyDeviceToDevice), "copy filters");
+    cuda_check(cudaMalloc(&pl->d_fsum, crs * 4), "cudaMalloc(fsum)");
+    cuda_check(cudaMalloc(&pl->d_ic, crs * 4), "cudaMalloc(ic)");
+    cuda_check(cudaMalloc(&pl->d_bsum, (size_t)g.n_phase * g.c16 * 16 * g.Hl * g.Wl * 4), "cudaMalloc(bsum)");
+    const int64_t tiles = (int64_t)p.n_tiles * p.m_tiles;
+    cuda_check(cudaMalloc(&pl->d_fc_rec, tiles * 4 * 8), "cudaMalloc(fc_rec)");
+    cuda_check(cudaMalloc(&pl->d_fic_part, tiles * 8), "cudaMalloc(fic_part)");
+    if (p.n_tiles > 1) cuda_check(cudaMalloc(&pl->d_fc_part, (size_t)p.n_tiles * p.m_tiles * 128 * 2 * 8), "cudaMalloc(fc_part)");
+    cuda_check(cudaMalloc(&pl->d_acc, (4 + shape.k) * 8), "cudaMalloc(acc)");
+    cuda_check(cudaMemset(pl->d_acc, 0, (4 + shape.k) * 8), "memset acc");
+    cuda_check(cudaMalloc(&pl->d_zero_bias, shape.k * 4), "cudaMalloc(bias)");
+    cuda_check(cudaMemset(pl->d_zero_bias, 0, shape.k * 4), "memset bias");
+
+    const int64_t rows = (int64_t)p.n_tiles * p.k_stages * p.ntaps * p.gps * p.block_n_tot;
+    pack_filters_kernel<<<grid_for(rows), 256>>>(filters, g, p.block_n, p.block_n_tot, p.n_tiles, p.gps,
+                                                 p.k_stages, (checks & ABED_CHECK_FC) ? 1 : 0, pl->d_wpk);
+    cuda_check(cudaGetLastError(), "pack_filters");
+    filter_sum_kernel<<<grid_for(crs), 256>>>(filters, shape.k, crs, pl->d_fsum);
+    cuda_check(cudaGetLastError(), "filter_sum");
+    cuda_check(cudaDeviceSynchronize(), "plan_create sync");
+  } catch (...) {
+    abed_conv_plan_destroy(pl);
+    throw;
+  }
+  return pl;
+}
+
+void plan_run(abed_conv_plan* pl, const int8_t* packed, const abed_epilog_params* ep, int out_mode, void* out,
+              const abed_conv_plan* next, int64_t fault_key, int fault_bit, cudaStream_t st) {
+  ConvTcParams p = pl->base;
+  p.act = packed;
+  p.wpk = pl->d_wpk;
+  p.out_mode = out_mode;
+  p.out = out;
+  p.check = pl->checks;
+  if (ep) {
+    if (!std::isfinite(ep->scale)) throw_invalid("epilog: non-finite scale");
+    if (ep->bias && ep->bias_len != pl->shape.k) throw_invalid("epilog: bias length must equal the channel count");
+    p.scale = ep->scale;
+    p.bias = ep->bias ? ep->bias : pl->d_zero_bias;
+    p.relu = ep->activation == ABED_RELU ? 1 : 0;
+  } else {
+    p.scale = 1.0f;
+    p.bias = pl->d_zero_bias;
+    p.relu = 0;
+  }
+  if (out_mode == ABED_OUT_I8_PACKED || out_mode == ABED_OUT_I8_COMPARE) {
+    if (next) {
+      const ActGeom& o = next->g;
+      if (o.c != pl->g.k || o.h != pl->g.p || o.w != pl->g.q || o.n != pl->g.n)
+        throw_invalid("conv plan: next layer input does not match this layer's output");
+      p.o_plane_len = o.plane_len; p.o_Hl = o.Hl; p.o_Wl = o.Wl; p.o_ph = o.ph; p.o_pw = o.pw;
+      p.o_sh = o.sh; p.o_sw = o.sw; p.o_nph_w = o.nph_w; p.o_c16 = o.c16;
+    } else {
+      // identity consumer geometry: 1x1, stride 1, pad 0
+      abed_layer_shape s1{pl->shape.n, pl->shape.k, pl->shape.p, pl->shape.q, 1, 1, 1, 1, 1, 0, 0, pl->shape.p, pl->shape.q};
+      const ActGeom o = make_geom(s1);
+      p.o_plane_len = o.plane_len; p.o_Hl = o.Hl; p.o_Wl = o.Wl; p.o_ph = 0; p.o_pw = 0;
+      p.o_sh = 1; p.o_sw = 1; p.o_nph_w = 1; p.o_c16 = o.c16;
+    }
+  }
+  p.fc_rec = pl->d_fc_rec;
+  p.fc_part = pl->d_fc_part;
+  p.fic_part = pl->d_fic_part;
+  p.ic_sum = pl->d_acc + 4;
+  p.cmp_count = pl->d_acc + 1;
+  p.fault_key = fault_key;
+  p.fault_bit = fault_bit;
+  if (pl->checks & ABED_CHECK_IC) cuda_check(cudaMemsetAsync(pl->d_acc + 4, 0, pl->shape.k * 8, st), "memset ic");
+  if (out_mode == ABED_OUT_I8_COMPARE) cuda_check(cudaMemsetAsync(pl->d_acc + 1, 0, 8, st), "memset cmp");
+  if (pl->checks & (ABED_CHECK_FIC | ABED_CHECK_IC)) {
+    // input checksum of the pristine input, ahead of the convolution (FR option)
+    const ActGeom& g = pl->g;
+    cuda_check(cudaMemsetAsync(pl->d_acc, 0, 8, st), "memset rhs");
+    const int64_t cnt = (int64_t)g.n_phase * g.c16 * g.Hl * g.Wl;
+    batch_sum_packed_kernel<<<grid_for(cnt), 256, 0, st>>>(packed, g, pl->d_bsum);
+    box_sum_dot_kernel<<<g.c, 256, 0, st>>>(pl->d_bsum, g, pl->d_fsum, pl->d_ic, pl->d_acc);
+    cuda_check(cudaGetLastError(), "input checksum");
+  }
+  cuda_check(conv_tc_launch(p, num_sms(), st), "conv_i8_tc launch");
+}
+
+void plan_finalize(abed_conv_plan* pl, abed_verify_outcome* out_dev, cudaStream_t st) {
+  const ConvTcParams& p = pl->base;
+  const ActGeom& g = pl->g;
+  if (pl->checks & ABED_CHECK_FC) {
+    if (p.n_tiles == 1) {
+      fc_finalize_rec_kernel<<<1, 256, 0, st>>>(pl->d_fc_rec, p.m_tiles, g.p, g.q, out_dev + 0);
+    } else {
+      unsigned long long init[2] = {0ull, ~0ull};
+      cuda_check(cudaMemcpyAsync(pl->d_acc + 2, init, 16, cudaMemcpyHostToDevice, st), "fc scratch");
+      fc_finalize_part_kernel<<<grid_for(g.m_total), 256, 0, st>>>(pl->d_fc_part, g, p.n_tiles, pl->d_acc + 2);
+      fc_finalize_part2_kernel<<<1, 32, 0, st>>>(pl->d_fc_part, g, p.n_tiles, pl->d_acc + 2, out_dev + 0);
+    }
+  }
+  if (pl->checks & ABED_CHECK_FIC)
+    fic_finalize_kernel<<<1, 256, 0, st>>>(pl->d_fic_part, p.n_tiles * p.m_tiles, pl->d_acc, out_dev + 1);
+  if (pl->checks & ABED_CHECK_IC)
+    ic_finalize_kernel<<<1, 256, 0, st>>>(pl->d_acc + 4, pl->d_filters, pl->d_ic, pl->shape.k,
+                                          pl->shape.c * pl->shape.r * pl->shape.s, out_dev + 2);
+  cuda_check(cudaGetLastError(), "finalize");
+}
+
+}  // namespace abed_host
+
+extern "C" {
+
+const char* abed_last_error(void) { return g_last_error.c_str(); }
+int abed_version(void) { return 1; }
+int abed_device_check(void) {
+  return guarded([] { require_device(); });
+}
+int abed_malloc(void** dptr, size_t bytes) {
+  return guarded([&] { require_device(); cuda_check(cudaMalloc(dptr, bytes ? bytes : 16), "cudaMalloc"); });
+}
+int abed_free(void* dptr) {
+  return guarded([&] { cuda_check(cudaFree(dptr), "cudaFree"); });
+}
+int abed_memcpy_h2d(void* dst, const void* src, size_t bytes) {
+  return guarded([&] { cuda_check(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice), "h2d"); });
+}
+int abed_memcpy_d2h(void* dst, const void* src, size_t bytes) {
+  return guarded([&] { cuda_check(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost), "d2h"); });
+}
+int abed_memset(void* dptr, int value, size_t bytes) {
+  return guarded([&] { cuda_check(cudaMemset(dptr, value, bytes), "memset"); });
+}
+int abed_synchronize(void) {
+  return guarded([] { cuda_check(cudaDeviceSynchronize(), "synchronize"); });
+}
+
+int abed_layer_shape_make(int64_t n, int64_t c, int64_t h, int64_t w, int64_t k, int64_t r, int64_t s,
+                          int64_t stride_h, int64_t stride_w, int64_t pad_h, int64_t pad_w,
+                          abed_layer_shape* out) {
+  return guarded([&] {
+    // tensor.hpp:178-193
+    if (n < 1 || c < 1 || h < 1 || w < 1 || k < 1 || r < 1 || s < 1) throw_invalid("LayerShape: extents must be >= 1");
+    if (stride_h < 1 || stride_w < 1) throw_invalid("LayerShape: strides must be >= 1");
+    if (pad_h < 0 || pad_w < 0) throw_invalid("LayerShape: pads must be >= 0");
+    if (r > h + 2 * pad_h || s > w + 2 * pad_w) throw_invalid("LayerShape: filter exceeds padded input");
+    *out = abed_layer_shape{n, c, h, w, k, r, s, stride_h, stride_w, pad_h, pad_w,
+                            (h + 2 * pad_h - r) / stride_h + 1, (w + 2 * pad_w - s) / stride_w + 1};
+  });
+}
+
+// ---------------------------------------------------------------- plan API
+int abed_conv_plan_create(const abed_layer_shape* shape, const int8_t* filters, int32_t checks,
+                          int32_t force_block_n, abed_conv_plan** plan) {
+  return guarded([&] { *plan = plan_create(*shape, filters, checks, force_block_n); });
+}
+int abed_conv_plan_destroy(abed_conv_plan* pl) {
+  if (!pl) return ABED_OK;
+  cudaFree(pl->d_wpk); cudaFree(pl->d_filters); cudaFree(pl->d_fsum); cudaFree(pl->d_ic);
+  cudaFree(pl->d_bsum); cudaFree(pl->d_fc_rec); cudaFree(pl->d_fc_part); cudaFree(pl->d_fic_part);
+  cudaFree(pl->d_acc); cudaFree(pl->d_zero_bias);
+  delete pl;
+  return ABED_OK;
+}
+int abed_conv_plan_info(const abed_conv_plan* pl, abed_plan_info* info) {
+  return guarded([&] {
+    info->packed_input_bytes = geom_packed_bytes(pl->g);
+    info->block_n = pl->base.block_n;
+    info->n_tiles = pl->base.n_tiles;
+    info->m_tiles = pl->base.m_tiles;
+    info->gps = pl->base.gps;
+    info->b_resident = pl->base.b_resident;
+    info->n_phase = pl->g.n_phase;
+    info->Hl = pl->g.Hl;
+    info->Wl = pl->g.Wl;
+    info->smem_bytes = conv_tc_smem_bytes(pl->base);
+  });
+}
+int abed_pack_input(const abed_conv_plan* pl, const int8_t* input, int8_t* packed, void* stream) {
+  return guarded([&] {
+    const int64_t n16 = geom_packed_bytes(pl->g) / 16;
+    pack_input_kernel<<<grid_for(n16), 256, 0, (cudaStream_t)stream>>>(input, pl->g, packed);
+    cuda_check(cudaGetLastError(), "pack_input");
+  });
+}
+int abed_conv_plan_run(abed_conv_plan* pl, const int8_t* packed, const abed_epilog_params* params, int32_t out_mode,
+                       void* out, const abed_conv_plan* next, int64_t fault_key, int32_t fault_bit, void* stream) {
+  return guarded([&] { plan_run(pl, packed, params, out_mode, out, next, fault_key, fault_bit, (cudaStream_t)stream); });
+}
+int abed_conv_plan_finalize(abed_conv_plan* pl, abed_verify_outcome* outcome_dev, void* stream) {
+  return guarded([&] { plan_finalize(pl, outcome_dev, (cudaStream_t)stream); });
+}
+int abed_conv_plan_compare_count(abed_conv_plan* pl, int64_t* count) {
+  return guarded([&] {
+    unsigned long long c = 0;
+    cuda_check(cudaMemcpy(&c, pl->d_acc + 1, 8, cudaMemcpyDeviceToHost), "cmp count");
+    *count = (int64_t)c;
+  });
+}
+
+// ---------------------------------------------------------------- conv_direct
+int abed_conv_i8(const int8_t* input, const int8_t* filters, const abed_layer_shape* shape, int32_t* convout,
+                 void* stream) {
+  return guarded([&] {
+    validate_shape(*shape);
+    if (shape->c * shape->r * shape->s > 65536)
+      throw_invalid("conv_direct: CRS > 65536 exceeds the int32 accumulator plan");
+    cudaStream_t st = (cudaStream_t)stream;
+    abed_conv_plan* pl = plan_create(*shape, filters, 0, 0);
+    int8_t* packed = nullptr;
+    try {
+      cuda_check(cudaMalloc(&packed, geom_packed_bytes(pl->g)), "cudaMalloc(packed)");
+      const int64_t n16 = geom_packed_bytes(pl->g) / 16;
+      pack_input_kernel<<<grid_for(n16), 256, 0, st>>>(input, pl->g, packed);
+      plan_run(pl, packed, nullptr, ABED_OUT_I32_NCHW, convout, nullptr, -1, 0, st);
+      cuda_check(cudaStreamSynchronize(st), "conv_i8 sync");
+    } catch (...) {
+      cudaFree(packed);
+      abed_conv_plan_destroy(pl);
+      throw;
+    }
+    cudaFree(packed);
+    abed_conv_plan_destroy(pl);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,103 @@
+// Shared host/device definitions for the tcgen05 implicit-GEMM convolution.
+//
+// Packed activation layout ("strip planes").  The reference keeps NCHW int8
+// (tensor.hpp:68-70).  On the device an activation tensor consumed by a conv
+// is stored as planes of 16-byte pixels:
+//
+//   plane (phase, g) : pixel t in [0, plane_len)  ->  16 channels g*16..g*16+15
+//   address          : act + ((phase * c16 + g) * plane_len + t) * 16
+//
+// Pixel t = (n * Hl + i) * Wl + j is sub-row i / sub-column j of image n in the
+// stride phase (a, b); it holds input pixel (h, w) = (i*sh + a - pad_h,
+// j*sw + b - pad_w), or zero outside the image.  For a stride-1 conv there is
+// one phase and Hl = H + pad_h, Wl = W + pad_w: the zero halo between two rows
+// (images) is shared, so every filter tap (r, s) is a constant pixel shift
+// r*Wl + s of the whole GEMM row range.  This is what lets one contiguous strip
+// of 128 + max_shift pixels per plane feed all R*S taps of a 128-row M tile
+// straight from shared memory (SWIZZLE_NONE K-major UMMA operand: rows 16 B
+// apart, so a tap is a descriptor start-address offset).
+//
+// GEMM view: M = output pixels in this "M-space" (m = (n*Hl + p)*Wl + q, valid
+// iff p < P and q < Q), N = output channels, K = taps x channels.
+#pragma once
+#include <cstdint>
+
+namespace abed_dev {
+
+constexpr int kMaxTaps = 64;
+constexpr int kBlockM = 128;
+constexpr int kStages = 4;       // activation/filter stage ring depth
+constexpr int kStages_host = kStages;
+constexpr int kThreads = 192;     // 6 warps: producer, MMA, 4 x epilogue
+
+enum OutMode : int {
+  OUT_NONE = 0,        // checks only (no activation written)
+  OUT_I32_NCHW = 1,    // raw ConvOut, reference layout N x K x P x Q
+  OUT_I8_NCHW = 2,     // epilog -> int8, reference layout
+  OUT_F32_NCHW = 3,    // epilog -> f32, reference layout
+  OUT_I8_PACKED = 4,   // epilog -> int8 straight into the next layer's strip planes
+  OUT_I8_COMPARE = 5,  // epilog -> int8 compared against `out` (duplication check)
+};
+
+enum CheckBits : int {
+  CHECK_FC = 1,   // filter checksum columns ride in B (checksum.hpp:211 fc_verify)
+  CHECK_FIC = 2,  // full-output int64 sum per tile (checksum.hpp:287 fic_verify)
+  CHECK_IC = 4,   // per-output-channel int64 sums (checksum.hpp:319 ic_verify_k)
+};
+
+// Geometry of one conv layer in packed form (computed on the host).
+struct ActGeom {
+  int n, c, h, w;          // logical input (reference LayerShape n,c,h,w)
+  int k, r, s;             // filters
+  int sh, sw, ph, pw;      // stride / pad
+  int p, q;                // output extents
+  int nph_h, nph_w;        // stride phases actually touched by taps
+  int n_phase;             // nph_h * nph_w
+  int c16;                 // channel groups of 16 (even, zero padded)
+  int Hl, Wl;              // M-space rows per image / pixels per row
+  int max_shift;           // largest tap pixel shift
+  int m_tiles;             // ceil(m_total / 128)
+  int64_t m_total;         // n * Hl * Wl
+  int64_t plane_len;       // pixels per plane (covers the last strip)
+};
+
+struct ConvTcParams {
+  // ---- A operand
+  const int8_t* act;
+  int64_t plane_len;
+  int n_phase, c16, gps, k_stages, strip_pix, ntaps;
+  int tap_phase[kMaxTaps];
+  int tap_shift[kMaxTaps];
+  // ---- B operand (packed filters, see pack_filters in conv_tc.cu)
+  const int8_t* wpk;
+  int block_n;       // output channels per N tile
+  int block_n_tot;   // + 16 checksum rows when CHECK_FC
+  int n_tiles;
+  int b_resident;    // 1: a CTA keeps its N tile's whole B in smem
+  uint32_t b_stage_bytes;
+  // ---- geometry
+  int64_t m_total;
+  int m_tiles, Hl, Wl, P, Q, N, K;
+  // ---- epilogue
+  int out_mode;
+  void* out;
+  const float* bias;  // K entries (device)
+  float scale;
+  int relu;
+  // next-layer packed output geometry (OUT_I8_PACKED)
+  int64_t o_plane_len;
+  int o_Hl, o_Wl, o_ph, o_pw, o_sh, o_sw, o_nph_w, o_c16;
+  // ---- checks
+  int check;
+  int64_t* fc_rec;    // [n_tiles*m_tiles][4] {count, first key, lhs, rhs}   (n_tiles == 1)
+  int64_t* fc_part;   // [n_tiles][m_tiles*128][2] {sum_k, extra}            (n_tiles  > 1)
+  int64_t* fic_part;  // [n_tiles*m_tiles] per-tile output sums
+  unsigned long long* ic_sum;  // [K] per-channel output sums (atomic, integer => deterministic)
+  unsigned long long* cmp_count;  // OUT_I8_COMPARE mismatch count
+  // ---- fault hook (ConvOut target): flip `fault_bit` of output element
+  // (n,k,p,q) = fault_key in reference flat order before checks and epilog.
+  int64_t fault_key;  // -1 = none
+  int fault_bit;
+};
+
+}  // namespace abed_dev

@@ -1,0 +1,415 @@
+// Layer planning and the HBM-bound helper kernels of the protected int8 conv:
+//   * geometry of the packed strip-plane activation layout (conv_tc.cuh)
+//   * pack_input:   reference NCHW int8  -> strip planes       (boundary, once per call)
+//   * pack_filters: reference KCRS int8  -> UMMA B blocks + FC checksum-digit rows
+//                   (checksum.hpp:75 gen_filter_checksum, :108 decompose, offline)
+//   * batch_sum / box_sum_dot: input checksum and FIC right-hand side
+//                   (checksum.hpp:248 gen_input_checksum, :275 fic_dot, :350 ic_batch_checksum)
+//   * finalize kernels turning per-tile records into a reference VerifyOutcome
+//                   (checksum.hpp:211-236 fc_verify, :287-294 fic_verify, :319-347 ic_verify_k)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+
+#include "abed_internal.h"
+
+namespace abed_host {
+
+using abed_dev::ActGeom;
+using abed_dev::ConvTcParams;
+
+static inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+ActGeom make_geom(const abed_layer_shape& s) {
+  ActGeom g{};
+  g.n = (int)s.n; g.c = (int)s.c; g.h = (int)s.h; g.w = (int)s.w;
+  g.k = (int)s.k; g.r = (int)s.r; g.s = (int)s.s;
+  g.sh = (int)s.stride_h; g.sw = (int)s.stride_w; g.ph = (int)s.pad_h; g.pw = (int)s.pad_w;
+  g.p = (int)s.p; g.q = (int)s.q;
+  g.nph_h = std::min(g.sh, g.r);
+  g.nph_w = std::min(g.sw, g.s);
+  g.n_phase = g.nph_h * g.nph_w;
+  g.c16 = (int)ceil_div(g.c, 16);
+  if (g.c16 & 1) g.c16 += 1;  // one MMA consumes 32 channels
+  auto extent = [](int P, int H, int R, int st, int pad, int nph) {
+    auto zero_lead = [&](int a) { return pad > a ? (int)ceil_div(pad - a, st) : 0; };
+    int L = P;
+    for (int a = 0; a < nph; ++a)
+      if (pad + H - 1 - a >= 0) L = std::max(L, 1 + (pad + H - 1 - a) / st);
+    for (int r = 0; r < R; ++r) L = std::max(L, P + r / st - zero_lead(r % st));
+    return L;
+  };
+  g.Hl = extent(g.p, g.h, g.r, g.sh, g.ph, g.nph_h);
+  g.Wl = extent(g.q, g.w, g.s, g.sw, g.pw, g.nph_w);
+  g.max_shift = ((g.r - 1) / g.sh) * g.Wl + (g.s - 1) / g.sw;
+  g.m_total = (int64_t)g.n * g.Hl * g.Wl;
+  g.m_tiles = (int)ceil_div(g.m_total, abed_dev::kBlockM);
+  const int strip = (int)((abed_dev::kBlockM + g.max_shift + 7) / 8 * 8);
+  g.plane_len = (int64_t)(g.m_tiles - 1) * abed_dev::kBlockM + strip;
+  return g;
+}
+
+int geom_strip_pix(const ActGeom& g) { return (abed_dev::kBlockM + g.max_shift + 7) / 8 * 8; }
+
+int64_t geom_packed_bytes(const ActGeom& g) {
+  return (int64_t)g.n_phase * g.c16 * g.plane_len * 16;
+}
+
+// ---------------------------------------------------------------------------
+// pack_input: one thread per (plane, pixel t); 16 channel bytes gathered from
+// NCHW, zero outside the image (padding halo) and beyond the last image.
+// ---------------------------------------------------------------------------
+__global__ void pack_input_kernel(const int8_t* __restrict__ x, ActGeom g, int8_t* __restrict__ out) {
+  const int64_t total = (int64_t)g.n_phase * g.c16 * g.plane_len;
+  const int64_t HlWl = (int64_t)g.Hl * g.Wl;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = idx % g.plane_len;
+    const int64_t plane = idx / g.plane_len;
+    const int grp = (int)(plane % g.c16);
+    const int phase = (int)(plane / g.c16);
+    uint32_t w4[4] = {0, 0, 0, 0};
+    if (t < g.m_total) {
+      const int n = (int)(t / HlWl);
+      const int64_t rem = t - n * HlWl;
+      const int i = (int)(rem / g.Wl), j = (int)(rem % g.Wl);
+      const int a = phase / g.nph_w, b = phase % g.nph_w;
+      const int hh = i * g.sh + a - g.ph, ww = j * g.sw + b - g.pw;
+      if (hh >= 0 && hh < g.h && ww >= 0 && ww < g.w) {
+        for (int e = 0; e < 16; ++e) {
+          const int c = grp * 16 + e;
+          if (c < g.c) {
+            const uint8_t v = (uint8_t)x[(((int64_t)n * g.c + c) * g.h + hh) * g.w + ww];
+            w4[e >> 2] |= (uint32_t)v << (8 * (e & 3));
+          }
+        }
+      }
+    }
+    reinterpret_cast<uint4*>(out)[idx] = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// pack_filters: B blocks [nt][ks][tap][gl][row][16B]; rows >= block_n hold the
+// balanced base-256 digits of the per-N-tile filter checksum
+// fsum_nt[c,r,s] = sum_{k in tile} f[k,c,r,s]  (checksum.hpp:75-90 restricted to
+// the tile; the per-tile extras add up to the reference's extra fmap exactly).
+// ---------------------------------------------------------------------------
+__global__ void pack_filters_kernel(const int8_t* __restrict__ f, ActGeom g, int block_n, int block_n_tot,
+                                    int n_tiles, int gps, int k_stages, int fc, int8_t* __restrict__ out) {
+  const int ntaps = g.r * g.s;
+  const int64_t rows_total = (int64_t)n_tiles * k_stages * ntaps * gps * block_n_tot;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < rows_total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    int64_t rem = idx;
+    const int row = (int)(rem % block_n_tot); rem /= block_n_tot;
+    const int gl = (int)(rem % gps); rem /= gps;
+    const int tap = (int)(rem % ntaps); rem /= ntaps;
+    const int ks = (int)(rem % k_stages); rem /= k_stages;
+    const int nt = (int)rem;
+    const int r = tap / g.s, s = tap % g.s;
+    const int cbase = (ks * gps + gl) * 16;
+    int8_t vals[16];
+    if (row < block_n) {
+      const int k = nt * block_n + row;
+      for (int e = 0; e < 16; ++e) {
+        const int c = cbase + e;
+        vals[e] = (k < g.k && c < g.c) ? f[(((int64_t)k * g.c + c) * g.r + r) * g.s + s] : (int8_t)0;
+      }
+    } else {
+      const int digit = row - block_n;
+      for (int e = 0; e < 16; ++e) {
+        const int c = cbase + e;
+        int32_t sum = 0;
+        if (fc && digit < 3 && c < g.c) {
+          const int k_end = min(g.k, (nt + 1) * block_n);
+          for (int k = nt * block_n; k < k_end; ++k) sum += f[(((int64_t)k * g.c + c) * g.r + r) * g.s + s];
+          // balanced digits: sum = d0 + 256 d1 + 65536 d2, each in [-128, 127]
+          int32_t d0 = ((sum + 128) & 0xFF) - 128;
+          int32_t rest = (sum - d0) / 256;
+          int32_t d1 = ((rest + 128) & 0xFF) - 128;
+          int32_t d2 = (rest - d1) / 256;
+          sum = digit == 0 ? d0 : digit == 1 ? d1 : d2;
+        } else {
+          sum = 0;
+        }
+        vals[e] = (int8_t)sum;
+      }
+    }
+    uint32_t w4[4] = {0, 0, 0, 0};
+    for (int e = 0; e < 16; ++e) w4[e >> 2] |= (uint32_t)(uint8_t)vals[e] << (8 * (e & 3));
+    reinterpret_cast<uint4*>(out)[idx] = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+  }
+}
+
+// filter checksum in reference (c,r,s) order, i32 (checksum.hpp:75-90)
+__global__ void filter_sum_kernel(const int8_t* __restrict__ f, int64_t K, int64_t crs, int32_t* __restrict__ sums) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < crs; i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t acc = 0;
+    for (int64_t k = 0; k < K; ++k) acc += f[k * crs + i];
+    sums[i] = acc;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Input checksum of the packed input.  Stage 1 (HBM-bound, reads the input
+// once): batch sum B[phase][c][i][j] = sum_n plane[(n*Hl+i)*Wl+j] (this is the
+// ICBatch checksum image, checksum.hpp:350-362, in packed coordinates).
+// Stage 2: ic[c,r,s] = box sum of B over i in [r/sh, r/sh+P), j in [s/sw, s/sw+Q)
+// in phase (r%sh, s%sw) -- every window position of gen_input_checksum
+// (checksum.hpp:248-266) -- fused with the FIC dot against the filter checksum.
+// ---------------------------------------------------------------------------
+__global__ void batch_sum_packed_kernel(const int8_t* __restrict__ act, ActGeom g, int32_t* __restrict__ bsum) {
+  const int64_t HlWl = (int64_t)g.Hl * g.Wl;
+  const int64_t total = (int64_t)g.n_phase * g.c16 * HlWl;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t pix = idx % HlWl;
+    const int64_t plane = idx / HlWl;
+    const uint4* src = reinterpret_cast<const uint4*>(act) + plane * g.plane_len + pix;
+    int32_t acc[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) acc[e] = 0;
+    for (int n = 0; n < g.n; ++n) {
+      const uint4 v = __ldg(src + (int64_t)n * HlWl);
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int e = 0; e < 16; ++e) acc[e] += (int32_t)(int8_t)(w[e >> 2] >> (8 * (e & 3)));
+    }
+    // layout [plane][16][HlWl] so stage 2 reads contiguous rows per channel
+    int32_t* dst = bsum + plane * 16 * HlWl + pix;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) dst[(int64_t)e * HlWl] = acc[e];
+  }
+}
+
+// one block per (channel c); computes ic[c,r,s] for all taps, writes ic (reference
+// (c,r,s) order) and atomically adds sum_rs fsum[c,r,s]*ic[c,r,s] into *fic_rhs.
+__global__ void box_sum_dot_kernel(const int32_t* __restrict__ bsum, ActGeom g, const int32_t* __restrict__ fsum,
+                                   int32_t* __restrict__ ic_out, unsigned long long* __restrict__ fic_rhs) {
+  const int c = blockIdx.x;
+  if (c >= g.c) return;
+  const int64_t HlWl = (int64_t)g.Hl * g.Wl;
+  const int grp = c >> 4, e = c & 15;
+  __shared__ long long red[32];
+  long long dot_local = 0;
+  for (int tap = 0; tap < g.r * g.s; ++tap) {
+    const int r = tap / g.s, s = tap % g.s;
+    const int phase = (r % g.sh) * g.nph_w + (s % g.sw);
+    const int i0 = r / g.sh, j0 = s / g.sw;
+    const int32_t* img = bsum + ((int64_t)(phase * g.c16 + grp) * 16 + e) * HlWl;
+    long long acc = 0;
+    const int64_t cnt = (int64_t)g.p * g.q;
+    for (int64_t t = threadIdx.x; t < cnt; t += blockDim.x) {
+      const int pp = (int)(t / g.q), qq = (int)(t % g.q);
+      const int i = i0 + pp, j = j0 + qq;
+      // positions past the image block alias the next image's zero halo
+      if (i < g.Hl && j < g.Wl) acc += img[(int64_t)i * g.Wl + j];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      long long tot = 0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += red[w];
+      const int64_t ci = ((int64_t)c * g.r + r) * g.s + s;
+      if (ic_out) ic_out[ci] = (int32_t)tot;
+      if (fsum) dot_local += (long long)fsum[ci] * tot;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && fic_rhs) atomicAdd(fic_rhs, (unsigned long long)dot_local);
+}
+
+// ---------------------------------------------------------------------------
+// finalize kernels (single block), write an abed_verify_outcome to device memory
+// ---------------------------------------------------------------------------
+__device__ void write_outcome(abed_verify_outcome* o, int mismatch, int has_locus, int64_t l0, int64_t l1,
+                              int64_t l2, int64_t lhs, int64_t rhs, int64_t count) {
+  o->status = mismatch;
+  o->has_locus = has_locus;
+  o->locus[0] = l0; o->locus[1] = l1; o->locus[2] = l2;
+  o->lhs = lhs; o->rhs = rhs;
+  o->lhs_f = 0.0; o->rhs_f = 0.0;
+  o->error_count = count;
+}
+
+// FC, single N tile: records in M order -> first mismatching tile gives the locus
+__global__ void fc_finalize_rec_kernel(const int64_t* __restrict__ rec, int m_tiles, int P, int Q,
+                                       abed_verify_outcome* out) {
+  __shared__ long long s_cnt[32];
+  __shared__ int s_first[32];
+  long long cnt = 0;
+  int first = 0x7fffffff;
+  for (int t = threadIdx.x; t < m_tiles; t += blockDim.x) {
+    cnt += rec[t * 4 + 0];
+    if (rec[t * 4 + 0] > 0 && t < first) first = t;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    first = min(first, __shfl_xor_sync(0xffffffffu, first, o));
+  }
+  if ((threadIdx.x & 31) == 0) { s_cnt[threadIdx.x >> 5] = cnt; s_first[threadIdx.x >> 5] = first; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long c = 0; int f = 0x7fffffff;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { c += s_cnt[w]; f = min(f, s_first[w]); }
+    if (c == 0) {
+      write_outcome(out, 0, 0, 0, 0, 0, 0, 0, 0);
+    } else {
+      const int64_t key = rec[f * 4 + 1];
+      const int64_t PQ = (int64_t)P * Q;
+      write_outcome(out, 1, 1, key / PQ, (key % PQ) / Q, key % Q, rec[f * 4 + 2], rec[f * 4 + 3], c);
+    }
+  }
+}
+
+// FC, several N tiles: combine per-row partials over tiles; first mismatching
+// valid row in M order (== reference (n, p*Q+q) order).
+__global__ void fc_finalize_part_kernel(const int64_t* __restrict__ part, ActGeom g, int n_tiles,
+                                        unsigned long long* __restrict__ scratch /*[2]: count, min m*/) {
+  const int64_t rows = (int64_t)g.m_tiles * abed_dev::kBlockM;
+  const int64_t HlWl = (int64_t)g.Hl * g.Wl;
+  for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < g.m_total; m += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t rem = m % HlWl;
+    if (rem / g.Wl >= g.p || rem % g.Wl >= g.q) continue;
+    long long lhs = 0, rhs = 0;
+    for (int nt = 0; nt < n_tiles; ++nt) {
+      lhs += part[((int64_t)nt * rows + m) * 2 + 0];
+      rhs += part[((int64_t)nt * rows + m) * 2 + 1];
+    }
+    if (lhs != rhs) {
+      atomicAdd(&scratch[0], 1ull);
+      atomicMin(&scratch[1], (unsigned long long)m);
+    }
+  }
+}
+__global__ void fc_finalize_part2_kernel(const int64_t* __restrict__ part, ActGeom g, int n_tiles,
+                                         const unsigned long long* __restrict__ scratch, abed_verify_outcome* out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const unsigned long long cnt = scratch[0];
+  if (cnt == 0) { write_outcome(out, 0, 0, 0, 0, 0, 0, 0, 0); return; }
+  const int64_t m = (int64_t)scratch[1];
+  const int64_t rows = (int64_t)g.m_tiles * abed_dev::kBlockM;
+  const int64_t HlWl = (int64_t)g.Hl * g.Wl;
+  long long lhs = 0, rhs = 0;
+  for (int nt = 0; nt < n_tiles; ++nt) {
+    lhs += part[((int64_t)nt * rows + m) * 2 + 0];
+    rhs += part[((int64_t)nt * rows + m) * 2 + 1];
+  }
+  const int64_t n = m / HlWl, rem = m % HlWl;
+  write_outcome(out, 1, 1, n, rem / g.Wl, rem % g.Wl, lhs, rhs, (int64_t)cnt);
+}
+
+// FIC: lhs = sum of per-tile output sums; rhs = fic_dot (already reduced)
+__global__ void fic_finalize_kernel(const int64_t* __restrict__ part, int n, const unsigned long long* __restrict__ rhs_p,
+                                    abed_verify_outcome* out) {
+  __shared__ long long red[32];
+  long long s = 0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += part[i];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long tot = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += red[w];
+    const long long rhs = (long long)*rhs_p;
+    // checksum.hpp:287-294: Pass reports lhs = rhs = sum
+    write_outcome(out, tot != rhs ? 1 : 0, 0, 0, 0, 0, tot, rhs, tot != rhs ? 1 : 0);
+  }
+}
+
+// IC per-channel: out_sum[k] vs dot(f[k,:], ic) in i64; first mismatching k
+__global__ void ic_finalize_kernel(const unsigned long long* __restrict__ ksum, const int8_t* __restrict__ f,
+                                   const int32_t* __restrict__ ic, int64_t K, int64_t crs, abed_verify_outcome* out) {
+  __shared__ int s_first;
+  __shared__ long long s_lhs, s_rhs, s_cnt;
+  if (threadIdx.x == 0) { s_first = 0x7fffffff; s_cnt = 0; }
+  __syncthreads();
+  for (int64_t k = threadIdx.x; k < K; k += blockDim.x) {
+    long long dot = 0;
+    for (int64_t i = 0; i < crs; ++i) dot += (long long)f[k * crs + i] * ic[i];
+    const long long lhs = (long long)ksum[k];
+    if (lhs != dot) {
+      atomicAdd((unsigned long long*)&s_cnt, 1ull);
+      atomicMin(&s_first, (int)k);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (s_cnt == 0) {
+      write_outcome(out, 0, 0, 0, 0, 0, 0, 0, 0);
+    } else {
+      const int64_t k = s_first;
+      long long dot = 0;
+      for (int64_t i = 0; i < crs; ++i) dot += (long long)f[k * crs + i] * ic[i];
+      write_outcome(out, 1, 1, k, -1, -1, (long long)ksum[k], dot, s_cnt);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// plan construction
+// ---------------------------------------------------------------------------
+static int g_num_sms = 0;
+int num_sms() {
+  if (g_num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+static constexpr uint32_t kSmemBudget = 232448 - 2048;
+
+bool choose_tiling(const ActGeom& g, bool fc, int force_block_n, ConvTcParams& p) {
+  const int ntaps = g.r * g.s;
+  const int k_pad = (int)ceil_div(g.k, 16) * 16;
+  const int strip = geom_strip_pix(g);
+  auto a_stage = [&](int gps) { return (uint32_t)g.n_phase * gps * strip * 16u; };
+  // 1) B resident in shared memory, one N tile per CTA
+  for (int bn = std::min(k_pad, 256); bn >= 64; bn -= 16) {
+    if (force_block_n && bn != force_block_n) continue;
+    if (k_pad % bn) continue;
+    const int tot = bn + (fc ? 16 : 0);
+    if (tot > 256) continue;
+    const uint32_t bres = (uint32_t)tot * ntaps * g.c16 * 16u;
+    for (int gps : {4, 2}) {
+      if (g.c16 % gps) continue;
+      const uint32_t bytes = bres + abed_dev::kStages_host * a_stage(gps) + 512;
+      if (bytes > kSmemBudget) continue;
+      p.block_n = bn; p.block_n_tot = tot; p.gps = gps; p.b_resident = 1;
+      p.n_tiles = k_pad / bn;
+      p.k_stages = g.c16 / gps;
+      p.b_stage_bytes = (uint32_t)tot * ntaps * gps * 16u;
+      return true;
+    }
+  }
+  // 2) B streamed with the activation strips through the stage ring
+  for (int bn = std::min(k_pad, 256); bn >= 16; bn -= 16) {
+    if (force_block_n && bn != force_block_n) continue;
+    if (k_pad % bn) continue;
+    const int tot = bn + (fc ? 16 : 0);
+    for (int gps : {4, 2}) {
+      if (g.c16 % gps) continue;
+      const uint32_t bstage = (uint32_t)tot * ntaps * gps * 16u;
+      const uint32_t bytes = abed_dev::kStages_host * (a_stage(gps) + bstage) + 512;
+      if (bytes > kSmemBudget) continue;
+      p.block_n = bn; p.block_n_tot = tot; p.gps = gps; p.b_resident = 0;
+      p.n_tiles = k_pad / bn;
+      p.k_stages = g.c16 / gps;
+      p.b_stage_bytes = bstage;
+      return true;
+    }
+  }
+  return false;
+}
+
+}  // namespace abed_host

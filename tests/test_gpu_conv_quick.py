@@ -1,0 +1,43 @@
+"""First GPU parity check of the tcgen05 conv: abed_conv_i8 vs an exact float64 conv."""
+import ctypes as C
+
+import pytest
+import torch
+
+from paper_2006_04984_b200 import abi
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [
+    (1, 64, 56, 56, 64, 3, 3, 1, 1, 1, 1),    # cfg1
+    (2, 32, 9, 11, 16, 3, 3, 1, 1, 1, 1),
+    (1, 8, 12, 12, 8, 3, 3, 1, 1, 1, 1),
+    (2, 4, 8, 8, 3, 3, 3, 2, 2, 1, 1),
+    (3, 128, 14, 14, 256, 3, 3, 1, 1, 1, 1),
+    (2, 256, 7, 7, 512, 3, 3, 1, 1, 1, 1),
+    (2, 64, 16, 16, 64, 1, 1, 1, 1, 0, 0),
+    (2, 64, 16, 16, 128, 3, 3, 2, 2, 1, 1),
+    (1, 16, 10, 10, 32, 5, 5, 1, 1, 2, 2),
+]
+
+
+def ref_conv(x, f, ls):
+    y = torch.nn.functional.conv2d(x.double(), f.double(), stride=(ls.stride_h, ls.stride_w),
+                                   padding=(ls.pad_h, ls.pad_w))
+    return y.to(torch.int64)
+
+
+@pytest.mark.parametrize("dims", SHAPES)
+def test_conv_i8_matches_exact(dims):
+    ls = abi.layer_shape(*dims)
+    g = torch.Generator().manual_seed(sum(dims))
+    x = torch.randint(-128, 128, ls.input_dims(), dtype=torch.int8, generator=g)
+    f = torch.randint(-128, 128, ls.filter_dims(), dtype=torch.int8, generator=g)
+    xd, fd = x.cuda(), f.cuda()
+    out = torch.empty(ls.output_dims(), dtype=torch.int32, device="cuda")
+    abi.call("abed_conv_i8", xd.data_ptr(), fd.data_ptr(), C.byref(ls), out.data_ptr(), None)
+    torch.cuda.synchronize()
+    want = ref_conv(x, f, ls)
+    got = out.cpu().to(torch.int64)
+    bad = (got != want).nonzero()
+    assert bad.numel() == 0, f"{bad.shape[0]} mismatches, first {bad[:4].tolist()} got {got.flatten()[:8]} want {want.flatten()[:8]}"
