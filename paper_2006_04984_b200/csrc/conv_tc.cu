@@ -7,11 +7,12 @@
 // per-channel reduction (:319-347), all inside the accumulator epilogue, before
 // the fused scale/bias/ReLU/requantise (convolution.hpp:353-387).
 //
-// CTA = 6 warps, one CTA per SM, persistent over (M tile, N tile) work units:
+// CTA = 10 warps, one CTA per SM, persistent over (M tile, N tile) work units:
 //   warp 0      producer: one thread issues 1-D bulk copies (cp.async.bulk) of
 //               the activation strips (and B blocks unless B is resident)
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
-//   warps 2..5  epilogue: tcgen05.ld (thread = GEMM row = output pixel),
+//   warps 2..9  epilogue: tcgen05.ld (thread = GEMM row = output pixel), two
+//               warps per TMEM lane quarter splitting the 16-column chunks;
 //               checks, epilog, stores; double-buffered TMEM accumulators.
 #include <cuda_runtime.h>
 
@@ -22,28 +23,36 @@
 
 namespace abed_dev {
 
+constexpr int kEpiWarps = 8;
+constexpr int kEpiThreads = kEpiWarps * 32;
+constexpr int kConvThreads = 64 + kEpiThreads;
+constexpr int kBiasSmem = 2048;
+
+// compile-time output flavours
+enum EpiKind : int { EPI_NONE = 0, EPI_NCHW = 1, EPI_PACKED = 2, EPI_COMPARE = 3 };
+
 struct SmemLayout {
-  uint32_t a_off, a_stage_bytes, b_off, b_stage_bytes_smem, bar_off, total;
+  uint32_t a_off, a_stage_bytes, b_off, bar_off, tab_off, total;
 };
 
 __host__ __device__ inline SmemLayout smem_layout(const ConvTcParams& p) {
   SmemLayout L;
   L.a_stage_bytes = static_cast<uint32_t>(p.n_phase) * p.gps * p.strip_pix * 16u;
   L.a_off = 0;
-  uint32_t off = L.a_stage_bytes * kStages;
+  uint32_t off = L.a_stage_bytes * p.n_stages;
   off = (off + 127u) & ~127u;
   L.b_off = off;
-  L.b_stage_bytes_smem = p.b_stage_bytes;
-  off += p.b_resident ? p.b_stage_bytes * p.k_stages : p.b_stage_bytes * kStages;
+  off += p.b_resident ? p.b_stage_bytes * p.k_stages : p.b_stage_bytes * p.n_stages;
   off = (off + 127u) & ~127u;
   L.bar_off = off;
   off += 8 * (2 * kStages + 5) + 16;
+  L.tab_off = off;  // per-stage MMA operand offset table (uint2 per MMA)
+  off += 8u * p.ntaps * (p.gps / 2);
   L.total = off;
   return L;
 }
 
-__device__ __forceinline__ void decode_tile(const ConvTcParams& p, int tile_seq, int& mt,
-                                            int& nt) {
+__device__ __forceinline__ void decode_tile(const ConvTcParams& p, int tile_seq, int& mt, int& nt) {
   // b_resident with several N tiles: each CTA owns one N tile (blockIdx % n_tiles)
   if (p.b_resident) {
     nt = blockIdx.x % p.n_tiles;
@@ -55,16 +64,30 @@ __device__ __forceinline__ void decode_tile(const ConvTcParams& p, int tile_seq,
   }
 }
 
-__device__ __forceinline__ int8_t requant(int32_t acc, float scale, float bias, int relu) {
-  // convolution.hpp:374-381 under the reference's -march=native build: the
-  // multiply-add contracts to one fused FMA, then ReLU, clamp, truncate.
+// convolution.hpp:374-381 under the reference's -march=native build: the
+// multiply-add contracts to one fused FMA, then ReLU, clamp, truncate.
+__device__ __forceinline__ int32_t requant_i8(int32_t acc, float scale, float bias, int relu) {
   float v = __fmaf_rn(static_cast<float>(acc), scale, bias);
-  if (relu && v < 0.0f) v = 0.0f;
+  if (relu) {
+    // v < 0 -> 0 (reference keeps -0.0, which truncates to 0 as well)
+    v = fminf(fmaxf(v, 0.0f), 127.0f);
+    // 2^23 + v rounded toward zero puts trunc(v) in the low mantissa bits
+    return static_cast<int32_t>(__float_as_uint(__fadd_rz(v, 8388608.0f)) & 0xFFu);
+  }
   v = fminf(127.0f, fmaxf(-128.0f, v));
-  return static_cast<int8_t>(__float2int_rz(v));
+  return __float2int_rz(v);
 }
 
-__global__ void __launch_bounds__(kThreads, 1) conv_i8_tc_kernel(const __grid_constant__ ConvTcParams p) {
+__device__ __forceinline__ uint32_t pack4(int32_t a, int32_t b, int32_t c, int32_t d) {
+  const uint32_t lo = __byte_perm(static_cast<uint32_t>(a), static_cast<uint32_t>(b), 0x0040u);
+  const uint32_t hi = __byte_perm(static_cast<uint32_t>(c), static_cast<uint32_t>(d), 0x0040u);
+  return __byte_perm(lo, hi, 0x5410u);
+}
+
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory"); }
+
+template <int EPI, bool FC, bool FIC>
+__global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __grid_constant__ ConvTcParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   const SmemLayout L = smem_layout(p);
   uint8_t* sA = smem + L.a_off;
@@ -76,7 +99,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_i8_tc_kernel(const __grid_co
   uint64_t* tempty = bars + 2 * kStages + 2;
   uint64_t* bres = bars + 2 * kStages + 4;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 5);
-  __shared__ int64_t red_s64[4][4];
+  __shared__ float s_bias[kBiasSmem];
+  __shared__ int64_t s_red[kEpiWarps][4];
+  __shared__ int64_t s_rowsum[kBlockM];
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -94,10 +119,13 @@ __global__ void __launch_bounds__(kThreads, 1) conv_i8_tc_kernel(const __grid_co
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 4);
+      mbar_init(&tempty[i], kEpiWarps);
     }
     mbar_init(bres, 1);
     fence_mbar_init();
+  }
+  if (EPI != EPI_NONE && p.K <= kBiasSmem) {
+    for (int i = threadIdx.x; i < p.K; i += blockDim.x) s_bias[i] = p.bias[i];
   }
   if (warp == 1) tmem_alloc(tmem_slot, tmem_cols);
   tc_fence_before();
@@ -110,10 +138,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv_i8_tc_kernel(const __grid_co
   if (p.b_resident) {
     const int per = gridDim.x / p.n_tiles;
     const int mt0 = blockIdx.x / p.n_tiles;
-    n_units = (blockIdx.x < per * p.n_tiles && mt0 < p.m_tiles) ? (p.m_tiles - mt0 + per - 1) / per : 0;
+    n_units = (static_cast<int>(blockIdx.x) < per * p.n_tiles && mt0 < p.m_tiles) ? (p.m_tiles - mt0 + per - 1) / per : 0;
   } else {
     const int total = p.m_tiles * p.n_tiles;
-    n_units = blockIdx.x < total ? (total - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    n_units = static_cast<int>(blockIdx.x) < total ? (total - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
   }
 
   if (warp == 0) {
@@ -125,7 +153,6 @@ __global__ void __launch_bounds__(kThreads, 1) conv_i8_tc_kernel(const __grid_co
         const uint32_t bytes = p.b_stage_bytes * p.k_stages;
         mbar_arrive_expect_tx(bres, bytes);
         const int8_t* src = p.wpk + static_cast<int64_t>(nt) * p.k_stages * p.b_stage_bytes;
-        // split into <= 64 KB pieces
         for (uint32_t o = 0; o < bytes; o += 65536u) {
           const uint32_t sz = (bytes - o) < 65536u ? (bytes - o) : 65536u;
           bulk_g2s_evict_last(sB + o, src + o, sz, bres, pol_b);
@@ -134,14 +161,13 @@ __global__ void __launch_bounds__(kThreads, 1) conv_i8_tc_kernel(const __grid_co
       int stage = 0;
       uint32_t phase = 0;
       const uint32_t strip_bytes = p.strip_pix * 16u;
+      const uint32_t bytes = L.a_stage_bytes + (p.b_resident ? 0u : p.b_stage_bytes);
       for (int u = 0; u < n_units; ++u) {
         int mt, nt;
         decode_tile(p, u, mt, nt);
         const int64_t m0 = static_cast<int64_t>(mt) * kBlockM;
         for (int ks = 0; ks < p.k_stages; ++ks) {
           mbar_wait(&empty[stage], phase ^ 1u);
-          const uint32_t bytes =
-              L.a_stage_bytes + (p.b_resident ? 0u : p.b_stage_bytes);
           mbar_arrive_expect_tx(&full[stage], bytes);
           uint8_t* dstA = sA + stage * L.a_stage_bytes;
           for (int ph = 0; ph < p.n_phase; ++ph) {
@@ -152,12 +178,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv_i8_tc_kernel(const __grid_co
             }
           }
           if (!p.b_resident) {
-            const int8_t* src =
-                p.wpk + (static_cast<int64_t>(nt) * p.k_stages + ks) * p.b_stage_bytes;
-            bulk_g2s_evict_last(sB + stage * p.b_stage_bytes, src, p.b_stage_bytes, &full[stage],
-                                pol_b);
+            const int8_t* src = p.wpk + (static_cast<int64_t>(nt) * p.k_stages + ks) * p.b_stage_bytes;
+            bulk_g2s_evict_last(sB + stage * p.b_stage_bytes, src, p.b_stage_bytes, &full[stage], pol_b);
           }
-          if (++stage == kStages) {
+          if (++stage == p.n_stages) {
             stage = 0;
             phase ^= 1u;
           }
@@ -166,51 +190,53 @@ __global__ void __launch_bounds__(kThreads, 1) conv_i8_tc_kernel(const __grid_co
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
+    // Per-MMA descriptor offsets (16-byte units) are tabulated once: the issue
+    // loop is then one smem load, two adds and the tcgen05.mma per instruction.
+    uint2* tab = reinterpret_cast<uint2*>(smem + L.tab_off);
+    const int n_mma = p.ntaps * (p.gps / 2);
+    const uint32_t strip_bytes = p.strip_pix * 16u;
+    const uint32_t b_lbo = p.block_n_tot * 16u;
+    for (int i = lane; i < n_mma; i += 32) {
+      const int tap = i / (p.gps / 2), g = (i % (p.gps / 2)) * 2;
+      const uint32_t a_off = p.tap_phase[tap] * p.gps * strip_bytes + static_cast<uint32_t>(p.tap_shift[tap]) * 16u +
+                             g * strip_bytes;
+      const uint32_t b_off = (tap * p.gps + g) * b_lbo;
+      tab[i] = make_uint2(a_off >> 4, b_off >> 4);
+    }
+    __syncwarp();
     if (n_units > 0) {
-      if (p.b_resident) {
-        mbar_wait(bres, 0);
-      }
+      if (p.b_resident) mbar_wait(bres, 0);
       int stage = 0;
       uint32_t phase = 0;
       int as = 0;
       uint32_t aphase = 0;
-      const uint32_t strip_bytes = p.strip_pix * 16u;
       const uint32_t n_main = p.block_n_tot > 256 ? 256u : static_cast<uint32_t>(p.block_n_tot);
       const uint32_t n_rest = p.block_n_tot > 256 ? static_cast<uint32_t>(p.block_n_tot - 256) : 0u;
       const uint32_t idesc_main = make_idesc_i8(n_main);
       const uint32_t idesc_rest = make_idesc_i8(n_rest > 0 ? n_rest : 16u);
-      const uint32_t b_lbo = p.block_n_tot * 16u;
       for (int u = 0; u < n_units; ++u) {
         mbar_wait(&tempty[as], aphase ^ 1u);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + as * acc_cols;
-        uint32_t accum = 0;
         for (int ks = 0; ks < p.k_stages; ++ks) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           if (lane == 0) {
-            const uint32_t a_base = smem_u32(sA + stage * L.a_stage_bytes);
-            const uint32_t b_base = smem_u32(
-                p.b_resident ? sB + ks * p.b_stage_bytes : sB + stage * p.b_stage_bytes);
-            for (int tap = 0; tap < p.ntaps; ++tap) {
-              const uint32_t a_tap = a_base + p.tap_phase[tap] * p.gps * strip_bytes +
-                                     static_cast<uint32_t>(p.tap_shift[tap]) * 16u;
-              for (int g = 0; g < p.gps; g += 2) {
-                const uint64_t adesc = make_sdesc(a_tap + g * strip_bytes, strip_bytes, 128u);
-                const uint32_t b_off = (tap * p.gps + g) * b_lbo;
-                const uint64_t bdesc = make_sdesc(b_base + b_off, b_lbo, 128u);
-                mma_i8(d_tmem, adesc, bdesc, idesc_main, accum);
-                if (n_rest) {
-                  const uint64_t bdesc2 = make_sdesc(b_base + b_off + 256u * 16u, b_lbo, 128u);
-                  mma_i8(d_tmem + 256u, adesc, bdesc2, idesc_rest, accum);
-                }
-                accum = 1;
-              }
+            const uint64_t a0 = make_sdesc(smem_u32(sA + stage * L.a_stage_bytes), strip_bytes, 128u);
+            const uint64_t b0 = make_sdesc(
+                smem_u32(p.b_resident ? sB + ks * p.b_stage_bytes : sB + stage * p.b_stage_bytes), b_lbo, 128u);
+            uint32_t accum = ks > 0 ? 1u : 0u;
+#pragma unroll 3
+            for (int i = 0; i < n_mma; ++i) {
+              const uint2 o = tab[i];
+              mma_i8(d_tmem, a0 + o.x, b0 + o.y, idesc_main, accum);
+              if (n_rest) mma_i8(d_tmem + 256u, a0 + o.x, b0 + o.y + 256u, idesc_rest, accum);
+              accum = 1u;
             }
             mma_commit(&empty[stage]);
           }
           __syncwarp();
-          if (++stage == kStages) {
+          if (++stage == p.n_stages) {
             stage = 0;
             phase ^= 1u;
           }
@@ -225,201 +251,233 @@ __global__ void __launch_bounds__(kThreads, 1) conv_i8_tc_kernel(const __grid_co
     }
   } else {
     // ------------------------------------------------------------ epilogue
-    const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+    const int ew = warp - 2;                // 0..7
+    const int quarter = warp & 3;           // TMEM lane quarter this warp may access
+    const int half = ew >> 2;               // which alternate 16-column chunks
     const int row = quarter * 32 + lane;
-    const int ew = warp - 2;       // 0..3
     int as = 0;
     uint32_t aphase = 0;
+    const uint32_t HlWl = static_cast<uint32_t>(p.Hl) * p.Wl;
     const int64_t PQ = static_cast<int64_t>(p.P) * p.Q;
-    const int64_t HlWl = static_cast<int64_t>(p.Hl) * p.Wl;
+    const bool bias_in_smem = p.K <= kBiasSmem;
+    const float scale = p.scale;
+    // chunk-sum in int32 is exact when 16 * max|acc| < 2^31 (CRS < 8192)
+    const bool chunk32 = p.ntaps * p.c16 * 16 < 8192;
     for (int u = 0; u < n_units; ++u) {
       int mt, nt;
       decode_tile(p, u, mt, nt);
-      const int64_t m = static_cast<int64_t>(mt) * kBlockM + row;
-      int n_img = 0, pp = 0, qq = 0;
-      bool valid = m < p.m_total;
+      const uint32_t m = static_cast<uint32_t>(mt) * kBlockM + row;
+      uint32_t n_img = 0, pp = 0, qq = 0;
+      bool valid = m < static_cast<uint64_t>(p.m_total);
       if (valid) {
-        n_img = static_cast<int>(m / HlWl);
-        const int64_t rem = m - n_img * HlWl;
-        pp = static_cast<int>(rem / p.Wl);
-        qq = static_cast<int>(rem - static_cast<int64_t>(pp) * p.Wl);
-        valid = pp < p.P && qq < p.Q;
+        n_img = m / HlWl;
+        const uint32_t rem = m - n_img * HlWl;
+        pp = rem / p.Wl;
+        qq = rem - pp * p.Wl;
+        valid = pp < static_cast<uint32_t>(p.P) && qq < static_cast<uint32_t>(p.Q);
       }
-      const int64_t ref_pix = static_cast<int64_t>(n_img) * PQ + static_cast<int64_t>(pp) * p.Q + qq;
+      // per-row output base addresses
+      int8_t* pk_row = nullptr;
+      int64_t nchw_row = 0;
+      if (EPI == EPI_PACKED || EPI == EPI_COMPARE) {
+        const int hh = pp + p.o_ph, ww = qq + p.o_pw;
+        const int a_ph = hh % p.o_sh, b_ph = ww % p.o_sw;
+        const int64_t t = (static_cast<int64_t>(n_img) * p.o_Hl + hh / p.o_sh) * p.o_Wl + ww / p.o_sw;
+        pk_row = static_cast<int8_t*>(p.out) +
+                 (static_cast<int64_t>(a_ph * p.o_nph_w + b_ph) * p.o_c16 * p.o_plane_len + t) * 16;
+      } else if (EPI == EPI_NCHW) {
+        nchw_row = static_cast<int64_t>(n_img) * p.K * PQ + static_cast<int64_t>(pp) * p.Q + qq;
+      }
 
       mbar_wait(&tfull[as], aphase);
       tc_fence_after();
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + as * acc_cols;
 
-      int64_t row_sum = 0;   // sum over this tile's channels (FC lhs part, FIC)
+      int64_t row_sum = 0;  // this warp's channels of the row (FC lhs part, FIC)
       const int k_base = nt * p.block_n;
-      for (int cb = 0; cb < p.block_n; cb += 16) {
+      for (int cb = half * 16; cb < p.block_n; cb += 32) {
         uint32_t v[16];
         tmem_ld16(t_row + cb, v);
         tmem_ld_wait();
         int32_t a[16];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          a[j] = static_cast<int32_t>(v[j]);
-          const int k = k_base + cb + j;
-          if (p.fault_key >= 0 && valid && k < p.K) {
-            const int64_t key = (static_cast<int64_t>(n_img) * p.K + k) * PQ +
-                                static_cast<int64_t>(pp) * p.Q + qq;
-            if (key == p.fault_key) a[j] = static_cast<int32_t>(static_cast<uint32_t>(a[j]) ^ (1u << p.fault_bit));
-          }
-          if (!(valid && k < p.K)) a[j] = 0;
-          row_sum += a[j];
-        }
-        if (p.check & CHECK_IC) {
-          // per-channel column sums over the 32 rows of this warp, then one
-          // atomic per channel per warp
+        for (int j = 0; j < 16; ++j) a[j] = static_cast<int32_t>(v[j]);
+        const int k0 = k_base + cb;
+        if (p.fault_key >= 0 && valid) {
+          // ConvOut fault hook (faults.hpp:230-233): flip before checks and epilog
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
-            long long s = a[j];
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-            const int k = k_base + cb + j;
-            if (lane == j && k < p.K && s != 0)
-              atomicAdd(&p.ic_sum[k], static_cast<unsigned long long>(s));
+            const int64_t key = (static_cast<int64_t>(n_img) * p.K + k0 + j) * PQ + static_cast<int64_t>(pp) * p.Q + qq;
+            if (key == p.fault_key) a[j] = static_cast<int32_t>(static_cast<uint32_t>(a[j]) ^ (1u << p.fault_bit));
           }
         }
-        if (valid) {
-          const int k0 = k_base + cb;
-          switch (p.out_mode) {
-            case OUT_I32_NCHW: {
-              int32_t* o = static_cast<int32_t*>(p.out);
+        const bool kfull = k0 + 16 <= p.K;
+        if (!kfull) {
 #pragma unroll
-              for (int j = 0; j < 16; ++j)
-                if (k0 + j < p.K)
-                  o[(static_cast<int64_t>(n_img) * p.K + k0 + j) * PQ + static_cast<int64_t>(pp) * p.Q + qq] = a[j];
-              break;
+          for (int j = 0; j < 16; ++j)
+            if (k0 + j >= p.K) a[j] = 0;
+        }
+        if (FC || FIC || (p.check & CHECK_IC)) {
+          if (chunk32) {
+            int32_t s = 0;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) s += a[j];
+            row_sum += s;
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) row_sum += a[j];
+          }
+        }
+        if (p.check & CHECK_IC) {
+          // per-channel column sums over the 32 rows of this warp, one atomic per channel
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            long long s = valid ? a[j] : 0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+            if (lane == j && k0 + j < p.K && s != 0) atomicAdd(&p.ic_sum[k0 + j], static_cast<unsigned long long>(s));
+          }
+        }
+        if (EPI == EPI_PACKED || EPI == EPI_COMPARE) {
+          int32_t y[16];
+          if (bias_in_smem) {
+            const float4* b4 = reinterpret_cast<const float4*>(s_bias + k0);
+#pragma unroll
+            for (int j4 = 0; j4 < 4; ++j4) {
+              const float4 bb = b4[j4];
+              y[j4 * 4 + 0] = requant_i8(a[j4 * 4 + 0], scale, bb.x, p.relu);
+              y[j4 * 4 + 1] = requant_i8(a[j4 * 4 + 1], scale, bb.y, p.relu);
+              y[j4 * 4 + 2] = requant_i8(a[j4 * 4 + 2], scale, bb.z, p.relu);
+              y[j4 * 4 + 3] = requant_i8(a[j4 * 4 + 3], scale, bb.w, p.relu);
             }
-            case OUT_I8_NCHW: {
-              int8_t* o = static_cast<int8_t*>(p.out);
+          } else {
 #pragma unroll
-              for (int j = 0; j < 16; ++j)
-                if (k0 + j < p.K)
-                  o[(static_cast<int64_t>(n_img) * p.K + k0 + j) * PQ + static_cast<int64_t>(pp) * p.Q + qq] =
-                      requant(a[j], p.scale, __ldg(p.bias + k0 + j), p.relu);
-              break;
+            for (int j = 0; j < 16; ++j) y[j] = requant_i8(a[j], scale, __ldg(p.bias + k0 + j), p.relu);
+          }
+          if (!kfull) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (k0 + j >= p.K) y[j] = 0;
+          }
+          const uint4 val = make_uint4(pack4(y[0], y[1], y[2], y[3]), pack4(y[4], y[5], y[6], y[7]),
+                                       pack4(y[8], y[9], y[10], y[11]), pack4(y[12], y[13], y[14], y[15]));
+          if (valid) {
+            uint4* dst = reinterpret_cast<uint4*>(pk_row + static_cast<int64_t>(k0 >> 4) * p.o_plane_len * 16);
+            if (EPI == EPI_PACKED) {
+              *dst = val;
+            } else {
+              const uint4 ref = *dst;
+              if (ref.x != val.x || ref.y != val.y || ref.z != val.z || ref.w != val.w) atomicAdd(p.cmp_count, 1ull);
             }
-            case OUT_F32_NCHW: {
-              float* o = static_cast<float*>(p.out);
+          }
+        } else if (EPI == EPI_NCHW) {
+          if (valid) {
+            const int64_t base = nchw_row + static_cast<int64_t>(k0) * PQ;
+            switch (p.out_mode) {
+              case OUT_I32_NCHW: {
+                int32_t* o = static_cast<int32_t*>(p.out) + base;
 #pragma unroll
-              for (int j = 0; j < 16; ++j)
-                if (k0 + j < p.K) {
-                  float f = __fmaf_rn(static_cast<float>(a[j]), p.scale, __ldg(p.bias + k0 + j));
-                  if (p.relu && f < 0.0f) f = 0.0f;
-                  o[(static_cast<int64_t>(n_img) * p.K + k0 + j) * PQ + static_cast<int64_t>(pp) * p.Q + qq] = f;
-                }
-              break;
-            }
-            case OUT_I8_PACKED:
-            case OUT_I8_COMPARE: {
-              uint32_t w4[4];
-#pragma unroll
-              for (int j4 = 0; j4 < 4; ++j4) {
-                uint32_t word = 0;
-#pragma unroll
-                for (int b = 0; b < 4; ++b) {
-                  const int j = j4 * 4 + b;
-                  const int8_t y = (k0 + j < p.K) ? requant(a[j], p.scale, __ldg(p.bias + k0 + j), p.relu) : int8_t(0);
-                  word |= static_cast<uint32_t>(static_cast<uint8_t>(y)) << (8 * b);
-                }
-                w4[j4] = word;
+                for (int j = 0; j < 16; ++j)
+                  if (k0 + j < p.K) o[j * PQ] = a[j];
+                break;
               }
-              // output pixel (n, h=pp, w=qq) -> next layer's phase/sub-pixel
-              const int hh = pp + p.o_ph, ww = qq + p.o_pw;
-              const int a_ph = hh % p.o_sh, b_ph = ww % p.o_sw;
-              const int ii = hh / p.o_sh, jj = ww / p.o_sw;
-              const int phase_id = a_ph * p.o_nph_w + b_ph;
-              const int64_t t = (static_cast<int64_t>(n_img) * p.o_Hl + ii) * p.o_Wl + jj;
-              const int g = k0 >> 4;
-              uint4* dst = reinterpret_cast<uint4*>(static_cast<int8_t*>(p.out) +
-                                                    ((static_cast<int64_t>(phase_id) * p.o_c16 + g) * p.o_plane_len + t) * 16);
-              const uint4 val = make_uint4(w4[0], w4[1], w4[2], w4[3]);
-              if (p.out_mode == OUT_I8_PACKED) {
-                *dst = val;
-              } else {
-                const uint4 ref = *dst;
-                if (ref.x != val.x || ref.y != val.y || ref.z != val.z || ref.w != val.w)
-                  atomicAdd(p.cmp_count, 1ull);
+              case OUT_I8_NCHW: {
+                int8_t* o = static_cast<int8_t*>(p.out) + base;
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                  if (k0 + j < p.K) o[j * PQ] = static_cast<int8_t>(requant_i8(a[j], scale, __ldg(p.bias + k0 + j), p.relu));
+                break;
               }
-              break;
+              default: {  // OUT_F32_NCHW
+                float* o = static_cast<float*>(p.out) + base;
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                  if (k0 + j < p.K) {
+                    float f = __fmaf_rn(static_cast<float>(a[j]), scale, __ldg(p.bias + k0 + j));
+                    if (p.relu && f < 0.0f) f = 0.0f;
+                    o[j * PQ] = f;
+                  }
+                break;
+              }
             }
-            default:
-              break;
           }
         }
       }
       int64_t extra = 0;
-      if (p.check & CHECK_FC) {
+      if (FC && half == 0) {
         uint32_t v[16];
         tmem_ld16(t_row + p.block_n, v);
         tmem_ld_wait();
         extra = static_cast<int64_t>(static_cast<int32_t>(v[0])) +
                 (static_cast<int64_t>(static_cast<int32_t>(v[1])) << 8) +
                 (static_cast<int64_t>(static_cast<int32_t>(v[2])) << 16);
-        if (!valid) extra = 0;
       }
-      // accumulator consumed: hand TMEM stage back to the MMA warp
+      // accumulator consumed: hand the TMEM stage back to the MMA warp
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[as]);
+      if (!valid) row_sum = 0;
 
       const int tile_id = nt * p.m_tiles + mt;
-      if (p.check & CHECK_FC) {
-        if (p.n_tiles > 1) {
-          int64_t* part = p.fc_part + (static_cast<int64_t>(nt) * p.m_tiles * kBlockM + mt * kBlockM + row) * 2;
-          part[0] = row_sum;
-          part[1] = extra;
-        } else {
-          const bool bad = valid && (row_sum != extra);
-          const unsigned ballot = __ballot_sync(0xffffffffu, bad);
-          int64_t cnt = __popc(ballot);
-          // first mismatching row of this warp (rows are in reference order)
-          int64_t key = -1, lhs = 0, rhs = 0;
-          if (ballot) {
-            const int src = __ffs(ballot) - 1;
-            key = __shfl_sync(0xffffffffu, ref_pix, src);
-            lhs = __shfl_sync(0xffffffffu, row_sum, src);
-            rhs = __shfl_sync(0xffffffffu, extra, src);
-          }
-          if (lane == 0) {
-            red_s64[quarter][0] = cnt;
-            red_s64[quarter][1] = key;
-            red_s64[quarter][2] = lhs;
-            red_s64[quarter][3] = rhs;
-          }
-          asm volatile("bar.sync 1, 128;" ::: "memory");
-          if (ew == 0 && lane == 0) {
-            int64_t c = 0, k = -1, l = 0, r = 0;
-            for (int qd = 0; qd < 4; ++qd) {
-              c += red_s64[qd][0];
-              if (k < 0 && red_s64[qd][1] >= 0) {
-                k = red_s64[qd][1];
-                l = red_s64[qd][2];
-                r = red_s64[qd][3];
-              }
+      if (FC) {
+        // combine the two column halves of each row
+        if (half == 1) s_rowsum[row] = row_sum;
+        epi_bar();
+        if (half == 0) {
+          const int64_t lhs = row_sum + s_rowsum[row];
+          if (p.n_tiles > 1) {
+            int64_t* part = p.fc_part + (static_cast<int64_t>(nt) * p.m_tiles * kBlockM + m) * 2;
+            part[0] = valid ? lhs : 0;
+            part[1] = valid ? extra : 0;
+          } else {
+            const bool bad = valid && (lhs != extra);
+            const unsigned ballot = __ballot_sync(0xffffffffu, bad);
+            int64_t key = -1, l = 0, r = 0;
+            if (ballot) {
+              const int src = __ffs(ballot) - 1;
+              key = __shfl_sync(0xffffffffu, static_cast<int64_t>(n_img) * PQ + static_cast<int64_t>(pp) * p.Q + qq, src);
+              l = __shfl_sync(0xffffffffu, lhs, src);
+              r = __shfl_sync(0xffffffffu, extra, src);
             }
-            int64_t* rec = p.fc_rec + static_cast<int64_t>(tile_id) * 4;
-            rec[0] = c;
-            rec[1] = k;
-            rec[2] = l;
-            rec[3] = r;
+            if (lane == 0) {
+              s_red[quarter][0] = __popc(ballot);
+              s_red[quarter][1] = key;
+              s_red[quarter][2] = l;
+              s_red[quarter][3] = r;
+            }
           }
-          asm volatile("bar.sync 1, 128;" ::: "memory");
+        }
+        epi_bar();
+        if (p.n_tiles == 1 && ew == 0 && lane == 0) {
+          int64_t c = 0, k = -1, l = 0, r = 0;
+          for (int qd = 0; qd < 4; ++qd) {
+            c += s_red[qd][0];
+            if (k < 0 && s_red[qd][1] >= 0) {
+              k = s_red[qd][1];
+              l = s_red[qd][2];
+              r = s_red[qd][3];
+            }
+          }
+          int64_t* rec = p.fc_rec + static_cast<int64_t>(tile_id) * 4;
+          rec[0] = c;
+          rec[1] = k;
+          rec[2] = l;
+          rec[3] = r;
         }
       }
-      if (p.check & CHECK_FIC) {
+      if (FIC) {
         long long s = row_sum;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (lane == 0) red_s64[quarter][0] = s;
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (ew == 0 && lane == 0)
-          p.fic_part[tile_id] = red_s64[0][0] + red_s64[1][0] + red_s64[2][0] + red_s64[3][0];
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+        epi_bar();  // s_red reuse guard
+        if (lane == 0) s_red[ew][0] = s;
+        epi_bar();
+        if (ew == 0 && lane == 0) {
+          int64_t tot = 0;
+#pragma unroll
+          for (int w = 0; w < kEpiWarps; ++w) tot += s_red[w][0];
+          p.fic_part[tile_id] = tot;
+        }
       }
       if (++as == n_acc) {
         as = 0;
@@ -447,15 +505,29 @@ using abed_dev::ConvTcParams;
 
 uint32_t conv_tc_smem_bytes(const ConvTcParams& p) { return abed_dev::smem_layout(p).total; }
 
-cudaError_t conv_tc_launch(const ConvTcParams& p, int num_sms, cudaStream_t stream) {
-  const uint32_t smem = conv_tc_smem_bytes(p);
+template <int EPI, bool FC, bool FIC>
+static cudaError_t launch_variant(const ConvTcParams& p, int grid, cudaStream_t stream) {
   static bool attr_done = false;
+  auto kern = abed_dev::conv_i8_tc_kernel<EPI, FC, FIC>;
   if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(abed_dev::conv_i8_tc_kernel,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 232448 - 1024);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, abed_dev::kConvDynSmemMax);
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
+  kern<<<grid, abed_dev::kConvThreads, conv_tc_smem_bytes(p), stream>>>(p);
+  return cudaGetLastError();
+}
+
+template <int EPI>
+static cudaError_t launch_epi(const ConvTcParams& p, int grid, cudaStream_t st) {
+  const bool fc = (p.check & abed_dev::CHECK_FC) != 0, fic = (p.check & abed_dev::CHECK_FIC) != 0;
+  if (fc && fic) return launch_variant<EPI, true, true>(p, grid, st);
+  if (fc) return launch_variant<EPI, true, false>(p, grid, st);
+  if (fic) return launch_variant<EPI, false, true>(p, grid, st);
+  return launch_variant<EPI, false, false>(p, grid, st);
+}
+
+cudaError_t conv_tc_launch(const ConvTcParams& p, int num_sms, cudaStream_t stream) {
   int grid;
   if (p.b_resident) {
     int per = num_sms / p.n_tiles;
@@ -466,8 +538,12 @@ cudaError_t conv_tc_launch(const ConvTcParams& p, int num_sms, cudaStream_t stre
     grid = p.m_tiles * p.n_tiles;
     if (grid > num_sms) grid = num_sms;
   }
-  abed_dev::conv_i8_tc_kernel<<<grid, abed_dev::kThreads, smem, stream>>>(p);
-  return cudaGetLastError();
+  switch (p.out_mode) {
+    case abed_dev::OUT_NONE: return launch_epi<abed_dev::EPI_NONE>(p, grid, stream);
+    case abed_dev::OUT_I8_PACKED: return launch_epi<abed_dev::EPI_PACKED>(p, grid, stream);
+    case abed_dev::OUT_I8_COMPARE: return launch_epi<abed_dev::EPI_COMPARE>(p, grid, stream);
+    default: return launch_epi<abed_dev::EPI_NCHW>(p, grid, stream);
+  }
 }
 
 }  // namespace abed_host

@@ -28,7 +28,8 @@ constexpr int kMaxTaps = 64;
 constexpr int kBlockM = 128;
 constexpr int kStages = 4;       // activation/filter stage ring depth
 constexpr int kStages_host = kStages;
-constexpr int kThreads = 192;     // 6 warps: producer, MMA, 4 x epilogue
+// dynamic smem cap for the conv kernel: 227 KB minus its static smem (bias, reductions)
+constexpr int kConvDynSmemMax = 232448 - 12288;
 
 enum OutMode : int {
   OUT_NONE = 0,        // checks only (no activation written)
@@ -66,6 +67,7 @@ struct ConvTcParams {
   const int8_t* act;
   int64_t plane_len;
   int n_phase, c16, gps, k_stages, strip_pix, ntaps;
+  int n_stages;  // depth of the smem stage ring actually used (<= kStages)
   int tap_phase[kMaxTaps];
   int tap_shift[kMaxTaps];
   // ---- B operand (packed filters, see pack_filters in conv_tc.cu)

@@ -328,7 +328,7 @@ __global__ void fic_finalize_kernel(const int64_t* __restrict__ part, int n, con
 __global__ void ic_finalize_kernel(const unsigned long long* __restrict__ ksum, const int8_t* __restrict__ f,
                                    const int32_t* __restrict__ ic, int64_t K, int64_t crs, abed_verify_outcome* out) {
   __shared__ int s_first;
-  __shared__ long long s_lhs, s_rhs, s_cnt;
+  __shared__ long long s_cnt;
   if (threadIdx.x == 0) { s_first = 0x7fffffff; s_cnt = 0; }
   __syncthreads();
   for (int64_t k = threadIdx.x; k < K; k += blockDim.x) {
@@ -367,49 +367,48 @@ int num_sms() {
   return g_num_sms;
 }
 
-static constexpr uint32_t kSmemBudget = 232448 - 2048;
+static constexpr uint32_t kSmemBudget = abed_dev::kConvDynSmemMax - 256;
 
 bool choose_tiling(const ActGeom& g, bool fc, int force_block_n, ConvTcParams& p) {
+  // SS-mode tcgen05 cost model (measured, tools/mma_microbench.cu): one
+  // M=128 x K=32 MMA costs max(~133, N/2) cycles (A-operand smem reads), so the
+  // widest N (<= 256 incl. the FC checksum rows) minimises the MMA count.
   const int ntaps = g.r * g.s;
   const int k_pad = (int)ceil_div(g.k, 16) * 16;
   const int strip = geom_strip_pix(g);
+  const int fcrows = fc ? 16 : 0;
   auto a_stage = [&](int gps) { return (uint32_t)g.n_phase * gps * strip * 16u; };
-  // 1) B resident in shared memory, one N tile per CTA
-  for (int bn = std::min(k_pad, 256); bn >= 64; bn -= 16) {
+  int best_tot = -1;
+  ConvTcParams best{};
+  for (int bn = std::min(k_pad, 256 - fcrows); bn >= 16; bn -= 16) {
     if (force_block_n && bn != force_block_n) continue;
     if (k_pad % bn) continue;
-    const int tot = bn + (fc ? 16 : 0);
-    if (tot > 256) continue;
-    const uint32_t bres = (uint32_t)tot * ntaps * g.c16 * 16u;
-    for (int gps : {4, 2}) {
-      if (g.c16 % gps) continue;
-      const uint32_t bytes = bres + abed_dev::kStages_host * a_stage(gps) + 512;
-      if (bytes > kSmemBudget) continue;
-      p.block_n = bn; p.block_n_tot = tot; p.gps = gps; p.b_resident = 1;
-      p.n_tiles = k_pad / bn;
-      p.k_stages = g.c16 / gps;
-      p.b_stage_bytes = (uint32_t)tot * ntaps * gps * 16u;
-      return true;
-    }
-  }
-  // 2) B streamed with the activation strips through the stage ring
-  for (int bn = std::min(k_pad, 256); bn >= 16; bn -= 16) {
-    if (force_block_n && bn != force_block_n) continue;
-    if (k_pad % bn) continue;
-    const int tot = bn + (fc ? 16 : 0);
+    const int tot = bn + fcrows;
     for (int gps : {4, 2}) {
       if (g.c16 % gps) continue;
       const uint32_t bstage = (uint32_t)tot * ntaps * gps * 16u;
-      const uint32_t bytes = abed_dev::kStages_host * (a_stage(gps) + bstage) + 512;
-      if (bytes > kSmemBudget) continue;
-      p.block_n = bn; p.block_n_tot = tot; p.gps = gps; p.b_resident = 0;
-      p.n_tiles = k_pad / bn;
-      p.k_stages = g.c16 / gps;
-      p.b_stage_bytes = bstage;
-      return true;
+      const uint32_t tab = 8u * ntaps * (gps / 2) + 512;
+      // resident B (a CTA keeps its N tile's filters in smem)
+      const uint32_t bres = bstage * (g.c16 / gps);
+      int stages_res = 0;
+      if (bres + tab < kSmemBudget) stages_res = std::min<int>(abed_dev::kStages, (kSmemBudget - bres - tab) / a_stage(gps));
+      const int stages_ring = std::min<int>(abed_dev::kStages, (kSmemBudget - tab) / (a_stage(gps) + bstage));
+      const bool res_ok = stages_res >= 2;
+      const bool ring_ok = stages_ring >= 2;
+      if (!res_ok && !ring_ok) continue;
+      if (tot <= best_tot) continue;
+      best_tot = tot;
+      best = p;
+      best.block_n = bn; best.block_n_tot = tot; best.gps = gps; best.n_tiles = k_pad / bn;
+      best.k_stages = g.c16 / gps; best.b_stage_bytes = bstage;
+      best.b_resident = res_ok ? 1 : 0;
+      best.n_stages = res_ok ? stages_res : stages_ring;
+      break;  // gps=4 preferred (fewer, larger bulk copies)
     }
   }
-  return false;
+  if (best_tot < 0) return false;
+  p = best;
+  return true;
 }
 
 }  // namespace abed_host
