@@ -52,6 +52,22 @@ cudaError_t conv_tc_launch(const abed_dev::ConvTcParams& p, int num_sms, cudaStr
 
 }  // namespace abed_host
 
+struct abed_conv_plan;
+namespace abed_host {
+// abi_core.cu
+int set_error(int code, const std::string& msg);
+void require_device();
+int grid_for(int64_t n, int threads);
+void validate_shape(const abed_layer_shape& s);
+abed_conv_plan* plan_create(const abed_layer_shape& shape, const int8_t* filters, int checks, int force_bn);
+void plan_run(abed_conv_plan* pl, const int8_t* packed, const abed_epilog_params* ep, int out_mode, void* out,
+              const abed_conv_plan* next, int64_t fault_key, int fault_bit, cudaStream_t st);
+void plan_finalize(abed_conv_plan* pl, abed_verify_outcome* out_dev, cudaStream_t st);
+// ref_kernels.cu
+void dev_gen_input_checksum(const int8_t* x, const abed_layer_shape& s, int32_t* sums, cudaStream_t st);
+void dev_epilog(const int32_t* in, abed_dims4 d, const abed_epilog_params* p, void* out, cudaStream_t st);
+}  // namespace abed_host
+
 // opaque plan (C ABI handle)
 struct abed_conv_plan {
   abed_layer_shape shape;
@@ -68,4 +84,8 @@ struct abed_conv_plan {
   int64_t* d_fic_part = nullptr;
   unsigned long long* d_acc = nullptr;  // [0]=fic rhs, [1]=cmp count, [2..3]=fc scratch, [4..4+K) ic sums
   float* d_zero_bias = nullptr;
+  // when set, runs skip the input-checksum kernels and keep d_ic / the FIC
+  // right-hand side of an earlier run (fault campaigns: checksums come from
+  // the pristine input, faults.hpp:111-115)
+  int reuse_input_checksum = 0;
 };

@@ -174,7 +174,7 @@ void plan_run(abed_conv_plan* pl, const int8_t* packed, const abed_epilog_params
   p.fault_bit = fault_bit;
   if (pl->checks & ABED_CHECK_IC) cuda_check(cudaMemsetAsync(pl->d_acc + 4, 0, pl->shape.k * 8, st), "memset ic");
   if (out_mode == ABED_OUT_I8_COMPARE) cuda_check(cudaMemsetAsync(pl->d_acc + 1, 0, 8, st), "memset cmp");
-  if (pl->checks & (ABED_CHECK_FIC | ABED_CHECK_IC)) {
+  if ((pl->checks & (ABED_CHECK_FIC | ABED_CHECK_IC)) && !pl->reuse_input_checksum) {
     // input checksum of the pristine input, ahead of the convolution (FR option)
     const ActGeom& g = pl->g;
     cuda_check(cudaMemsetAsync(pl->d_acc, 0, 8, st), "memset rhs");

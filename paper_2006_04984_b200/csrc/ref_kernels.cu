@@ -1,0 +1,617 @@
+// C ABI: the reference-facing L0-L2 functions other than the tensor-core conv.
+// Each kernel restates one reference function on the device; integer
+// reductions are exact (order-independent) and float-mode reductions keep the
+// reference's sequential order so results are bit-identical to its -march=native
+// build (FMA contraction spelled out with fma/fmaf).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <type_traits>
+#include <vector>
+
+#include "abed_internal.h"
+
+using namespace abed_host;
+
+namespace abed_host {
+int grid_for(int64_t n, int threads);
+void require_device();
+void validate_shape(const abed_layer_shape& s);
+}  // namespace abed_host
+
+namespace {
+
+constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ULL;
+
+__host__ __device__ inline uint64_t mix64(uint64_t z) {  // rng.hpp:16-19
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+// ------------------------------------------------------------------- rng
+// fill_random_i8 (rng.hpp:46): element i of a stream is mix(seed + (i+1)*golden),
+// so the fill is embarrassingly parallel.
+__global__ void fill_i8_kernel(int8_t* t, int64_t n, uint64_t seed, uint64_t off, int extreme) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t v = mix64(seed + (uint64_t)(off + i + 1) * kGolden);
+    t[i] = extreme ? ((v & 1) ? (int8_t)127 : (int8_t)-128) : (int8_t)(v & 0xFF);
+  }
+}
+
+// ------------------------------------------------------------- direct conv
+// conv_reference (convolution.hpp:78-111) for the widened instantiations the
+// reference uses off the int8 hot path; one thread per output, window walked in
+// (c,r,s) order.
+template <typename TX, typename TW, typename TA>
+__global__ void conv_direct_kernel(const TX* __restrict__ x, const TW* __restrict__ f, abed_layer_shape s,
+                                   TA* __restrict__ out) {
+  const int64_t total = s.n * s.k * s.p * s.q;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t q = idx % s.q, p = (idx / s.q) % s.p, k = (idx / (s.q * s.p)) % s.k, n = idx / (s.q * s.p * s.k);
+    TA acc = 0;
+    for (int64_t c = 0; c < s.c; ++c)
+      for (int64_t r = 0; r < s.r; ++r) {
+        const int64_t hi = p * s.stride_h - s.pad_h + r;
+        if (hi < 0 || hi >= s.h) continue;
+        for (int64_t ss = 0; ss < s.s; ++ss) {
+          const int64_t wi = q * s.stride_w - s.pad_w + ss;
+          if (wi < 0 || wi >= s.w) continue;
+          const TA xv = (TA)x[((n * s.c + c) * s.h + hi) * s.w + wi];
+          const TA fv = (TA)f[((k * s.c + c) * s.r + r) * s.s + ss];
+          if constexpr (std::is_same<TA, float>::value) acc = __fmaf_rn(xv, fv, acc);
+          else acc += xv * fv;
+        }
+      }
+    out[idx] = acc;
+  }
+}
+
+// conv_checksum_planes (checksum.hpp:134-176): 4 plane filters, planes 0-2 as u8, 3 as s8
+__global__ void planes_conv_kernel(const int8_t* __restrict__ x, abed_layer_shape s, const int8_t* __restrict__ planes,
+                                   int32_t* __restrict__ extra) {
+  const int64_t npq = s.n * s.p * s.q, crs = s.c * s.r * s.s;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < npq; j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t q = j % s.q, p = (j / s.q) % s.p, n = j / (s.q * s.p);
+    uint32_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+    for (int64_t c = 0; c < s.c; ++c)
+      for (int64_t r = 0; r < s.r; ++r) {
+        const int64_t hi = p * s.stride_h - s.pad_h + r;
+        if (hi < 0 || hi >= s.h) continue;
+        for (int64_t ss = 0; ss < s.s; ++ss) {
+          const int64_t wi = q * s.stride_w - s.pad_w + ss;
+          if (wi < 0 || wi >= s.w) continue;
+          const int32_t xv = x[((n * s.c + c) * s.h + hi) * s.w + wi];
+          const int64_t i = (c * s.r + r) * s.s + ss;
+          a0 += (uint32_t)(xv * (int32_t)(uint8_t)planes[i]);
+          a1 += (uint32_t)(xv * (int32_t)(uint8_t)planes[crs + i]);
+          a2 += (uint32_t)(xv * (int32_t)(uint8_t)planes[2 * crs + i]);
+          a3 += (uint32_t)(xv * (int32_t)planes[3 * crs + i]);
+        }
+      }
+    extra[j] = (int32_t)a0;
+    extra[npq + j] = (int32_t)a1;
+    extra[2 * npq + j] = (int32_t)a2;
+    extra[3 * npq + j] = (int32_t)a3;
+  }
+}
+
+// ------------------------------------------------------------------ epilog
+__global__ void epilog_kernel(const int32_t* __restrict__ in, abed_dims4 d, float scale, const float* __restrict__ bias,
+                              int relu, int f32out, void* __restrict__ out) {
+  const int64_t total = d.d0 * d.d1 * d.d2 * d.d3, pq = d.d2 * d.d3;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = (i / pq) % d.d1;
+    float v = __fmaf_rn((float)in[i], scale, bias[k]);  // convolution.hpp:374 (FMA-contracted)
+    if (relu && v < 0.0f) v = 0.0f;
+    if (f32out) {
+      static_cast<float*>(out)[i] = v;
+    } else {
+      v = fminf(127.0f, fmaxf(-128.0f, v));
+      static_cast<int8_t*>(out)[i] = (int8_t)truncf(v);
+    }
+  }
+}
+
+// ---------------------------------------------------------- checksum kernels
+__global__ void decompose_kernel(const int32_t* __restrict__ sums, int64_t n, int8_t* __restrict__ planes) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t u = (uint32_t)sums[i];  // checksum.hpp:93-97
+    for (int b = 0; b < 4; ++b) planes[b * n + i] = (int8_t)(uint8_t)(u >> (8 * b));
+  }
+}
+__global__ void recombine_kernel(const int32_t* __restrict__ e, int64_t n, int64_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (int64_t)e[i] + ((int64_t)e[n + i] << 8) + ((int64_t)e[2 * n + i] << 16) + ((int64_t)e[3 * n + i] << 24);
+}
+__global__ void batch_sum_nchw_kernel(const int8_t* __restrict__ x, abed_dims4 d, int32_t* __restrict__ out) {
+  const int64_t chw = d.d1 * d.d2 * d.d3;  // checksum.hpp:350-362
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < chw; i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t acc = 0;
+    for (int64_t n = 0; n < d.d0; ++n) acc += x[n * chw + i];
+    out[i] = acc;
+  }
+}
+// gen_input_checksum (checksum.hpp:248-266) from the batch-summed image: one
+// block per (c, r, s), lattice sum over every window position.
+__global__ void input_checksum_kernel(const int32_t* __restrict__ bsum, abed_layer_shape s, int32_t* __restrict__ ic) {
+  const int64_t crs = s.c * s.r * s.s;
+  for (int64_t e = blockIdx.x; e < crs; e += gridDim.x) {
+    const int64_t c = e / (s.r * s.s), r = (e / s.s) % s.r, ss = e % s.s;
+    int32_t acc = 0;
+    for (int64_t t = threadIdx.x; t < s.p * s.q; t += blockDim.x) {
+      const int64_t p = t / s.q, q = t % s.q;
+      const int64_t hi = p * s.stride_h - s.pad_h + r, wi = q * s.stride_w - s.pad_w + ss;
+      if (hi >= 0 && hi < s.h && wi >= 0 && wi < s.w) acc += bsum[(c * s.h + hi) * s.w + wi];
+    }
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    __shared__ int32_t red[32];
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int32_t tot = 0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += red[w];
+      ic[e] = tot;
+    }
+    __syncthreads();
+  }
+}
+__global__ void reduce_i64_kernel(const int32_t* __restrict__ c, int64_t n, unsigned long long* __restrict__ out,
+                                  unsigned int* __restrict__ wrap32) {
+  long long s = 0;
+  uint32_t w = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    s += c[i];
+    w += (uint32_t)c[i];
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+    w += __shfl_xor_sync(0xffffffffu, w, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(out, (unsigned long long)s);
+    atomicAdd(wrap32, w);
+  }
+}
+__global__ void dot_i64_kernel(const int32_t* __restrict__ a, const int32_t* __restrict__ b, int64_t n,
+                               unsigned long long* __restrict__ out) {
+  long long s = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    s += (long long)a[i] * b[i];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(out, (unsigned long long)s);
+}
+
+// First-mismatch search: key = reference loop position; atomicMin gives the
+// first locus, atomicAdd the mismatch count (both exact and deterministic).
+struct Mism {
+  unsigned long long first;
+  unsigned long long count;
+};
+__global__ void fc_verify_kernel(const int32_t* __restrict__ cv, abed_dims4 d, const int64_t* __restrict__ ev,
+                                 int64_t k_lim, Mism* m) {
+  const int64_t pq = d.d2 * d.d3, rows = d.d0 * pq;  // checksum.hpp:224-234 order (n, j)
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < rows; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n = t / pq, j = t % pq;
+    long long sum = 0;
+    for (int64_t k = 0; k < k_lim; ++k) sum += cv[(n * d.d1 + k) * pq + j];
+    if (sum != ev[t]) {
+      atomicMin(&m->first, (unsigned long long)t);
+      atomicAdd(&m->count, 1ull);
+    }
+  }
+}
+__global__ void icb_verify_kernel(const int32_t* __restrict__ cv, abed_dims4 d, const int64_t* __restrict__ ev, Mism* m) {
+  const int64_t kpq = d.d1 * d.d2 * d.d3;  // checksum.hpp:409-419 order (k,p,q)
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < kpq; i += (int64_t)gridDim.x * blockDim.x) {
+    long long sum = 0;
+    for (int64_t n = 0; n < d.d0; ++n) sum += cv[n * kpq + i];
+    if (sum != ev[i]) {
+      atomicMin(&m->first, (unsigned long long)i);
+      atomicAdd(&m->count, 1ull);
+    }
+  }
+}
+// ic_verify_k: one block per k: out_sum over (n, j) and dot(f[k], ic)
+__global__ void ick_sums_kernel(const int32_t* __restrict__ cv, abed_dims4 d, const int8_t* __restrict__ f, int64_t crs,
+                                const int32_t* __restrict__ ic, long long* __restrict__ lhs, long long* __restrict__ rhs) {
+  const int64_t k = blockIdx.x, pq = d.d2 * d.d3;
+  long long s = 0, dot = 0;
+  for (int64_t t = threadIdx.x; t < d.d0 * pq; t += blockDim.x) s += cv[((t / pq) * d.d1 + k) * pq + t % pq];
+  for (int64_t i = threadIdx.x; i < crs; i += blockDim.x) dot += (long long)f[k * crs + i] * ic[i];
+  for (int o = 16; o > 0; o >>= 1) {
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+    dot += __shfl_xor_sync(0xffffffffu, dot, o);
+  }
+  __shared__ long long rs[32], rd[32];
+  if ((threadIdx.x & 31) == 0) { rs[threadIdx.x >> 5] = s; rd[threadIdx.x >> 5] = dot; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long a = 0, b = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { a += rs[w]; b += rd[w]; }
+    lhs[k] = a;
+    rhs[k] = b;
+  }
+}
+
+// ------------------------------------------------------------- float mode
+// Sequential reductions (single thread per output) keep the reference's order.
+__global__ void filter_sum_f64_kernel(const float* __restrict__ f, abed_dims4 fd, double* __restrict__ out) {
+  const int64_t crs = fd.d1 * fd.d2 * fd.d3;  // checksum.hpp:483-494
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < crs; i += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int64_t k = 0; k < fd.d0; ++k) s += (double)f[k * crs + i];
+    out[i] = s;
+  }
+}
+__global__ void input_sum_f64_kernel(const float* __restrict__ x, abed_layer_shape s, double* __restrict__ out) {
+  const int64_t crs = s.c * s.r * s.s;  // checksum.hpp:496-522, additions in (n, p, q) order
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < crs; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = e / (s.r * s.s), r = (e / s.s) % s.r, ss = e % s.s;
+    double acc = 0.0;
+    for (int64_t n = 0; n < s.n; ++n)
+      for (int64_t p = 0; p < s.p; ++p) {
+        const int64_t hi = p * s.stride_h - s.pad_h + r;
+        if (hi < 0 || hi >= s.h) continue;
+        for (int64_t q = 0; q < s.q; ++q) {
+          const int64_t wi = q * s.stride_w - s.pad_w + ss;
+          if (wi < 0 || wi >= s.w) continue;
+          acc += (double)x[((n * s.c + c) * s.h + hi) * s.w + wi];
+        }
+      }
+    out[e] = acc;
+  }
+}
+__global__ void seq_f64_kernel(const float* __restrict__ c, int64_t n, double* out) {
+  if (blockIdx.x || threadIdx.x) return;  // checksum.hpp:524-528
+  double s = 0.0;
+  for (int64_t i = 0; i < n; ++i) s += (double)c[i];
+  *out = s;
+}
+__global__ void dot_f64_kernel(const double* __restrict__ a, const double* __restrict__ b, int64_t n, double* out) {
+  if (blockIdx.x || threadIdx.x) return;  // checksum.hpp:530-535 (acc += a*b -> fma)
+  double s = 0.0;
+  for (int64_t i = 0; i < n; ++i) s = fma(a[i], b[i], s);
+  *out = s;
+}
+__global__ void fc_rows_f64_kernel(const float* __restrict__ cv, abed_dims4 d, const float* __restrict__ ev, double* lhs,
+                                   double* rhs) {
+  const int64_t pq = d.d2 * d.d3, rows = d.d0 * pq;  // checksum.hpp:551-556
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < rows; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t n = t / pq, j = t % pq;
+    double s = 0.0;
+    for (int64_t k = 0; k < d.d1; ++k) s += (double)cv[(n * d.d1 + k) * pq + j];
+    lhs[t] = s;
+    rhs[t] = (double)ev[t];
+  }
+}
+__global__ void ick_f64_kernel(const float* __restrict__ cv, abed_dims4 d, const float* __restrict__ f, int64_t crs,
+                               const double* __restrict__ ic, double* lhs, double* rhs) {
+  const int64_t pq = d.d2 * d.d3;  // checksum.hpp:579-587, per k sequential
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < d.d1; k += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0, dot = 0.0;
+    for (int64_t n = 0; n < d.d0; ++n)
+      for (int64_t j = 0; j < pq; ++j) s += (double)cv[(n * d.d1 + k) * pq + j];
+    for (int64_t i = 0; i < crs; ++i) dot = fma((double)f[k * crs + i], ic[i], dot);
+    lhs[k] = s;
+    rhs[k] = dot;
+  }
+}
+
+__global__ void flip_kernel(uint8_t* data, int64_t byte, uint8_t mask) { data[byte] ^= mask; }
+
+// ------------------------------------------------------------- helpers
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  explicit DevBuf(size_t n) { cuda_check(cudaMalloc(&p, (n ? n : 1) * sizeof(T)), "cudaMalloc(tmp)"); }
+  ~DevBuf() { cudaFree(p); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+};
+template <typename T>
+T d2h(const T* d) {
+  T h;
+  cuda_check(cudaMemcpy(&h, d, sizeof(T), cudaMemcpyDeviceToHost), "d2h");
+  return h;
+}
+void sync() { cuda_check(cudaDeviceSynchronize(), "synchronize"); }
+void launched(const char* what) { cuda_check(cudaGetLastError(), what); }
+int64_t count4(abed_dims4 d) { return d.d0 * d.d1 * d.d2 * d.d3; }
+void check_dims(abed_dims4 d) {
+  if (d.d0 < 1 || d.d1 < 1 || d.d2 < 1 || d.d3 < 1) throw_invalid("Tensor4D: all extents must be >= 1");
+}
+void set_fail(abed_verify_outcome* o, int64_t lhs, int64_t rhs, bool locus, int64_t l0, int64_t l1, int64_t l2,
+              int64_t count) {
+  std::memset(o, 0, sizeof(*o));
+  o->status = 1;
+  o->lhs = lhs;
+  o->rhs = rhs;
+  o->has_locus = locus ? 1 : 0;
+  o->locus[0] = l0; o->locus[1] = l1; o->locus[2] = l2;
+  o->error_count = count;
+}
+void set_ok(abed_verify_outcome* o) { std::memset(o, 0, sizeof(*o)); }
+int ceil_log2_host(int64_t v) {
+  int bits = 0;
+  uint64_t u = (uint64_t)v - 1;
+  while (u) { ++bits; u >>= 1; }
+  return bits;
+}
+void float_verify_host(double lhs, double rhs, double tau, abed_verify_outcome* o) {
+  if (!(tau >= 0.0)) throw_invalid("float_verify: tau must be >= 0");  // checksum.hpp:474-481
+  std::memset(o, 0, sizeof(*o));
+  o->lhs_f = lhs;
+  o->rhs_f = rhs;
+  if (!(std::fabs(lhs - rhs) <= tau)) { o->status = 1; o->error_count = 1; }
+}
+
+}  // namespace
+
+namespace abed_host {
+int set_error(int code, const std::string& msg);
+template <typename Fn>
+int guarded2(Fn&& fn) {
+  try {
+    fn();
+    return ABED_OK;
+  } catch (const AbedError& e) {
+    return set_error(e.code, e.what());
+  } catch (const std::exception& e) {
+    return set_error(ABED_ERR_RUNTIME, e.what());
+  }
+}
+// exported to campaign.cu / abi_core.cu
+void dev_gen_input_checksum(const int8_t* x, const abed_layer_shape& s, int32_t* sums, cudaStream_t st) {
+  if (8 + ceil_log2_host(s.n * s.p * s.q) > 32)
+    throw_invalid("gen_input_checksum: PQN too large for i32 checksums; a wider plan is required");
+  DevBuf<int32_t> b((size_t)(s.c * s.h * s.w));
+  batch_sum_nchw_kernel<<<grid_for(s.c * s.h * s.w, 256), 256, 0, st>>>(x, abed_dims4{s.n, s.c, s.h, s.w}, b.p);
+  input_checksum_kernel<<<(int)std::min<int64_t>(s.c * s.r * s.s, 65535), 256, 0, st>>>(b.p, s, sums);
+  launched("gen_input_checksum");
+  cuda_check(cudaStreamSynchronize(st), "gen_input_checksum sync");
+}
+void dev_epilog(const int32_t* in, abed_dims4 d, const abed_epilog_params* p, void* out, cudaStream_t st) {
+  check_dims(d);
+  if (p->bias_len != d.d1) throw_invalid("epilog: bias length must equal the channel count");
+  if (!std::isfinite(p->scale)) throw_invalid("epilog: non-finite scale");
+  if (p->bias_len > 0) {
+    std::vector<float> hb((size_t)p->bias_len);
+    cuda_check(cudaMemcpy(hb.data(), p->bias, hb.size() * 4, cudaMemcpyDeviceToHost), "bias d2h");
+    for (float b : hb)
+      if (!std::isfinite(b)) throw_invalid("epilog: non-finite bias");
+  }
+  if (p->output_kind != ABED_I8 && p->output_kind != ABED_F32) throw_invalid("epilog: output kind must be i8 or f32");
+  epilog_kernel<<<grid_for(count4(d), 256), 256, 0, st>>>(in, d, p->scale, p->bias, p->activation == ABED_RELU,
+                                                           p->output_kind == ABED_F32, out);
+  launched("epilog");
+}
+}  // namespace abed_host
+
+#define GUARD(...) return guarded2([&] { require_device(); __VA_ARGS__; })
+
+extern "C" {
+
+uint64_t abed_derive_seed(uint64_t root, uint64_t index) {  // rng.hpp:41-44
+  return mix64((root ^ (0xA02E9D4BD1C96D4FULL + index * kGolden)) + kGolden);
+}
+int abed_fill_random_i8(int8_t* t, int64_t n, uint64_t seed, uint64_t off, void* stream) {
+  GUARD(fill_i8_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(t, n, seed, off, 0); launched("fill_random_i8"));
+}
+int abed_fill_random_extreme(int8_t* t, int64_t n, uint64_t seed, uint64_t off, void* stream) {
+  GUARD(fill_i8_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(t, n, seed, off, 1); launched("fill_random_extreme"));
+}
+
+int abed_conv_f32(const float* x, const float* f, const abed_layer_shape* s, float* out, void* stream) {
+  GUARD(validate_shape(*s);
+        conv_direct_kernel<float, float, float><<<grid_for(s->n * s->k * s->p * s->q, 128), 128, 0, (cudaStream_t)stream>>>(x, f, *s, out);
+        launched("conv_f32"); cuda_check(cudaStreamSynchronize((cudaStream_t)stream), "conv_f32"));
+}
+int abed_epilog(const int32_t* convout, abed_dims4 d, const abed_epilog_params* p, void* out, void* stream) {
+  GUARD(dev_epilog(convout, d, p, out, (cudaStream_t)stream));
+}
+int abed_gen_filter_checksum(const int8_t* f, abed_dims4 fd, int32_t* sums, void* stream) {
+  GUARD(check_dims(fd);
+        if (fd.d0 > (int64_t(1) << 24)) throw_invalid("gen_filter_checksum: K too large for i32 checksums");
+        const int64_t crs = fd.d1 * fd.d2 * fd.d3;
+        filter_sum_kernel<<<grid_for(crs, 256), 256, 0, (cudaStream_t)stream>>>(f, fd.d0, crs, sums);
+        launched("gen_filter_checksum"));
+}
+int abed_decompose_checksum_filters(const int32_t* sums, int64_t n, int8_t* planes, void* stream) {
+  GUARD(decompose_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(sums, n, planes); launched("decompose"));
+}
+int abed_conv_checksum_planes(const int8_t* x, const abed_layer_shape* s, const int8_t* planes, int32_t* extra, void* stream) {
+  GUARD(validate_shape(*s);
+        if (s->c * s->r * s->s > 65536) throw_invalid("conv_checksum_planes: CRS > 65536 exceeds the i32 plan");
+        planes_conv_kernel<<<grid_for(s->n * s->p * s->q, 128), 128, 0, (cudaStream_t)stream>>>(x, *s, planes, extra);
+        launched("conv_checksum_planes"));
+}
+int abed_recombine_extra_fmaps(const int32_t* e, int64_t n, int64_t* out, void* stream) {
+  GUARD(recombine_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(e, n, out); launched("recombine"));
+}
+int abed_conv_filter_checksum(const int8_t* x, const abed_layer_shape* s, const int32_t* sums, int64_t* out, void* stream) {
+  GUARD(validate_shape(*s); abed_layer_shape one = *s; one.k = 1;
+        conv_direct_kernel<int8_t, int32_t, int64_t><<<grid_for(s->n * s->p * s->q, 128), 128, 0, (cudaStream_t)stream>>>(x, sums, one, out);
+        launched("conv_filter_checksum"));
+}
+int abed_fc_verify(const int32_t* cv, abed_dims4 d, const int64_t* extra, int64_t original_k, abed_verify_outcome* o) {
+  GUARD(check_dims(d);
+        const int64_t k_lim = original_k < 0 ? d.d1 : original_k;
+        if (k_lim < 1 || k_lim > d.d1) throw_invalid("fc_verify: bad original_k");
+        DevBuf<Mism> m(1); const Mism init{~0ull, 0ull};
+        cuda_check(cudaMemcpy(m.p, &init, sizeof(init), cudaMemcpyHostToDevice), "h2d");
+        fc_verify_kernel<<<grid_for(d.d0 * d.d2 * d.d3, 256), 256>>>(cv, d, extra, k_lim, m.p); launched("fc_verify");
+        const Mism r = d2h(m.p);
+        if (r.count == 0) { set_ok(o); return; }
+        const int64_t t = (int64_t)r.first, pq = d.d2 * d.d3, n = t / pq, j = t % pq;
+        // lhs/rhs at the first mismatch, recomputed exactly on the host from two small reads
+        std::vector<int32_t> col((size_t)k_lim);
+        for (int64_t k = 0; k < k_lim; ++k)
+          cuda_check(cudaMemcpy(&col[(size_t)k], cv + (n * d.d1 + k) * pq + j, 4, cudaMemcpyDeviceToHost), "d2h");
+        int64_t lhs = 0; for (int32_t v : col) lhs += v;
+        const int64_t rhs = d2h(extra + t);
+        set_fail(o, lhs, rhs, true, n, j / d.d3, j % d.d3, (int64_t)r.count));
+}
+int abed_gen_input_checksum(const int8_t* x, const abed_layer_shape* s, int32_t* sums, void* stream) {
+  GUARD(validate_shape(*s); dev_gen_input_checksum(x, *s, sums, (cudaStream_t)stream));
+}
+int abed_reduce_all_i64(const int32_t* c, int64_t n, int64_t* result) {
+  GUARD(DevBuf<unsigned long long> acc(2); cuda_check(cudaMemset(acc.p, 0, 16), "memset");
+        reduce_i64_kernel<<<grid_for(n, 256), 256>>>(c, n, acc.p, reinterpret_cast<unsigned int*>(acc.p + 1));
+        launched("reduce_all_i64"); *result = (int64_t)d2h(acc.p));
+}
+int abed_reduce_all_wrap32(const int32_t* c, int64_t n, int32_t* result) {
+  GUARD(DevBuf<unsigned long long> acc(2); cuda_check(cudaMemset(acc.p, 0, 16), "memset");
+        reduce_i64_kernel<<<grid_for(n, 256), 256>>>(c, n, acc.p, reinterpret_cast<unsigned int*>(acc.p + 1));
+        launched("reduce_all_wrap32"); *result = (int32_t)d2h(reinterpret_cast<unsigned int*>(acc.p + 1)));
+}
+int abed_fic_dot(const int32_t* fc, const int32_t* ic, int64_t n, int64_t* result) {
+  GUARD(DevBuf<unsigned long long> acc(1); cuda_check(cudaMemset(acc.p, 0, 8), "memset");
+        dot_i64_kernel<<<grid_for(n, 256), 256>>>(fc, ic, n, acc.p); launched("fic_dot");
+        *result = (int64_t)d2h(acc.p));
+}
+static void fic_common(const int32_t* c, int64_t n, int64_t expected, abed_verify_outcome* o, bool forced32) {
+  DevBuf<unsigned long long> acc(2);
+  cuda_check(cudaMemset(acc.p, 0, 16), "memset");
+  reduce_i64_kernel<<<grid_for(n, 256), 256>>>(c, n, acc.p, reinterpret_cast<unsigned int*>(acc.p + 1));
+  launched("fic_verify");
+  const int64_t sum = forced32 ? (int64_t)(int32_t)d2h(reinterpret_cast<unsigned int*>(acc.p + 1)) : (int64_t)d2h(acc.p);
+  if (sum != expected) {
+    set_fail(o, sum, expected, false, 0, 0, 0, 1);
+  } else {
+    set_ok(o);  // checksum.hpp:290-293: Pass reports lhs = rhs = sum
+    o->lhs = sum;
+    o->rhs = expected;
+  }
+}
+int abed_fic_verify(const int32_t* c, int64_t n, int64_t expected, abed_verify_outcome* o) {
+  GUARD(fic_common(c, n, expected, o, false));
+}
+int abed_fic_verify_forced32(const int32_t* c, int64_t n, int64_t expected, abed_verify_outcome* o) {
+  GUARD(fic_common(c, n, expected, o, true));
+}
+int abed_ic_verify_k(const int32_t* cv, abed_dims4 d, const int8_t* f, abed_dims4 fd, const int32_t* ic, abed_verify_outcome* o) {
+  GUARD(check_dims(d); check_dims(fd);
+        if (fd.d0 != d.d1) throw_invalid("ic_verify_k: filter count does not match convout");
+        const int64_t crs = fd.d1 * fd.d2 * fd.d3;
+        DevBuf<long long> lhs((size_t)d.d1), rhs((size_t)d.d1);
+        ick_sums_kernel<<<(unsigned)d.d1, 256>>>(cv, d, f, crs, ic, lhs.p, rhs.p); launched("ic_verify_k");
+        std::vector<long long> hl((size_t)d.d1), hr((size_t)d.d1);
+        cuda_check(cudaMemcpy(hl.data(), lhs.p, hl.size() * 8, cudaMemcpyDeviceToHost), "d2h");
+        cuda_check(cudaMemcpy(hr.data(), rhs.p, hr.size() * 8, cudaMemcpyDeviceToHost), "d2h");
+        int64_t first = -1, cnt = 0;
+        for (int64_t k = 0; k < d.d1; ++k) if (hl[(size_t)k] != hr[(size_t)k]) { if (first < 0) first = k; ++cnt; }
+        if (first < 0) set_ok(o); else set_fail(o, hl[(size_t)first], hr[(size_t)first], true, first, -1, -1, cnt));
+}
+int abed_ic_batch_checksum(const int8_t* x, abed_dims4 d, int32_t* out, void* stream) {
+  GUARD(check_dims(d);
+        batch_sum_nchw_kernel<<<grid_for(d.d1 * d.d2 * d.d3, 256), 256, 0, (cudaStream_t)stream>>>(x, d, out);
+        launched("ic_batch_checksum"));
+}
+int abed_ic_batch_verify(const int32_t* cv, abed_dims4 d, const int64_t* extra, abed_verify_outcome* o) {
+  GUARD(check_dims(d);
+        DevBuf<Mism> m(1); const Mism init{~0ull, 0ull};
+        cuda_check(cudaMemcpy(m.p, &init, sizeof(init), cudaMemcpyHostToDevice), "h2d");
+        icb_verify_kernel<<<grid_for(d.d1 * d.d2 * d.d3, 256), 256>>>(cv, d, extra, m.p); launched("ic_batch_verify");
+        const Mism r = d2h(m.p);
+        if (r.count == 0) { set_ok(o); return; }
+        const int64_t i = (int64_t)r.first, kpq = d.d1 * d.d2 * d.d3, pq = d.d2 * d.d3;
+        int64_t lhs = 0;
+        for (int64_t n = 0; n < d.d0; ++n) lhs += d2h(cv + n * kpq + i);
+        set_fail(o, lhs, d2h(extra + i), true, i / pq, (i % pq) / d.d3, i % d.d3, (int64_t)r.count));
+}
+int abed_plan_precision(const abed_layer_shape* s, int32_t b, abed_precision_plan* p) {
+  return guarded2([&] {  // checksum.hpp:451-468 (host arithmetic only)
+    if (b != 4 && b != 8) throw_invalid("plan_precision: operand width must be 4 or 8 bits");
+    const int64_t crs = s->c * s->r * s->s, npq = s->n * s->p * s->q;
+    auto kind = [](int bits) {
+      if (bits <= 32) return (int32_t)ABED_I32;
+      if (bits <= 64) return (int32_t)ABED_I64;
+      throw_invalid("plan_precision: requirement exceeds 64 bits");
+    };
+    std::memset(p, 0, sizeof(*p));
+    p->operand_bits = b;
+    p->bits_output_fmap = 2 * b + ceil_log2_host(crs);
+    p->bits_reduced_fc = 2 * b + ceil_log2_host(crs * s->k);
+    p->bits_reduced_fic = 2 * b + ceil_log2_host(npq * s->k * crs);
+    p->bits_filter_checksum = b + ceil_log2_host(s->k);
+    p->bits_input_checksum = b + ceil_log2_host(npq);
+    p->output_fmap_kind = kind(p->bits_output_fmap);
+    p->reduced_fc_kind = kind(p->bits_reduced_fc);
+    p->reduced_fic_kind = kind(p->bits_reduced_fic);
+    p->filter_checksum_kind = kind(p->bits_filter_checksum);
+    p->input_checksum_kind = kind(p->bits_input_checksum);
+  });
+}
+
+// ------------------------------------------------------------- float mode
+int abed_float_verify(double lhs, double rhs, double tau, abed_verify_outcome* o) {
+  return guarded2([&] { float_verify_host(lhs, rhs, tau, o); });
+}
+int abed_filter_checksum_f64(const float* f, abed_dims4 fd, double* sums, void* stream) {
+  GUARD(check_dims(fd);
+        filter_sum_f64_kernel<<<grid_for(fd.d1 * fd.d2 * fd.d3, 128), 128, 0, (cudaStream_t)stream>>>(f, fd, sums);
+        launched("filter_checksum_f64"));
+}
+int abed_input_checksum_f64(const float* x, const abed_layer_shape* s, double* sums, void* stream) {
+  GUARD(validate_shape(*s);
+        input_sum_f64_kernel<<<grid_for(s->c * s->r * s->s, 64), 64, 0, (cudaStream_t)stream>>>(x, *s, sums);
+        launched("input_checksum_f64"));
+}
+int abed_reduce_all_f64(const float* c, int64_t n, double* result) {
+  GUARD(DevBuf<double> r(1); seq_f64_kernel<<<1, 1>>>(c, n, r.p); launched("reduce_all_f64"); *result = d2h(r.p));
+}
+int abed_fic_dot_f64(const double* a, const double* b, int64_t n, double* result) {
+  GUARD(DevBuf<double> r(1); dot_f64_kernel<<<1, 1>>>(a, b, n, r.p); launched("fic_dot_f64"); *result = d2h(r.p));
+}
+int abed_fic_verify_f32(const float* c, int64_t n, double expected, double tau, abed_verify_outcome* o) {
+  GUARD(DevBuf<double> r(1); seq_f64_kernel<<<1, 1>>>(c, n, r.p); launched("fic_verify_f32");
+        float_verify_host(d2h(r.p), expected, tau, o));
+}
+int abed_fc_verify_f32(const float* cv, abed_dims4 d, const float* extra, double tau, abed_verify_outcome* o) {
+  GUARD(check_dims(d);
+        const int64_t rows = d.d0 * d.d2 * d.d3;
+        DevBuf<double> l((size_t)rows), r((size_t)rows);
+        fc_rows_f64_kernel<<<grid_for(rows, 256), 256>>>(cv, d, extra, l.p, r.p); launched("fc_verify_f32");
+        std::vector<double> hl((size_t)rows), hr((size_t)rows);
+        cuda_check(cudaMemcpy(hl.data(), l.p, (size_t)rows * 8, cudaMemcpyDeviceToHost), "d2h");
+        cuda_check(cudaMemcpy(hr.data(), r.p, (size_t)rows * 8, cudaMemcpyDeviceToHost), "d2h");
+        const int64_t pq = d.d2 * d.d3;
+        for (int64_t t = 0; t < rows; ++t)
+          if (!(std::fabs(hl[(size_t)t] - hr[(size_t)t]) <= tau)) {
+            float_verify_host(hl[(size_t)t], hr[(size_t)t], tau, o);
+            o->has_locus = 1; o->locus[0] = t / pq; o->locus[1] = (t % pq) / d.d3; o->locus[2] = t % d.d3;
+            return;
+          }
+        set_ok(o));
+}
+int abed_ic_verify_k_f32(const float* cv, abed_dims4 d, const float* f, abed_dims4 fd, const double* ic, double tau,
+                         abed_verify_outcome* o) {
+  GUARD(check_dims(d); check_dims(fd);
+        DevBuf<double> l((size_t)d.d1), r((size_t)d.d1);
+        ick_f64_kernel<<<grid_for(d.d1, 32), 32>>>(cv, d, f, fd.d1 * fd.d2 * fd.d3, ic, l.p, r.p); launched("ic_verify_k_f32");
+        std::vector<double> hl((size_t)d.d1), hr((size_t)d.d1);
+        cuda_check(cudaMemcpy(hl.data(), l.p, hl.size() * 8, cudaMemcpyDeviceToHost), "d2h");
+        cuda_check(cudaMemcpy(hr.data(), r.p, hr.size() * 8, cudaMemcpyDeviceToHost), "d2h");
+        for (int64_t k = 0; k < d.d1; ++k)
+          if (!(std::fabs(hl[(size_t)k] - hr[(size_t)k]) <= tau)) {
+            float_verify_host(hl[(size_t)k], hr[(size_t)k], tau, o);
+            o->has_locus = 1; o->locus[0] = k; o->locus[1] = -1; o->locus[2] = -1;
+            return;
+          }
+        set_ok(o));
+}
+
+// --------------------------------------------------------------- faults
+int abed_flip_bit(void* data, int32_t kind, int64_t count, int64_t flat_index, int32_t bit, void* stream) {
+  GUARD(  // faults.hpp:53-62
+      const int64_t es = kind == ABED_I8 ? 1 : kind == ABED_I64 ? 8 : 4;
+      if (flat_index < 0 || flat_index >= count) throw_range("flip_bit: flat index out of bounds");
+      if (bit < 0 || bit >= 8 * es) throw_range("flip_bit: bit position out of range for element kind");
+      flip_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(static_cast<uint8_t*>(data), flat_index * es + bit / 8,
+                                                     (uint8_t)(1u << (bit % 8)));
+      launched("flip_bit"));
+}
+
+}  // extern "C"
