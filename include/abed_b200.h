@@ -263,6 +263,10 @@ int abed_conv_plan_run(abed_conv_plan* plan, const int8_t* packed_input, const a
 /* Reduces the run's per-tile records into reference VerifyOutcomes (device side),
  * asynchronously; outcome_dev points to 3 device abed_verify_outcome {FC, FIC, IC}. */
 int abed_conv_plan_finalize(abed_conv_plan* plan, abed_verify_outcome* outcome_dev, void* stream);
+/* reuse = 1: later runs keep the input checksum / FIC right-hand side computed by
+ * an earlier run instead of recomputing it from the (possibly corrupted) input;
+ * the run is then exactly one kernel launch (fault campaigns, kernel timing). */
+int abed_conv_plan_set_reuse_input_checksum(abed_conv_plan* plan, int32_t reuse);
 /* duplication baseline: mismatch count of the last OUT_I8_COMPARE run (synchronous) */
 int abed_conv_plan_compare_count(abed_conv_plan* plan, int64_t* count);
 

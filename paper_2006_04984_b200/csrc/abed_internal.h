@@ -36,6 +36,9 @@ __global__ void filter_sum_kernel(const int8_t* f, int64_t K, int64_t crs, int32
 __global__ void batch_sum_packed_kernel(const int8_t* act, abed_dev::ActGeom g, int32_t* bsum);
 __global__ void box_sum_dot_kernel(const int32_t* bsum, abed_dev::ActGeom g, const int32_t* fsum,
                                    int32_t* ic_out, unsigned long long* fic_rhs);
+__global__ void fic_weight_kernel(const int32_t* fsum, abed_dev::ActGeom g, int32_t* G);
+__global__ void fic_rhs_kernel(const int8_t* act, abed_dev::ActGeom g, const int32_t* G, int nsplit,
+                               unsigned long long* rhs);
 __global__ void fc_finalize_rec_kernel(const int64_t* rec, int m_tiles, int P, int Q, abed_verify_outcome* out);
 __global__ void fc_finalize_part_kernel(const int64_t* part, abed_dev::ActGeom g, int n_tiles,
                                         unsigned long long* scratch);
@@ -79,6 +82,7 @@ struct abed_conv_plan {
   int32_t* d_fsum = nullptr;    // filter checksum (c,r,s) order, i32
   int32_t* d_ic = nullptr;      // input checksum of the last run (c,r,s)
   int32_t* d_bsum = nullptr;    // batch-sum image [phase][c16*16][Hl*Wl]
+  int32_t* d_ficw = nullptr;    // FIC position weights G [phase][c16][Hl*Wl][16] (offline)
   int64_t* d_fc_rec = nullptr;
   int64_t* d_fc_part = nullptr;
   int64_t* d_fic_part = nullptr;

@@ -123,6 +123,12 @@ abed_conv_plan* plan_create(const abed_layer_shape& shape, const int8_t* filters
     cuda_check(cudaGetLastError(), "pack_filters");
     filter_sum_kernel<<<grid_for(crs), 256>>>(filters, shape.k, crs, pl->d_fsum);
     cuda_check(cudaGetLastError(), "filter_sum");
+    if (checks & ABED_CHECK_FIC) {
+      const int64_t nw = (int64_t)g.n_phase * g.c16 * 16 * g.Hl * g.Wl;
+      cuda_check(cudaMalloc(&pl->d_ficw, nw * 4), "cudaMalloc(ficw)");
+      fic_weight_kernel<<<grid_for(nw), 256>>>(pl->d_fsum, g, pl->d_ficw);
+      cuda_check(cudaGetLastError(), "fic_weight");
+    }
     cuda_check(cudaDeviceSynchronize(), "plan_create sync");
   } catch (...) {
     abed_conv_plan_destroy(pl);
@@ -179,8 +185,15 @@ void plan_run(abed_conv_plan* pl, const int8_t* packed, const abed_epilog_params
     const ActGeom& g = pl->g;
     cuda_check(cudaMemsetAsync(pl->d_acc, 0, 8, st), "memset rhs");
     const int64_t cnt = (int64_t)g.n_phase * g.c16 * g.Hl * g.Wl;
-    batch_sum_packed_kernel<<<grid_for(cnt), 256, 0, st>>>(packed, g, pl->d_bsum);
-    box_sum_dot_kernel<<<g.c, 256, 0, st>>>(pl->d_bsum, g, pl->d_fsum, pl->d_ic, pl->d_acc);
+    if (pl->checks & ABED_CHECK_IC) {
+      // per-tap input checksum needed (IC): batch sum, then window sums + FIC dot
+      batch_sum_packed_kernel<<<grid_for(cnt), 256, 0, st>>>(packed, g, pl->d_bsum);
+      box_sum_dot_kernel<<<g.c, 256, 0, st>>>(pl->d_bsum, g, pl->d_fsum, pl->d_ic, pl->d_acc);
+    } else {
+      // FIC only: one HBM pass, rhs = sum x * G
+      const int nsplit = g.n >= 8 ? 8 : g.n;
+      fic_rhs_kernel<<<grid_for(cnt * nsplit), 256, 0, st>>>(packed, g, pl->d_ficw, nsplit, pl->d_acc);
+    }
     cuda_check(cudaGetLastError(), "input checksum");
   }
   cuda_check(conv_tc_launch(p, num_sms(), st), "conv_i8_tc launch");
@@ -257,7 +270,7 @@ int abed_conv_plan_create(const abed_layer_shape* shape, const int8_t* filters, 
 int abed_conv_plan_destroy(abed_conv_plan* pl) {
   if (!pl) return ABED_OK;
   cudaFree(pl->d_wpk); cudaFree(pl->d_filters); cudaFree(pl->d_fsum); cudaFree(pl->d_ic);
-  cudaFree(pl->d_bsum); cudaFree(pl->d_fc_rec); cudaFree(pl->d_fc_part); cudaFree(pl->d_fic_part);
+  cudaFree(pl->d_bsum); cudaFree(pl->d_ficw); cudaFree(pl->d_fc_rec); cudaFree(pl->d_fc_part); cudaFree(pl->d_fic_part);
   cudaFree(pl->d_acc); cudaFree(pl->d_zero_bias);
   delete pl;
   return ABED_OK;
@@ -289,6 +302,9 @@ int abed_conv_plan_run(abed_conv_plan* pl, const int8_t* packed, const abed_epil
 }
 int abed_conv_plan_finalize(abed_conv_plan* pl, abed_verify_outcome* outcome_dev, void* stream) {
   return guarded([&] { plan_finalize(pl, outcome_dev, (cudaStream_t)stream); });
+}
+int abed_conv_plan_set_reuse_input_checksum(abed_conv_plan* pl, int32_t reuse) {
+  return guarded([&] { pl->reuse_input_checksum = reuse ? 1 : 0; });
 }
 int abed_conv_plan_compare_count(abed_conv_plan* pl, int64_t* count) {
   return guarded([&] {

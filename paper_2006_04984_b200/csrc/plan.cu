@@ -227,6 +227,78 @@ __global__ void box_sum_dot_kernel(const int32_t* __restrict__ bsum, ActGeom g, 
 }
 
 // ---------------------------------------------------------------------------
+// FIC right-hand side in ONE pass over the input (FR option).  fic_dot(fc, ic)
+// = sum_{c,r,s} fsum[c,r,s] * sum_{windows} x = sum_{pixels} x * G, where
+// G[phase][c][i][j] = sum of fsum[c,r,s] over the taps (r,s) of that phase whose
+// window position (i - r/sh, j - s/sw) is a valid output (checksum.hpp:248-285
+// regrouped by input position).  G depends only on the offline filters.
+// ---------------------------------------------------------------------------
+__global__ void fic_weight_kernel(const int32_t* __restrict__ fsum, ActGeom g, int32_t* __restrict__ G) {
+  const int64_t HlWl = (int64_t)g.Hl * g.Wl;
+  const int64_t total = (int64_t)g.n_phase * g.c16 * 16 * HlWl;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t pix = idx % HlWl;
+    const int64_t ce = idx / HlWl;  // phase * c16*16 + channel
+    const int c = (int)(ce % (g.c16 * 16));
+    const int phase = (int)(ce / (g.c16 * 16));
+    const int i = (int)(pix / g.Wl), j = (int)(pix % g.Wl);
+    int32_t acc = 0;
+    if (c < g.c) {
+      for (int r = 0; r < g.r; ++r)
+        for (int s = 0; s < g.s; ++s) {
+          if ((r % g.sh) * g.nph_w + (s % g.sw) != phase) continue;
+          const int p = i - r / g.sh, q = j - s / g.sw;
+          if (p >= 0 && p < g.p && q >= 0 && q < g.q) acc += fsum[((int64_t)c * g.r + r) * g.s + s];
+        }
+    }
+    // layout [phase][c16][HlWl][16]: one 64-byte vector per packed pixel
+    const int grp = c >> 4, e = c & 15;
+    G[(((int64_t)phase * g.c16 + grp) * HlWl + pix) * 16 + e] = acc;
+  }
+}
+
+// rhs += sum over (plane, image block pixel, image) of x . G ; images split in
+// `nsplit` groups so enough loads are in flight to stream HBM.
+__global__ void fic_rhs_kernel(const int8_t* __restrict__ act, ActGeom g, const int32_t* __restrict__ G, int nsplit,
+                               unsigned long long* __restrict__ rhs) {
+  const int64_t HlWl = (int64_t)g.Hl * g.Wl;
+  const int64_t planes = (int64_t)g.n_phase * g.c16;
+  const int64_t total = planes * HlWl * nsplit;
+  long long acc = 0;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t pix = idx % HlWl;
+    const int64_t rest = idx / HlWl;
+    const int split = (int)(rest % nsplit);
+    const int64_t plane = rest / nsplit;
+    const int4* gw = reinterpret_cast<const int4*>(G + (plane * HlWl + pix) * 16);
+    int32_t w[16];
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const int4 t = __ldg(gw + v);
+      w[4 * v] = t.x; w[4 * v + 1] = t.y; w[4 * v + 2] = t.z; w[4 * v + 3] = t.w;
+    }
+    const uint4* src = reinterpret_cast<const uint4*>(act) + plane * g.plane_len + pix;
+    const int n0 = (int)((int64_t)g.n * split / nsplit), n1 = (int)((int64_t)g.n * (split + 1) / nsplit);
+#pragma unroll 4
+    for (int n = n0; n < n1; ++n) {
+      const uint4 x = __ldcs(src + (int64_t)n * HlWl);
+      const uint32_t xw[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+      for (int e = 0; e < 16; ++e) acc += (long long)(int8_t)(xw[e >> 2] >> (8 * (e & 3))) * w[e];
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  __shared__ long long red[32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long t = 0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];
+    atomicAdd(rhs, (unsigned long long)t);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // finalize kernels (single block), write an abed_verify_outcome to device memory
 // ---------------------------------------------------------------------------
 __device__ void write_outcome(abed_verify_outcome* o, int mismatch, int has_locus, int64_t l0, int64_t l1,
