@@ -1,0 +1,12 @@
+// abed/abed.hpp -- umbrella header of the B200 drop-in for the reference's ABED
+// convolution path (reference: proj/include/abed/abed.hpp).  The reference's
+// analytic cost model, ABFT-GEMM baseline and JSON network configs are out of
+// the hot-path scope and not included.
+#pragma once
+
+#include "checksum.hpp"
+#include "convolution.hpp"
+#include "faults.hpp"
+#include "protected_conv.hpp"
+#include "rng.hpp"
+#include "tensor.hpp"
