@@ -171,6 +171,14 @@ class ClockSampler:
         except (OSError, FileNotFoundError):
             self.proc = None
 
+    def keep_busy(self, fn, seconds):
+        import torch
+        t_end = time.time() + seconds
+        while time.time() < t_end:
+            for _ in range(20):
+                fn()
+            torch.cuda.synchronize()
+
     def stop(self):
         if not self.proc:
             return None
@@ -279,7 +287,11 @@ def run_ours(args, world, rank, local):
             dist.barrier()
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
         if sampler:
+            # nvidia-smi needs a few hundred ms for its first sample: keep the same
+            # step running under load until samples flow, time the K steps, then keep
+            # the load on briefly so the samples bracket the timed region
             sampler.start()
+            sampler.keep_busy(lambda: (flush.zero_(), graphs[v].replay()), 1.0)
         cur = torch.cuda.current_stream()
         for i in range(steps):
             flush.zero_()
@@ -289,6 +301,8 @@ def run_ours(args, world, rank, local):
                 dist.all_reduce(counts)
             evs[i][1].record(cur)
         torch.cuda.synchronize()
+        if sampler:
+            sampler.keep_busy(lambda: (flush.zero_(), graphs[v].replay()), 0.4)
         clocks = sampler.stop() if sampler else None
         ms = statistics.mean(a.elapsed_time(b) for a, b in evs)
         if dist:

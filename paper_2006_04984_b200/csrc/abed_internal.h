@@ -75,7 +75,7 @@ void dev_epilog(const int32_t* in, abed_dims4 d, const abed_epilog_params* p, vo
 struct abed_conv_plan {
   abed_layer_shape shape;
   abed_dev::ActGeom g;
-  abed_dev::ConvTcParams base;  // tiling + tap tables; pointers filled per run
+  abed_dev::ConvTcParams base{};  // tiling + tap tables; pointers filled per run
   int checks;
   int8_t* d_wpk = nullptr;      // packed B blocks
   int8_t* d_filters = nullptr;  // KCRS copy (IC verify reads filter storage)

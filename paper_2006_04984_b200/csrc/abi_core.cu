@@ -340,4 +340,11 @@ int abed_conv_i8(const int8_t* input, const int8_t* filters, const abed_layer_sh
   });
 }
 
+// ---------------------------------------------------------------- diagnostics
+// Per-CTA clock timeline of the conv kernel (conv_tc.cuh kTraceSlots int64 per
+// CTA, zeroed by the caller); nullptr switches it off.  Not on any reference path.
+int abed_debug_set_conv_trace(abed_conv_plan* pl, int64_t* trace_dev) {
+  return guarded([&] { pl->base.trace = trace_dev; });
+}
+
 }  // extern "C"

@@ -105,6 +105,14 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  int64_t* const trace = p.trace ? p.trace + static_cast<int64_t>(blockIdx.x) * kTraceSlots : nullptr;
+  const long long t_entry = clock64();
+  if (trace && threadIdx.x == 0) {
+    uint64_t gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    trace[0] = static_cast<int64_t>(gt);
+    trace[1] = t_entry;
+  }
 
   // accumulator stages: columns per stage (multiple of 32), 2 stages when they fit
   const int acc_cols = (p.block_n_tot + 31) & ~31;
@@ -132,6 +140,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (trace && threadIdx.x == 0) trace[2] = clock64() - t_entry;
 
   // number of work units for this CTA
   int n_units;
@@ -146,40 +155,42 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
-    if (lane == 0 && n_units > 0) {
+    // warp-uniform loop; one elected lane issues each copy (ptx.cuh *_w)
+    if (n_units > 0) {
       const uint64_t pol_b = policy_evict_last();
       if (p.b_resident) {
         const int nt = blockIdx.x % p.n_tiles;
         const uint32_t bytes = p.b_stage_bytes * p.k_stages;
-        mbar_arrive_expect_tx(bres, bytes);
+        mbar_arrive_expect_tx_w(bres, bytes);
         const int8_t* src = p.wpk + static_cast<int64_t>(nt) * p.k_stages * p.b_stage_bytes;
         for (uint32_t o = 0; o < bytes; o += 65536u) {
           const uint32_t sz = (bytes - o) < 65536u ? (bytes - o) : 65536u;
-          bulk_g2s_evict_last(sB + o, src + o, sz, bres, pol_b);
+          bulk_g2s_evict_last_w(sB + o, src + o, sz, bres, pol_b);
         }
       }
       int stage = 0;
       uint32_t phase = 0;
       const uint32_t strip_bytes = p.strip_pix * 16u;
       const uint32_t bytes = L.a_stage_bytes + (p.b_resident ? 0u : p.b_stage_bytes);
+      if (trace && lane == 0) trace[8] = clock64() - t_entry;
       for (int u = 0; u < n_units; ++u) {
         int mt, nt;
         decode_tile(p, u, mt, nt);
         const int64_t m0 = static_cast<int64_t>(mt) * kBlockM;
         for (int ks = 0; ks < p.k_stages; ++ks) {
           mbar_wait(&empty[stage], phase ^ 1u);
-          mbar_arrive_expect_tx(&full[stage], bytes);
+          mbar_arrive_expect_tx_w(&full[stage], bytes);
           uint8_t* dstA = sA + stage * L.a_stage_bytes;
           for (int ph = 0; ph < p.n_phase; ++ph) {
             for (int g = 0; g < p.gps; ++g) {
               const int64_t plane = static_cast<int64_t>(ph) * p.c16 + ks * p.gps + g;
               const int8_t* src = p.act + (plane * p.plane_len + m0) * 16;
-              bulk_g2s(dstA + (ph * p.gps + g) * strip_bytes, src, strip_bytes, &full[stage]);
+              bulk_g2s_w(dstA + (ph * p.gps + g) * strip_bytes, src, strip_bytes, &full[stage]);
             }
           }
           if (!p.b_resident) {
             const int8_t* src = p.wpk + (static_cast<int64_t>(nt) * p.k_stages + ks) * p.b_stage_bytes;
-            bulk_g2s_evict_last(sB + stage * p.b_stage_bytes, src, p.b_stage_bytes, &full[stage], pol_b);
+            bulk_g2s_evict_last_w(sB + stage * p.b_stage_bytes, src, p.b_stage_bytes, &full[stage], pol_b);
           }
           if (++stage == p.n_stages) {
             stage = 0;
@@ -187,6 +198,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
           }
         }
       }
+      if (trace && lane == 0) trace[7] = clock64() - t_entry;
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
@@ -219,30 +231,46 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + as * acc_cols;
         for (int ks = 0; ks < p.k_stages; ++ks) {
-          mbar_wait(&full[stage], phase);
+          if (trace) {
+            const long long w0 = clock64();
+            mbar_wait(&full[stage], phase);
+            const long long w1 = clock64();
+            if (lane == 0) {
+              if (u == 0 && ks == 0) trace[3] = w1 - t_entry;
+              trace[9] += w1 - w0;
+            }
+          } else {
+            mbar_wait(&full[stage], phase);
+          }
           tc_fence_after();
-          if (lane == 0) {
-            const uint64_t a0 = make_sdesc(smem_u32(sA + stage * L.a_stage_bytes), strip_bytes, 128u);
-            const uint64_t b0 = make_sdesc(
-                smem_u32(p.b_resident ? sB + ks * p.b_stage_bytes : sB + stage * p.b_stage_bytes), b_lbo, 128u);
-            uint32_t accum = ks > 0 ? 1u : 0u;
-#pragma unroll 3
+          // warp-uniform issue: every lane walks the table, one elected lane issues
+          const uint64_t a0 = make_sdesc(smem_u32(sA + stage * L.a_stage_bytes), strip_bytes, 128u);
+          const uint64_t b0 = make_sdesc(
+              smem_u32(p.b_resident ? sB + ks * p.b_stage_bytes : sB + stage * p.b_stage_bytes), b_lbo, 128u);
+          uint32_t accum = ks > 0 ? 1u : 0u;
+          if (n_rest) {
             for (int i = 0; i < n_mma; ++i) {
               const uint2 o = tab[i];
-              mma_i8(d_tmem, a0 + o.x, b0 + o.y, idesc_main, accum);
-              if (n_rest) mma_i8(d_tmem + 256u, a0 + o.x, b0 + o.y + 256u, idesc_rest, accum);
+              mma_i8_w(d_tmem, a0 + o.x, b0 + o.y, idesc_main, accum);
+              mma_i8_w(d_tmem + 256u, a0 + o.x, b0 + o.y + 256u, idesc_rest, accum);
               accum = 1u;
             }
-            mma_commit(&empty[stage]);
+          } else {
+#pragma unroll 6
+            for (int i = 0; i < n_mma; ++i) {
+              const uint2 o = tab[i];
+              mma_i8_w(d_tmem, a0 + o.x, b0 + o.y, idesc_main, accum);
+              accum = 1u;
+            }
           }
-          __syncwarp();
+          mma_commit_w(&empty[stage]);
           if (++stage == p.n_stages) {
             stage = 0;
             phase ^= 1u;
           }
         }
-        if (lane == 0) mma_commit(&tfull[as]);
-        __syncwarp();
+        mma_commit_w(&tfull[as]);
+        if (trace && lane == 0 && u == n_units - 1) trace[4] = clock64() - t_entry;
         if (++as == n_acc) {
           as = 0;
           aphase ^= 1u;
@@ -289,7 +317,13 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
         nchw_row = static_cast<int64_t>(n_img) * p.K * PQ + static_cast<int64_t>(pp) * p.Q + qq;
       }
 
-      mbar_wait(&tfull[as], aphase);
+      if (trace && warp == 2) {
+        const long long w0 = clock64();
+        mbar_wait(&tfull[as], aphase);
+        if (lane == 0) trace[10] += clock64() - w0;
+      } else {
+        mbar_wait(&tfull[as], aphase);
+      }
       tc_fence_after();
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + as * acc_cols;
 
@@ -486,6 +520,10 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
     }
   }
 
+  if (trace && warp == 2 && lane == 0) {
+    trace[5] = clock64() - t_entry;
+    trace[6] = n_units;
+  }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {

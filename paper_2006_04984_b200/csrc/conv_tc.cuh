@@ -100,6 +100,13 @@ struct ConvTcParams {
   // (n,k,p,q) = fault_key in reference flat order before checks and epilog.
   int64_t fault_key;  // -1 = none
   int fault_bit;
+  // ---- diagnostics: per-CTA clock timeline (kTraceSlots int64 per CTA) or nullptr
+  int64_t* trace;
 };
+// trace slots: 0 globaltimer at entry, 1 clock at entry, 2 setup done, 3 first
+// stage ready (MMA warp), 4 last MMA commit, 5 epilogue done, 6 units, 7 producer
+// done, 8 first copy issued, 9 summed MMA-warp wait cycles on `full`, 10 summed
+// epilogue-warp wait cycles on the accumulator
+constexpr int kTraceSlots = 16;
 
 }  // namespace abed_dev

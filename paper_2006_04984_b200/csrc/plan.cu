@@ -441,18 +441,33 @@ int num_sms() {
 
 static constexpr uint32_t kSmemBudget = abed_dev::kConvDynSmemMax - 256;
 
+// Cycles of one M=128 x K=32 SS-mode kind::i8 MMA with N columns, measured on
+// B200 with warp-uniform issue (tools/mma_microbench2.cu,
+// profiles/mma_microbench2_r01.txt): the tensor floor N/2, or the shared-memory
+// operand read (A 4 KB + B 32*N bytes at 128 B/clk) when N < 128.
+static double mma_cycles(int n) {
+  double c = 0.0;
+  while (n > 0) {
+    const int part = n > 256 ? 256 : n;
+    c += std::max(part / 2.0, (4096.0 + 32.0 * part) / 128.0) + 1.0;
+    n -= part;
+  }
+  return c;
+}
+
 bool choose_tiling(const ActGeom& g, bool fc, int force_block_n, ConvTcParams& p) {
-  // SS-mode tcgen05 cost model (measured, tools/mma_microbench.cu): one
-  // M=128 x K=32 MMA costs max(~133, N/2) cycles (A-operand smem reads), so the
-  // widest N (<= 256 incl. the FC checksum rows) minimises the MMA count.
+  // Pick (block_n, channel groups per stage) minimising the modelled kernel time:
+  // waves of persistent work units x MMAs per unit x cycles per MMA.
   const int ntaps = g.r * g.s;
   const int k_pad = (int)ceil_div(g.k, 16) * 16;
   const int strip = geom_strip_pix(g);
   const int fcrows = fc ? 16 : 0;
+  const int sms = num_sms();
   auto a_stage = [&](int gps) { return (uint32_t)g.n_phase * gps * strip * 16u; };
   int best_tot = -1;
+  double best_cost = 1e300;
   ConvTcParams best{};
-  for (int bn = std::min(k_pad, 256 - fcrows); bn >= 16; bn -= 16) {
+  for (int bn = std::min(k_pad, 256); bn >= 16; bn -= 16) {
     if (force_block_n && bn != force_block_n) continue;
     if (k_pad % bn) continue;
     const int tot = bn + fcrows;
@@ -468,14 +483,26 @@ bool choose_tiling(const ActGeom& g, bool fc, int force_block_n, ConvTcParams& p
       const bool res_ok = stages_res >= 2;
       const bool ring_ok = stages_ring >= 2;
       if (!res_ok && !ring_ok) continue;
-      if (tot <= best_tot) continue;
+      const int n_tiles = k_pad / bn;
+      int64_t waves;
+      if (res_ok) {
+        const int per = std::max(1, std::min(sms / n_tiles, g.m_tiles));
+        waves = ceil_div(g.m_tiles, per);
+      } else {
+        waves = ceil_div((int64_t)g.m_tiles * n_tiles, sms);
+      }
+      const double per_unit = (double)ntaps * (g.c16 / 2) * mma_cycles(tot) + 300.0;
+      double cost = waves * per_unit;
+      if (!res_ok) cost *= 1.02;  // streamed B: extra L2 traffic per unit
+      if (2 * ((tot + 31) & ~31) > 512) cost *= 1.10;  // single TMEM accumulator: no epilogue overlap
+      if (cost >= best_cost * 0.999) continue;
+      best_cost = cost;
       best_tot = tot;
       best = p;
-      best.block_n = bn; best.block_n_tot = tot; best.gps = gps; best.n_tiles = k_pad / bn;
+      best.block_n = bn; best.block_n_tot = tot; best.gps = gps; best.n_tiles = n_tiles;
       best.k_stages = g.c16 / gps; best.b_stage_bytes = bstage;
       best.b_resident = res_ok ? 1 : 0;
       best.n_stages = res_ok ? stages_res : stages_ring;
-      break;  // gps=4 preferred (fewer, larger bulk copies)
     }
   }
   if (best_tot < 0) return false;

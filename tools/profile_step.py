@@ -39,6 +39,10 @@ def main():
         layers.append((name, pl, pl.pack(x), torch.zeros(ls.n * k * (ls.p + 1) * (ls.q + 1) + 65536, dtype=torch.int8,
                                                          device="cuda"), pl.epilog_params(0.05, torch.linspace(-2, 2, k), True)))
     torch.cuda.synchronize()
+    for name, pl, *_ in layers:
+        i = pl.info
+        print(f"{name}: block_n={i.block_n} n_tiles={i.n_tiles} m_tiles={i.m_tiles} gps={i.gps} "
+              f"b_resident={i.b_resident} n_phase={i.n_phase} Hl={i.Hl} Wl={i.Wl} smem={i.smem_bytes}")
     for _ in range(a.reps):
         for name, pl, packed, out, ep in layers:
             pl.run(packed, out, abi.OUT_I8_PACKED, ep=ep)
