@@ -270,8 +270,9 @@ int abed_conv_plan_set_reuse_input_checksum(abed_conv_plan* plan, int32_t reuse)
 /* duplication baseline: mismatch count of the last OUT_I8_COMPARE run (synchronous) */
 int abed_conv_plan_compare_count(abed_conv_plan* plan, int64_t* count);
 /* diagnostics (no reference counterpart): record a per-CTA clock timeline of the
- * conv kernel into trace_dev (16 int64 per CTA, caller-zeroed); NULL disables. */
-int abed_debug_set_conv_trace(abed_conv_plan* plan, int64_t* trace_dev);
+ * conv kernel into trace_dev (16 int64 per CTA, caller-zeroed); NULL disables.
+ * flags bit 0 makes the epilogue skip its work (timing experiments only). */
+int abed_debug_set_conv_trace(abed_conv_plan* plan, int64_t* trace_dev, int32_t flags);
 
 #ifdef __cplusplus
 }

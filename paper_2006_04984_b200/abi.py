@@ -170,7 +170,7 @@ SIGNATURES = {
     "abed_conv_plan_run": (C.c_int, [P, P, C.POINTER(EpilogParams), i32, P, P, i64, i32, P]),
     "abed_conv_plan_finalize": (C.c_int, [P, P, P]),
     "abed_conv_plan_compare_count": (C.c_int, [P, C.POINTER(i64)]),
-    "abed_debug_set_conv_trace": (C.c_int, [P, P]),
+    "abed_debug_set_conv_trace": (C.c_int, [P, P, i32]),
     "abed_conv_plan_set_reuse_input_checksum": (C.c_int, [P, i32]),
 }
 

@@ -37,6 +37,7 @@ __global__ void batch_sum_packed_kernel(const int8_t* act, abed_dev::ActGeom g, 
 __global__ void box_sum_dot_kernel(const int32_t* bsum, abed_dev::ActGeom g, const int32_t* fsum,
                                    int32_t* ic_out, unsigned long long* fic_rhs);
 __global__ void fic_weight_kernel(const int32_t* fsum, abed_dev::ActGeom g, int32_t* G);
+__global__ void fic_weight_digits_kernel(const int32_t* G, int64_t cells, int8_t* G8, int* too_big);
 __global__ void fic_rhs_kernel(const int8_t* act, abed_dev::ActGeom g, const int32_t* G, int nsplit,
                                unsigned long long* rhs);
 __global__ void fc_finalize_rec_kernel(const int64_t* rec, int m_tiles, int P, int Q, abed_verify_outcome* out);
@@ -51,7 +52,10 @@ __global__ void ic_finalize_kernel(const unsigned long long* ksum, const int8_t*
 
 // conv_tc.cu
 uint32_t conv_tc_smem_bytes(const abed_dev::ConvTcParams& p);
-cudaError_t conv_tc_launch(const abed_dev::ConvTcParams& p, int num_sms, cudaStream_t stream);
+int conv_tc_grid(const abed_dev::ConvTcParams& p, int num_sms);
+int mma_pattern_of(const abed_dev::ActGeom& g, int gps);
+// pdl: launch with programmatic stream serialization (griddepcontrol in the kernel)
+cudaError_t conv_tc_launch(const abed_dev::ConvTcParams& p, int num_sms, bool pdl, cudaStream_t stream);
 
 }  // namespace abed_host
 
@@ -83,13 +87,21 @@ struct abed_conv_plan {
   int32_t* d_ic = nullptr;      // input checksum of the last run (c,r,s)
   int32_t* d_bsum = nullptr;    // batch-sum image [phase][c16*16][Hl*Wl]
   int32_t* d_ficw = nullptr;    // FIC position weights G [phase][c16][Hl*Wl][16] (offline)
-  int64_t* d_fc_rec = nullptr;
-  int64_t* d_fc_part = nullptr;
-  int64_t* d_fic_part = nullptr;
+  int8_t* d_ficw8 = nullptr;    // G as 3 balanced base-256 digit planes [phase][c16][Hl*Wl][3][16]
+  int ficw8_ok = 0;             // every |G| < 2^23 (3 digits are exact)
+  int64_t* d_fc_part = nullptr;     // FC row partials per N tile (n_tiles > 1)
+  unsigned int* d_tile_sem = nullptr;  // FC tiles-done counters per M tile
+  int64_t* d_cta_rec = nullptr;     // FC per-CTA records
+  unsigned long long* d_kacc = nullptr;  // kernel accumulators {FIC lhs, FIC rhs, done ticket, -}
+  abed_verify_outcome* d_outcome = nullptr;  // {FC, FIC, IC} verdicts written by the conv kernel
   unsigned long long* d_acc = nullptr;  // [0]=fic rhs, [1]=cmp count, [2..3]=fc scratch, [4..4+K) ic sums
   float* d_zero_bias = nullptr;
   // when set, runs skip the input-checksum kernels and keep d_ic / the FIC
   // right-hand side of an earlier run (fault campaigns: checksums come from
   // the pristine input, faults.hpp:111-115)
   int reuse_input_checksum = 0;
+  // programmatic dependent launch of the conv kernel (its prologue overlaps the
+  // previous kernel); off for fault campaigns, which patch filter storage
+  // right before a run
+  int pdl = 1;
 };

@@ -89,11 +89,14 @@ abed_conv_plan* plan_create(const abed_layer_shape& shape, const int8_t* filters
     p.c16 = g.c16;
     p.strip_pix = geom_strip_pix(g);
     p.ntaps = g.r * g.s;
+    p.R = g.r; p.S = g.s; p.sh = g.sh; p.sw = g.sw; p.nph_w = g.nph_w;
+    p.mma_pattern = mma_pattern_of(g, p.gps);
     for (int r = 0; r < g.r; ++r)
       for (int s = 0; s < g.s; ++s) {
         const int t = r * g.s + s;
         p.tap_phase[t] = (r % g.sh) * g.nph_w + (s % g.sw);
         p.tap_shift[t] = (r / g.sh) * g.Wl + (s / g.sw);
+        p.tap_a16[t] = (uint32_t)(p.tap_phase[t] * p.gps * p.strip_pix + p.tap_shift[t]);
       }
     p.m_total = g.m_total;
     p.m_tiles = g.m_tiles;
@@ -108,10 +111,16 @@ abed_conv_plan* plan_create(const abed_layer_shape& shape, const int8_t* filters
     cuda_check(cudaMalloc(&pl->d_fsum, crs * 4), "cudaMalloc(fsum)");
     cuda_check(cudaMalloc(&pl->d_ic, crs * 4), "cudaMalloc(ic)");
     cuda_check(cudaMalloc(&pl->d_bsum, (size_t)g.n_phase * g.c16 * 16 * g.Hl * g.Wl * 4), "cudaMalloc(bsum)");
-    const int64_t tiles = (int64_t)p.n_tiles * p.m_tiles;
-    cuda_check(cudaMalloc(&pl->d_fc_rec, tiles * 4 * 8), "cudaMalloc(fc_rec)");
-    cuda_check(cudaMalloc(&pl->d_fic_part, tiles * 8), "cudaMalloc(fic_part)");
-    if (p.n_tiles > 1) cuda_check(cudaMalloc(&pl->d_fc_part, (size_t)p.n_tiles * p.m_tiles * 128 * 2 * 8), "cudaMalloc(fc_part)");
+    if (p.n_tiles > 1) {
+      cuda_check(cudaMalloc(&pl->d_fc_part, (size_t)p.n_tiles * p.m_tiles * 128 * 2 * 8), "cudaMalloc(fc_part)");
+      cuda_check(cudaMalloc(&pl->d_tile_sem, (size_t)p.m_tiles * 4), "cudaMalloc(tile_sem)");
+      cuda_check(cudaMemset(pl->d_tile_sem, 0, (size_t)p.m_tiles * 4), "memset tile_sem");
+    }
+    cuda_check(cudaMalloc(&pl->d_cta_rec, (size_t)conv_tc_grid(p, num_sms()) * 4 * 8), "cudaMalloc(cta_rec)");
+    cuda_check(cudaMalloc(&pl->d_kacc, 4 * 8), "cudaMalloc(kacc)");
+    cuda_check(cudaMemset(pl->d_kacc, 0, 4 * 8), "memset kacc");
+    cuda_check(cudaMalloc(&pl->d_outcome, 3 * sizeof(abed_verify_outcome)), "cudaMalloc(outcome)");
+    cuda_check(cudaMemset(pl->d_outcome, 0, 3 * sizeof(abed_verify_outcome)), "memset outcome");
     cuda_check(cudaMalloc(&pl->d_acc, (4 + shape.k) * 8), "cudaMalloc(acc)");
     cuda_check(cudaMemset(pl->d_acc, 0, (4 + shape.k) * 8), "memset acc");
     cuda_check(cudaMalloc(&pl->d_zero_bias, shape.k * 4), "cudaMalloc(bias)");
@@ -127,6 +136,15 @@ abed_conv_plan* plan_create(const abed_layer_shape& shape, const int8_t* filters
       const int64_t nw = (int64_t)g.n_phase * g.c16 * 16 * g.Hl * g.Wl;
       cuda_check(cudaMalloc(&pl->d_ficw, nw * 4), "cudaMalloc(ficw)");
       fic_weight_kernel<<<grid_for(nw), 256>>>(pl->d_fsum, g, pl->d_ficw);
+      cuda_check(cudaMalloc(&pl->d_ficw8, nw * 3), "cudaMalloc(ficw8)");
+      int* d_big = nullptr;
+      cuda_check(cudaMalloc(&d_big, 4), "cudaMalloc(flag)");
+      cuda_check(cudaMemset(d_big, 0, 4), "memset flag");
+      fic_weight_digits_kernel<<<grid_for(nw), 256>>>(pl->d_ficw, nw / 16, pl->d_ficw8, d_big);
+      int big = 0;
+      cuda_check(cudaMemcpy(&big, d_big, 4, cudaMemcpyDeviceToHost), "flag d2h");
+      cudaFree(d_big);
+      pl->ficw8_ok = big ? 0 : 1;
       cuda_check(cudaGetLastError(), "fic_weight");
     }
     cuda_check(cudaDeviceSynchronize(), "plan_create sync");
@@ -171,49 +189,58 @@ void plan_run(abed_conv_plan* pl, const int8_t* packed, const abed_epilog_params
       p.o_sh = 1; p.o_sw = 1; p.o_nph_w = 1; p.o_c16 = o.c16;
     }
   }
-  p.fc_rec = pl->d_fc_rec;
   p.fc_part = pl->d_fc_part;
-  p.fic_part = pl->d_fic_part;
+  p.tile_sem = pl->d_tile_sem;
+  p.cta_rec = pl->d_cta_rec;
+  p.kacc = pl->d_kacc;
+  p.outcome = pl->d_outcome;
+  p.rhs_ext = pl->d_acc;
+  p.ficw8 = pl->d_ficw8;
   p.ic_sum = pl->d_acc + 4;
   p.cmp_count = pl->d_acc + 1;
   p.fault_key = fault_key;
   p.fault_bit = fault_bit;
   if (pl->checks & ABED_CHECK_IC) cuda_check(cudaMemsetAsync(pl->d_acc + 4, 0, pl->shape.k * 8, st), "memset ic");
   if (out_mode == ABED_OUT_I8_COMPARE) cuda_check(cudaMemsetAsync(pl->d_acc + 1, 0, 8, st), "memset cmp");
+  p.rhs_mode = 0;
   if ((pl->checks & (ABED_CHECK_FIC | ABED_CHECK_IC)) && !pl->reuse_input_checksum) {
-    // input checksum of the pristine input, ahead of the convolution (FR option)
+    // input checksum of the pristine input (FR option)
     const ActGeom& g = pl->g;
-    cuda_check(cudaMemsetAsync(pl->d_acc, 0, 8, st), "memset rhs");
-    const int64_t cnt = (int64_t)g.n_phase * g.c16 * g.Hl * g.Wl;
     if (pl->checks & ABED_CHECK_IC) {
-      // per-tap input checksum needed (IC): batch sum, then window sums + FIC dot
+      // per-tap input checksum needed (IC): batch sum, then window sums + FIC dot,
+      // ahead of the convolution
+      cuda_check(cudaMemsetAsync(pl->d_acc, 0, 8, st), "memset rhs");
+      const int64_t cnt = (int64_t)g.n_phase * g.c16 * g.Hl * g.Wl;
       batch_sum_packed_kernel<<<grid_for(cnt), 256, 0, st>>>(packed, g, pl->d_bsum);
       box_sum_dot_kernel<<<g.c, 256, 0, st>>>(pl->d_bsum, g, pl->d_fsum, pl->d_ic, pl->d_acc);
+      cuda_check(cudaGetLastError(), "input checksum");
     } else {
-      // FIC only: one HBM pass, rhs = sum x * G
-      const int nsplit = g.n >= 8 ? 8 : g.n;
-      fic_rhs_kernel<<<grid_for(cnt * nsplit), 256, 0, st>>>(packed, g, pl->d_ficw, nsplit, pl->d_acc);
+      const int64_t cells = (int64_t)g.n_phase * g.c16 * g.Hl * g.Wl;
+      if (pl->ficw8_ok) {
+        // FIC only: rhs = sum x * G computed by the conv kernel's input-checksum
+        // warps from their own read of the stored input
+        p.rhs_mode = 1;
+        const int64_t want = 2LL * conv_tc_grid(p, num_sms()) * 64;
+        p.rhs_nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(g.n, (want + cells - 1) / cells));
+      } else {
+        // |G| too large for the 3-digit map: one separate pass ahead of the conv
+        cuda_check(cudaMemsetAsync(pl->d_acc, 0, 8, st), "memset rhs");
+        const int nsplit = g.n >= 8 ? 8 : g.n;
+        fic_rhs_kernel<<<grid_for(cells * nsplit), 256, 0, st>>>(packed, g, pl->d_ficw, nsplit, pl->d_acc);
+        cuda_check(cudaGetLastError(), "fic_rhs");
+      }
     }
-    cuda_check(cudaGetLastError(), "input checksum");
   }
-  cuda_check(conv_tc_launch(p, num_sms(), st), "conv_i8_tc launch");
+  cuda_check(conv_tc_launch(p, num_sms(), pl->pdl != 0, st), "conv_i8_tc launch");
 }
 
 void plan_finalize(abed_conv_plan* pl, abed_verify_outcome* out_dev, cudaStream_t st) {
-  const ConvTcParams& p = pl->base;
-  const ActGeom& g = pl->g;
-  if (pl->checks & ABED_CHECK_FC) {
-    if (p.n_tiles == 1) {
-      fc_finalize_rec_kernel<<<1, 256, 0, st>>>(pl->d_fc_rec, p.m_tiles, g.p, g.q, out_dev + 0);
-    } else {
-      unsigned long long init[2] = {0ull, ~0ull};
-      cuda_check(cudaMemcpyAsync(pl->d_acc + 2, init, 16, cudaMemcpyHostToDevice, st), "fc scratch");
-      fc_finalize_part_kernel<<<grid_for(g.m_total), 256, 0, st>>>(pl->d_fc_part, g, p.n_tiles, pl->d_acc + 2);
-      fc_finalize_part2_kernel<<<1, 32, 0, st>>>(pl->d_fc_part, g, p.n_tiles, pl->d_acc + 2, out_dev + 0);
-    }
-  }
-  if (pl->checks & ABED_CHECK_FIC)
-    fic_finalize_kernel<<<1, 256, 0, st>>>(pl->d_fic_part, p.n_tiles * p.m_tiles, pl->d_acc, out_dev + 1);
+  // FC and FIC verdicts were written by the conv kernel's last CTA
+  const int lo = (pl->checks & ABED_CHECK_FC) ? 0 : 1, hi = (pl->checks & ABED_CHECK_FIC) ? 2 : 1;
+  if (hi > lo)
+    cuda_check(cudaMemcpyAsync(out_dev + lo, pl->d_outcome + lo, (hi - lo) * sizeof(abed_verify_outcome),
+                               cudaMemcpyDeviceToDevice, st),
+               "outcome copy");
   if (pl->checks & ABED_CHECK_IC)
     ic_finalize_kernel<<<1, 256, 0, st>>>(pl->d_acc + 4, pl->d_filters, pl->d_ic, pl->shape.k,
                                           pl->shape.c * pl->shape.r * pl->shape.s, out_dev + 2);
@@ -270,7 +297,8 @@ int abed_conv_plan_create(const abed_layer_shape* shape, const int8_t* filters, 
 int abed_conv_plan_destroy(abed_conv_plan* pl) {
   if (!pl) return ABED_OK;
   cudaFree(pl->d_wpk); cudaFree(pl->d_filters); cudaFree(pl->d_fsum); cudaFree(pl->d_ic);
-  cudaFree(pl->d_bsum); cudaFree(pl->d_ficw); cudaFree(pl->d_fc_rec); cudaFree(pl->d_fc_part); cudaFree(pl->d_fic_part);
+  cudaFree(pl->d_bsum); cudaFree(pl->d_ficw); cudaFree(pl->d_ficw8); cudaFree(pl->d_fc_part); cudaFree(pl->d_tile_sem);
+  cudaFree(pl->d_cta_rec); cudaFree(pl->d_kacc); cudaFree(pl->d_outcome);
   cudaFree(pl->d_acc); cudaFree(pl->d_zero_bias);
   delete pl;
   return ABED_OK;
@@ -343,8 +371,11 @@ int abed_conv_i8(const int8_t* input, const int8_t* filters, const abed_layer_sh
 // ---------------------------------------------------------------- diagnostics
 // Per-CTA clock timeline of the conv kernel (conv_tc.cuh kTraceSlots int64 per
 // CTA, zeroed by the caller); nullptr switches it off.  Not on any reference path.
-int abed_debug_set_conv_trace(abed_conv_plan* pl, int64_t* trace_dev) {
-  return guarded([&] { pl->base.trace = trace_dev; });
+int abed_debug_set_conv_trace(abed_conv_plan* pl, int64_t* trace_dev, int32_t flags) {
+  return guarded([&] {
+    pl->base.trace = trace_dev;
+    pl->base.dbg = flags;
+  });
 }
 
 }  // extern "C"

@@ -154,6 +154,7 @@ void ctx_make(GpuTrialCtx& c, const abed_layer_shape& s, const int8_t* x, const 
   cuda_check(cudaMemsetAsync(c.trial_out, 0, (size_t)c.out_bytes, st), "memset");
   // golden run: checksums from the pristine input, golden output
   c.plan->reuse_input_checksum = 0;
+  c.plan->pdl = 0;  // trials patch filter storage right before each run
   plan_run(c.plan, c.packed, &c.ep, kind == ABED_F32 ? ABED_OUT_F32_NCHW : ABED_OUT_I8_NCHW, c.golden, nullptr, -1, 0, st);
   c.plan->reuse_input_checksum = 1;
   cuda_check(cudaStreamSynchronize(st), "golden run");

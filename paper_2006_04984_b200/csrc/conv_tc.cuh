@@ -67,9 +67,15 @@ struct ConvTcParams {
   const int8_t* act;
   int64_t plane_len;
   int n_phase, c16, gps, k_stages, strip_pix, ntaps;
+  int R, S, sh, sw, nph_w;  // filter taps, strides, stride phases per row
+  int mma_pattern;          // compile-time unrolled MMA issue routine (conv_tc.cu), 0 = generic
   int n_stages;  // depth of the smem stage ring actually used (<= kStages)
   int tap_phase[kMaxTaps];
   int tap_shift[kMaxTaps];
+  // A-operand start offset of each tap inside a stage, in 16-byte units:
+  // (tap_phase * gps * strip_pix + tap_shift) -- read with a uniform index by
+  // the MMA issuer, so descriptors stay in uniform registers
+  uint32_t tap_a16[kMaxTaps];
   // ---- B operand (packed filters, see pack_filters in conv_tc.cu)
   const int8_t* wpk;
   int block_n;       // output channels per N tile
@@ -89,11 +95,19 @@ struct ConvTcParams {
   // next-layer packed output geometry (OUT_I8_PACKED)
   int64_t o_plane_len;
   int o_Hl, o_Wl, o_ph, o_pw, o_sh, o_sw, o_nph_w, o_c16;
-  // ---- checks
+  // ---- checks (all verdicts are produced inside the kernel: the last CTA to
+  // finish reduces the per-CTA records and writes the reference VerifyOutcomes)
   int check;
-  int64_t* fc_rec;    // [n_tiles*m_tiles][4] {count, first key, lhs, rhs}   (n_tiles == 1)
-  int64_t* fc_part;   // [n_tiles][m_tiles*128][2] {sum_k, extra}            (n_tiles  > 1)
-  int64_t* fic_part;  // [n_tiles*m_tiles] per-tile output sums
+  int64_t* fc_part;            // [n_tiles][m_tiles*128][2] {sum_k, extra} row partials (n_tiles > 1)
+  unsigned int* tile_sem;      // [m_tiles] tiles-done counters for the cross-N-tile FC check
+  int64_t* cta_rec;            // [gridDim][4] FC per-CTA {count, first key, lhs, rhs}
+  unsigned long long* kacc;    // [0] FIC lhs, [1] FIC rhs (in-kernel), [2] CTA done ticket
+  unsigned long long* rhs_ext;  // FIC rhs of the pristine input: read (rhs_mode 0) or stored (rhs_mode 1)
+  int rhs_mode;                // 1: input-checksum warps compute the FIC rhs in this kernel
+  int rhs_nsplit;              // image split of the rhs work items
+  const int8_t* ficw8;         // FIC weight map G as balanced base-256 digits
+                               // [phase][c16][Hl*Wl][3 digits][16 channels] (|G| < 2^23)
+  void* outcome;               // abed_verify_outcome[3] {FC, FIC, IC}: FC and FIC written here
   unsigned long long* ic_sum;  // [K] per-channel output sums (atomic, integer => deterministic)
   unsigned long long* cmp_count;  // OUT_I8_COMPARE mismatch count
   // ---- fault hook (ConvOut target): flip `fault_bit` of output element
@@ -102,6 +116,7 @@ struct ConvTcParams {
   int fault_bit;
   // ---- diagnostics: per-CTA clock timeline (kTraceSlots int64 per CTA) or nullptr
   int64_t* trace;
+  int dbg;  // diagnostics: bit 0 = epilogue skips TMEM reads and processing
 };
 // trace slots: 0 globaltimer at entry, 1 clock at entry, 2 setup done, 3 first
 // stage ready (MMA warp), 4 last MMA commit, 5 epilogue done, 6 units, 7 producer

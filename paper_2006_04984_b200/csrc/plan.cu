@@ -257,6 +257,25 @@ __global__ void fic_weight_kernel(const int32_t* __restrict__ fsum, ActGeom g, i
   }
 }
 
+// G -> 3 balanced base-256 digits (G = d0 + 256 d1 + 65536 d2, d in [-128, 127]),
+// for the conv kernel's dp4a input-checksum warps; flags |G| >= 2^23 (not exact)
+__global__ void fic_weight_digits_kernel(const int32_t* __restrict__ G, int64_t cells, int8_t* __restrict__ G8,
+                                         int* __restrict__ too_big) {
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < cells * 16; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t cell = idx >> 4;
+    const int e = (int)(idx & 15);
+    int32_t v = G[idx];
+    if (v >= (1 << 23) - 128 || v <= -(1 << 23) + 128) atomicOr(too_big, 1);
+    const int32_t d0 = ((v + 128) & 255) - 128;
+    v = (v - d0) >> 8;
+    const int32_t d1 = ((v + 128) & 255) - 128;
+    v = (v - d1) >> 8;
+    G8[(cell * 3 + 0) * 16 + e] = (int8_t)d0;
+    G8[(cell * 3 + 1) * 16 + e] = (int8_t)d1;
+    G8[(cell * 3 + 2) * 16 + e] = (int8_t)v;
+  }
+}
+
 // rhs += sum over (plane, image block pixel, image) of x . G ; images split in
 // `nsplit` groups so enough loads are in flight to stream HBM.
 __global__ void fic_rhs_kernel(const int8_t* __restrict__ act, ActGeom g, const int32_t* __restrict__ G, int nsplit,
@@ -439,6 +458,16 @@ int num_sms() {
   return g_num_sms;
 }
 
+// compile-time unrolled MMA issue routine for this geometry (conv_tc.cu MmaPattern)
+int mma_pattern_of(const ActGeom& g, int gps) {
+  if (g.sh != g.sw || (g.sh != 1 && g.sh != 2) || (gps != 2 && gps != 4)) return 0;
+  const int gi = gps == 4 ? 0 : 1;
+  const int si = g.sh == 1 ? 0 : 2;
+  if (g.r == 3 && g.s == 3) return 1 + si + gi;
+  if (g.r == 1 && g.s == 1) return 5 + si + gi;
+  return 0;
+}
+
 static constexpr uint32_t kSmemBudget = abed_dev::kConvDynSmemMax - 256;
 
 // Cycles of one M=128 x K=32 SS-mode kind::i8 MMA with N columns, measured on
@@ -467,7 +496,8 @@ bool choose_tiling(const ActGeom& g, bool fc, int force_block_n, ConvTcParams& p
   int best_tot = -1;
   double best_cost = 1e300;
   ConvTcParams best{};
-  for (int bn = std::min(k_pad, 256); bn >= 16; bn -= 16) {
+  // one MMA covers the whole N tile (block_n + FC rows <= 256)
+  for (int bn = std::min(k_pad, 256 - fcrows); bn >= 16; bn -= 16) {
     if (force_block_n && bn != force_block_n) continue;
     if (k_pad % bn) continue;
     const int tot = bn + fcrows;

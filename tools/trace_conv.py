@@ -26,6 +26,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--variant", default="unprotected")
     ap.add_argument("--only", default="")
+    ap.add_argument("--dbg", type=int, default=0, help="debug flags (bit 0: epilogue skips its work)")
+    ap.add_argument("--fresh-rhs", action="store_true", help="FIC: recompute the input checksum every run")
     a = ap.parse_args()
     checks = {"unprotected": 0, "fc": abi.CHECK_FC, "fic": abi.CHECK_FIC}[a.variant]
     only = set(a.only.split(",")) if a.only else None
@@ -40,7 +42,7 @@ def main():
         packed = pl.pack(x)
         out = torch.zeros(ls.n * k * (ls.p + 1) * (ls.q + 1) + 65536, dtype=torch.int8, device="cuda")
         ep = pl.epilog_params(0.05, torch.linspace(-2, 2, k), True)
-        abi.call("abed_conv_plan_set_reuse_input_checksum", pl.handle, 1)
+        abi.call("abed_conv_plan_set_reuse_input_checksum", pl.handle, 0 if a.fresh_rhs else 1)
         for _ in range(3):
             pl.run(packed, out, abi.OUT_I8_PACKED, ep=ep)
         torch.cuda.synchronize()
@@ -54,10 +56,10 @@ def main():
             torch.cuda.synchronize()
             ts.append(e0.elapsed_time(e1) * 1e3)
         trace.zero_()
-        abi.call("abed_debug_set_conv_trace", pl.handle, C.c_void_p(trace.data_ptr()))
+        abi.call("abed_debug_set_conv_trace", pl.handle, C.c_void_p(trace.data_ptr()), a.dbg)
         pl.run(packed, out, abi.OUT_I8_PACKED, ep=ep)
         torch.cuda.synchronize()
-        abi.call("abed_debug_set_conv_trace", pl.handle, None)
+        abi.call("abed_debug_set_conv_trace", pl.handle, None, 0)
         t = trace.view(-1, 16).cpu()
         rows = [r for r in t.tolist() if r[1] != 0]
         i = pl.info
@@ -71,7 +73,8 @@ def main():
         print(f"{name:15s} bn={i.block_n:3d} nt={i.n_tiles} mt={i.m_tiles:3d} gps={i.gps} res={i.b_resident} "
               f"ctas={len(rows)} units(max)={max(r[6] for r in rows)} event_us={min(ts):6.2f} | "
               f"setup {med(2)} 1st-copy {med(8)} 1st-ready {med(3)} last-mma {med(4)} prod-done {med(7)} "
-              f"epi-done {med(5)} | mma-wait {med(9)} epi-wait {med(10)} | start spread {max(starts):.2f}us")
+              f"epi-done {med(5)} | mma-wait {med(9)} epi-wait {med(10)} last-acc {med(11)} epi-proc {med(12)} mma-tempty-wait {med(13)} rhs-done {med(15)} | "
+              f"start spread {max(starts):.2f}us")
 
 
 if __name__ == "__main__":
