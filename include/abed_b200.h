@@ -40,6 +40,8 @@ enum {
 
 /* element kinds, tensor.hpp:20 (ElemKind : uint8_t {I8, I32, I64, F32}) */
 enum { ABED_I8 = 0, ABED_I32 = 1, ABED_I64 = 2, ABED_F32 = 3 };
+/* float mode on tensor cores (extension): 16-bit operand storage kinds */
+enum { ABED_F16 = 4, ABED_BF16 = 5 };
 /* convolution.hpp:342 Activation */
 enum { ABED_RELU = 0, ABED_IDENTITY = 1 };
 /* checksum.hpp:15 Scheme */
@@ -240,7 +242,10 @@ int abed_run_campaign(const abed_campaign_config* config, int64_t trial_begin, i
 enum { ABED_CHECK_FC = 1, ABED_CHECK_FIC = 2, ABED_CHECK_IC = 4 };
 enum {
   ABED_OUT_NONE = 0, ABED_OUT_I32_NCHW = 1, ABED_OUT_I8_NCHW = 2, ABED_OUT_F32_NCHW = 3,
-  ABED_OUT_I8_PACKED = 4, ABED_OUT_I8_COMPARE = 5
+  ABED_OUT_I8_PACKED = 4, ABED_OUT_I8_COMPARE = 5,
+  /* float mode (fp16 / bf16 plans): 16-bit output into the next layer's packed
+   * planes, or compared against them (duplication baseline) */
+  ABED_OUT_H_PACKED = 6, ABED_OUT_H_COMPARE = 7
 };
 typedef struct abed_conv_plan abed_conv_plan;
 typedef struct abed_plan_info {
@@ -269,6 +274,18 @@ int abed_conv_plan_finalize(abed_conv_plan* plan, abed_verify_outcome* outcome_d
 int abed_conv_plan_set_reuse_input_checksum(abed_conv_plan* plan, int32_t reuse);
 /* duplication baseline: mismatch count of the last OUT_I8_COMPARE run (synchronous) */
 int abed_conv_plan_compare_count(abed_conv_plan* plan, int64_t* count);
+/* ---- float mode on tensor cores (fp16 / bf16 operands, f32 accumulation).
+ * The reference's float mode (checksum.hpp:471-595: f32 operands, f64 checksum
+ * reductions, Pass iff |lhs - rhs| <= tau) on tcgen05 kind::f16: filters (device
+ * f32 KCRS) and inputs (device f32 NCHW, via abed_pack_input_h) are rounded to
+ * elem_kind (ABED_F16 / ABED_BF16, round to nearest even).  checks: ABED_CHECK_FC
+ * and/or ABED_CHECK_FIC with absolute thresholds tau_fc / tau_fic (float_verify;
+ * tau < 0 is invalid_argument).  Run with abed_conv_plan_run (ABED_OUT_F32_NCHW,
+ * ABED_OUT_H_PACKED, ABED_OUT_H_COMPARE, ABED_OUT_NONE); verdicts carry lhs_f/rhs_f. */
+int abed_conv_plan_create_h(const abed_layer_shape* shape, const float* filters, int32_t elem_kind, int32_t checks,
+                            double tau_fc, double tau_fic, int32_t force_block_n, abed_conv_plan** plan);
+int abed_pack_input_h(const abed_conv_plan* plan, const float* input, void* packed, void* stream);
+int abed_conv_plan_set_tau(abed_conv_plan* plan, double tau_fc, double tau_fic);
 /* diagnostics (no reference counterpart): record a per-CTA clock timeline of the
  * conv kernel into trace_dev (16 int64 per CTA, caller-zeroed); NULL disables.
  * flags bit 0 makes the epilogue skip its work (timing experiments only). */

@@ -118,6 +118,14 @@ int ora_conv_f32(const float* x, const float* f, const abed_layer_shape* ls, flo
   ORA_CONV_BODY(float, XIDX, FIDX, o[p * Q + q] = fmaf(xv, fv, o[p * Q + q]))
   return ORA_OK;
 }
+/* Float mode on tensor cores (no reference counterpart -- parity unpinned, see
+ * DESIGN.md): conv_reference (convolution.hpp:78-111) with f64 accumulation, the
+ * exact-as-possible value the fp16/bf16 tensor-core conv approximates (x, f are
+ * f32 arrays already rounded to the 16-bit storage type). */
+int ora_conv_f64(const float* x, const float* f, const abed_layer_shape* ls, double* out) {
+  ORA_CONV_BODY(double, XIDX, FIDX, o[p * Q + q] += xv * fv)
+  return ORA_OK;
+}
 
 int ora_epilog(const int32_t* in, abed_dims4 d, float scale, const float* bias, int64_t bias_len,
                int activation, int output_kind, void* out) {

@@ -58,6 +58,18 @@ def ref_kind() -> str:
     return "native-vnni" if p and p.endswith("libabed_ref.so") else "x86-64-v3"
 
 
+def round_f16(a: np.ndarray) -> np.ndarray:
+    """f32 -> IEEE binary16 (round to nearest even) -> f32."""
+    return np.asarray(a, np.float32).astype(np.float16).astype(np.float32)
+
+
+def round_bf16(a: np.ndarray) -> np.ndarray:
+    """f32 -> bfloat16 (round to nearest even, finite inputs) -> f32."""
+    u = np.ascontiguousarray(a, np.float32).view(np.uint32).astype(np.uint64)
+    u = (u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000
+    return u.astype(np.uint32).view(np.float32)
+
+
 def ptr(a: np.ndarray):
     return a.ctypes.data_as(P)
 
@@ -151,6 +163,15 @@ class Oracle:
     def conv_f32(self, x, f, ls):
         out = np.empty(ls.output_dims(), np.float32)
         fn = self._f("conv_f32" if self.which == "ora" else "conv_direct_f32")
+        fn.argtypes = [P, P, C.POINTER(LayerShape), P]
+        self._chk(fn(ptr(np.ascontiguousarray(x, np.float32)), ptr(np.ascontiguousarray(f, np.float32)), C.byref(ls), ptr(out)))
+        return out
+
+    def conv_f64(self, x, f, ls):
+        """conv_reference with f64 accumulation (float mode on tensor cores: the
+        value an fp16/bf16 x f32-accumulate conv approximates)."""
+        out = np.empty(ls.output_dims(), np.float64)
+        fn = self._f("conv_f64")
         fn.argtypes = [P, P, C.POINTER(LayerShape), P]
         self._chk(fn(ptr(np.ascontiguousarray(x, np.float32)), ptr(np.ascontiguousarray(f, np.float32)), C.byref(ls), ptr(out)))
         return out

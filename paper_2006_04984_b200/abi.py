@@ -21,7 +21,8 @@ TARGET_INPUT, TARGET_FILTER, TARGET_CONVOUT = 0, 1, 2
 DETECTED, SDC, MASKED, DETECTED_BENIGN = 0, 1, 2, 3
 DATA_ONES, DATA_RANDOM_I8 = 0, 1
 CHECK_FC, CHECK_FIC, CHECK_IC = 1, 2, 4
-OUT_NONE, OUT_I32_NCHW, OUT_I8_NCHW, OUT_F32_NCHW, OUT_I8_PACKED, OUT_I8_COMPARE = range(6)
+OUT_NONE, OUT_I32_NCHW, OUT_I8_NCHW, OUT_F32_NCHW, OUT_I8_PACKED, OUT_I8_COMPARE, OUT_H_PACKED, OUT_H_COMPARE = range(8)
+F16, BF16 = 4, 5  # float mode on tensor cores: 16-bit operand storage kinds
 
 
 class Dims4(C.Structure):
@@ -171,6 +172,9 @@ SIGNATURES = {
     "abed_conv_plan_finalize": (C.c_int, [P, P, P]),
     "abed_conv_plan_compare_count": (C.c_int, [P, C.POINTER(i64)]),
     "abed_debug_set_conv_trace": (C.c_int, [P, P, i32]),
+    "abed_conv_plan_create_h": (C.c_int, [SHP, P, i32, i32, C.c_double, C.c_double, i32, C.POINTER(P)]),
+    "abed_pack_input_h": (C.c_int, [P, P, P, P]),
+    "abed_conv_plan_set_tau": (C.c_int, [P, C.c_double, C.c_double]),
     "abed_conv_plan_set_reuse_input_checksum": (C.c_int, [P, i32]),
 }
 

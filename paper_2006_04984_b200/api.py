@@ -355,3 +355,36 @@ class ConvPlan:
         res = (VerifyOutcome * 3)()
         C.memmove(res, host.ctypes.data, C.sizeof(res))
         return tuple(res)
+
+
+# ------------------------------------------------------------------ float mode on tensor cores
+class ConvPlanH(ConvPlan):
+    """Float-mode protected layer (checksum.hpp:471-595 semantics on tcgen05
+    kind::f16): f32 filters rounded to fp16 / bf16 (elem_kind abi.F16 / abi.BF16),
+    f32 accumulation, FC / FIC with absolute thresholds tau_fc / tau_fic."""
+
+    def __init__(self, ls: LayerShape, filters_f32: torch.Tensor, elem_kind: int = abi.F16, checks: int = 0,
+                 tau_fc: float = 0.0, tau_fic: float = 0.0, block_n: int = 0):
+        self.ls = ls
+        self.checks = checks
+        self.elem_kind = elem_kind
+        self.handle = C.c_void_p()
+        f = filters_f32.contiguous().to(torch.float32)
+        call("abed_conv_plan_create_h", C.byref(ls), _p(f), elem_kind, checks, float(tau_fc), float(tau_fic), block_n,
+             C.byref(self.handle))
+        self.info = abi.PlanInfo()
+        call("abed_conv_plan_info", self.handle, C.byref(self.info))
+        self._outcomes = torch.zeros(3 * C.sizeof(VerifyOutcome), dtype=torch.uint8, device="cuda")
+
+    def set_tau(self, tau_fc: float, tau_fic: float):
+        call("abed_conv_plan_set_tau", self.handle, float(tau_fc), float(tau_fic))
+
+    def pack(self, x_nchw_f32: torch.Tensor, packed: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        packed = self.packed_buffer() if packed is None else packed
+        call("abed_pack_input_h", self.handle, _p(x_nchw_f32.contiguous().to(torch.float32)), _p(packed),
+             stream or _stream())
+        return packed
+
+    def run(self, packed, out=None, out_mode=abi.OUT_F32_NCHW, scale=1.0, bias=None, relu=False, next_plan=None,
+            fault_key=-1, fault_bit=0, stream=None, ep=None):
+        return super().run(packed, out, out_mode, scale, bias, relu, next_plan, fault_key, fault_bit, stream, ep)

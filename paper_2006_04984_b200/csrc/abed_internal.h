@@ -22,8 +22,23 @@ inline void cuda_check(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw AbedError(ABED_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+int set_error(int code, const std::string& msg);
+// runs fn, mapping exceptions to the C-ABI status codes (+ abed_last_error)
+template <typename Fn>
+int guarded(Fn&& fn) {
+  try {
+    fn();
+    return ABED_OK;
+  } catch (const AbedError& e) {
+    return set_error(e.code, e.what());
+  } catch (const std::exception& e) {
+    return set_error(ABED_ERR_RUNTIME, e.what());
+  }
+}
+
 // plan.cu
-abed_dev::ActGeom make_geom(const abed_layer_shape& s);
+// cpg: channels per 16-byte pixel group (16 for int8, 8 for fp16/bf16)
+abed_dev::ActGeom make_geom(const abed_layer_shape& s, int cpg = 16);
 int geom_strip_pix(const abed_dev::ActGeom& g);
 int64_t geom_packed_bytes(const abed_dev::ActGeom& g);
 bool choose_tiling(const abed_dev::ActGeom& g, bool fc, int force_block_n, abed_dev::ConvTcParams& p);
@@ -67,6 +82,11 @@ void require_device();
 int grid_for(int64_t n, int threads);
 void validate_shape(const abed_layer_shape& s);
 abed_conv_plan* plan_create(const abed_layer_shape& shape, const int8_t* filters, int checks, int force_bn);
+// abi_f16.cu: float-mode plan (fp16 / bf16 operands from f32 filters)
+abed_conv_plan* plan_create_h(const abed_layer_shape& shape, const float* filters, int elem_kind, int checks,
+                              double tau_fc, double tau_fic, int force_bn);
+// geometry, tiling and the verdict buffers shared by the int8 and float-mode plans
+void plan_init_common(abed_conv_plan* pl, const abed_layer_shape& shape, int checks, int force_bn, int cpg);
 void plan_run(abed_conv_plan* pl, const int8_t* packed, const abed_epilog_params* ep, int out_mode, void* out,
               const abed_conv_plan* next, int64_t fault_key, int fault_bit, cudaStream_t st);
 void plan_finalize(abed_conv_plan* pl, abed_verify_outcome* out_dev, cudaStream_t st);
@@ -100,6 +120,13 @@ struct abed_conv_plan {
   // right-hand side of an earlier run (fault campaigns: checksums come from
   // the pristine input, faults.hpp:111-115)
   int reuse_input_checksum = 0;
+  // float mode (fp16 / bf16 operands, f32 accumulators; abi_f16.cu)
+  int dtype = 0;                 // abed_dev::DT_I8 / DT_F16 / DT_BF16
+  double tau_fc = 0.0, tau_fic = 0.0;
+  double* d_facc = nullptr;      // {FIC lhs, FIC rhs} f64 kernel accumulators
+  double* d_rhs_f = nullptr;     // FIC rhs of the pristine input (f64)
+  float* d_ficwf = nullptr;      // G as f32 [phase][c16][Hl*Wl][8]
+  double* d_fsum_f = nullptr;    // filter checksum (c,r,s) of the rounded filters, f64
   // programmatic dependent launch of the conv kernel (its prologue overlaps the
   // previous kernel); off for fault campaigns, which patch filter storage
   // right before a run

@@ -21,17 +21,6 @@ int set_error(int code, const std::string& msg) {
   return code;
 }
 
-template <typename Fn>
-int guarded(Fn&& fn) {
-  try {
-    fn();
-    return ABED_OK;
-  } catch (const AbedError& e) {
-    return set_error(e.code, e.what());
-  } catch (const std::exception& e) {
-    return set_error(ABED_ERR_RUNTIME, e.what());
-  }
-}
 
 void require_device() {
   static int ok = -1;
@@ -67,6 +56,49 @@ void validate_shape(const abed_layer_shape& s) {
 }
 
 // ---------------------------------------------------------------- plan
+void plan_init_common(abed_conv_plan* pl, const abed_layer_shape& shape, int checks, int force_bn, int cpg) {
+  pl->shape = shape;
+  pl->checks = checks;
+  pl->g = make_geom(shape, cpg);
+  const ActGeom& g = pl->g;
+  ConvTcParams& p = pl->base;
+  std::memset(&p, 0, sizeof(p));
+  if (!choose_tiling(g, (checks & ABED_CHECK_FC) != 0, force_bn, p))
+    throw_invalid("conv: no tiling fits shared memory for this layer");
+  p.plane_len = g.plane_len;
+  p.n_phase = g.n_phase;
+  p.c16 = g.c16;
+  p.strip_pix = geom_strip_pix(g);
+  p.ntaps = g.r * g.s;
+  p.R = g.r; p.S = g.s; p.sh = g.sh; p.sw = g.sw; p.nph_w = g.nph_w;
+  p.mma_pattern = mma_pattern_of(g, p.gps);
+  for (int r = 0; r < g.r; ++r)
+    for (int s = 0; s < g.s; ++s) {
+      const int t = r * g.s + s;
+      p.tap_phase[t] = (r % g.sh) * g.nph_w + (s % g.sw);
+      p.tap_shift[t] = (r / g.sh) * g.Wl + (s / g.sw);
+      p.tap_a16[t] = (uint32_t)(p.tap_phase[t] * p.gps * p.strip_pix + p.tap_shift[t]);
+    }
+  p.m_total = g.m_total;
+  p.m_tiles = g.m_tiles;
+  p.Hl = g.Hl; p.Wl = g.Wl; p.P = g.p; p.Q = g.q; p.N = g.n; p.K = g.k;
+  p.fault_key = -1;
+  if (p.n_tiles > 1) {
+    cuda_check(cudaMalloc(&pl->d_fc_part, (size_t)p.n_tiles * p.m_tiles * 128 * 2 * 8), "cudaMalloc(fc_part)");
+    cuda_check(cudaMalloc(&pl->d_tile_sem, (size_t)p.m_tiles * 4), "cudaMalloc(tile_sem)");
+    cuda_check(cudaMemset(pl->d_tile_sem, 0, (size_t)p.m_tiles * 4), "memset tile_sem");
+  }
+  cuda_check(cudaMalloc(&pl->d_cta_rec, (size_t)conv_tc_grid(p, num_sms()) * 4 * 8), "cudaMalloc(cta_rec)");
+  cuda_check(cudaMalloc(&pl->d_kacc, 4 * 8), "cudaMalloc(kacc)");
+  cuda_check(cudaMemset(pl->d_kacc, 0, 4 * 8), "memset kacc");
+  cuda_check(cudaMalloc(&pl->d_outcome, 3 * sizeof(abed_verify_outcome)), "cudaMalloc(outcome)");
+  cuda_check(cudaMemset(pl->d_outcome, 0, 3 * sizeof(abed_verify_outcome)), "memset outcome");
+  cuda_check(cudaMalloc(&pl->d_acc, (4 + shape.k) * 8), "cudaMalloc(acc)");
+  cuda_check(cudaMemset(pl->d_acc, 0, (4 + shape.k) * 8), "memset acc");
+  cuda_check(cudaMalloc(&pl->d_zero_bias, shape.k * 4), "cudaMalloc(bias)");
+  cuda_check(cudaMemset(pl->d_zero_bias, 0, shape.k * 4), "memset bias");
+}
+
 abed_conv_plan* plan_create(const abed_layer_shape& shape, const int8_t* filters, int checks, int force_bn) {
   require_device();
   validate_shape(shape);
@@ -76,33 +108,9 @@ abed_conv_plan* plan_create(const abed_layer_shape& shape, const int8_t* filters
   if (shape.k > (int64_t(1) << 24)) throw_invalid("gen_filter_checksum: K too large for i32 checksums");
   auto* pl = new abed_conv_plan();
   try {
-    pl->shape = shape;
-    pl->checks = checks;
-    pl->g = make_geom(shape);
+    plan_init_common(pl, shape, checks, force_bn, 16);
     const ActGeom& g = pl->g;
     ConvTcParams& p = pl->base;
-    std::memset(&p, 0, sizeof(p));
-    if (!choose_tiling(g, (checks & ABED_CHECK_FC) != 0, force_bn, p))
-      throw_invalid("conv: no tiling fits shared memory for this layer");
-    p.plane_len = g.plane_len;
-    p.n_phase = g.n_phase;
-    p.c16 = g.c16;
-    p.strip_pix = geom_strip_pix(g);
-    p.ntaps = g.r * g.s;
-    p.R = g.r; p.S = g.s; p.sh = g.sh; p.sw = g.sw; p.nph_w = g.nph_w;
-    p.mma_pattern = mma_pattern_of(g, p.gps);
-    for (int r = 0; r < g.r; ++r)
-      for (int s = 0; s < g.s; ++s) {
-        const int t = r * g.s + s;
-        p.tap_phase[t] = (r % g.sh) * g.nph_w + (s % g.sw);
-        p.tap_shift[t] = (r / g.sh) * g.Wl + (s / g.sw);
-        p.tap_a16[t] = (uint32_t)(p.tap_phase[t] * p.gps * p.strip_pix + p.tap_shift[t]);
-      }
-    p.m_total = g.m_total;
-    p.m_tiles = g.m_tiles;
-    p.Hl = g.Hl; p.Wl = g.Wl; p.P = g.p; p.Q = g.q; p.N = g.n; p.K = g.k;
-    p.fault_key = -1;
-
     const int64_t crs = shape.c * shape.r * shape.s;
     const size_t wpk_bytes = (size_t)p.n_tiles * p.k_stages * p.b_stage_bytes;
     cuda_check(cudaMalloc(&pl->d_wpk, wpk_bytes), "cudaMalloc(wpk)");
@@ -111,20 +119,6 @@ abed_conv_plan* plan_create(const abed_layer_shape& shape, const int8_t* filters
     cuda_check(cudaMalloc(&pl->d_fsum, crs * 4), "cudaMalloc(fsum)");
     cuda_check(cudaMalloc(&pl->d_ic, crs * 4), "cudaMalloc(ic)");
     cuda_check(cudaMalloc(&pl->d_bsum, (size_t)g.n_phase * g.c16 * 16 * g.Hl * g.Wl * 4), "cudaMalloc(bsum)");
-    if (p.n_tiles > 1) {
-      cuda_check(cudaMalloc(&pl->d_fc_part, (size_t)p.n_tiles * p.m_tiles * 128 * 2 * 8), "cudaMalloc(fc_part)");
-      cuda_check(cudaMalloc(&pl->d_tile_sem, (size_t)p.m_tiles * 4), "cudaMalloc(tile_sem)");
-      cuda_check(cudaMemset(pl->d_tile_sem, 0, (size_t)p.m_tiles * 4), "memset tile_sem");
-    }
-    cuda_check(cudaMalloc(&pl->d_cta_rec, (size_t)conv_tc_grid(p, num_sms()) * 4 * 8), "cudaMalloc(cta_rec)");
-    cuda_check(cudaMalloc(&pl->d_kacc, 4 * 8), "cudaMalloc(kacc)");
-    cuda_check(cudaMemset(pl->d_kacc, 0, 4 * 8), "memset kacc");
-    cuda_check(cudaMalloc(&pl->d_outcome, 3 * sizeof(abed_verify_outcome)), "cudaMalloc(outcome)");
-    cuda_check(cudaMemset(pl->d_outcome, 0, 3 * sizeof(abed_verify_outcome)), "memset outcome");
-    cuda_check(cudaMalloc(&pl->d_acc, (4 + shape.k) * 8), "cudaMalloc(acc)");
-    cuda_check(cudaMemset(pl->d_acc, 0, (4 + shape.k) * 8), "memset acc");
-    cuda_check(cudaMalloc(&pl->d_zero_bias, shape.k * 4), "cudaMalloc(bias)");
-    cuda_check(cudaMemset(pl->d_zero_bias, 0, shape.k * 4), "memset bias");
 
     const int64_t rows = (int64_t)p.n_tiles * p.k_stages * p.ntaps * p.gps * p.block_n_tot;
     pack_filters_kernel<<<grid_for(rows), 256>>>(filters, g, p.block_n, p.block_n_tot, p.n_tiles, p.gps,
@@ -174,17 +168,30 @@ void plan_run(abed_conv_plan* pl, const int8_t* packed, const abed_epilog_params
     p.bias = pl->d_zero_bias;
     p.relu = 0;
   }
-  if (out_mode == ABED_OUT_I8_PACKED || out_mode == ABED_OUT_I8_COMPARE) {
+  const bool fmode = pl->dtype != abed_dev::DT_I8;
+  const bool h_out = out_mode == ABED_OUT_H_PACKED || out_mode == ABED_OUT_H_COMPARE;
+  const bool i_out = out_mode == ABED_OUT_I32_NCHW || out_mode == ABED_OUT_I8_NCHW || out_mode == ABED_OUT_I8_PACKED ||
+                     out_mode == ABED_OUT_I8_COMPARE;
+  if ((fmode && i_out) || (!fmode && h_out))
+    throw_invalid("conv plan: output mode does not match the plan's operand type");
+  p.dtype = pl->dtype;
+  p.tau_fc = pl->tau_fc;
+  p.tau_fic = pl->tau_fic;
+  p.facc = pl->d_facc;
+  p.rhs_ext_f = pl->d_rhs_f;
+  p.ficwf = pl->d_ficwf;
+  if (out_mode == ABED_OUT_I8_PACKED || out_mode == ABED_OUT_I8_COMPARE || out_mode == ABED_OUT_H_PACKED ||
+      out_mode == ABED_OUT_H_COMPARE) {
     if (next) {
       const ActGeom& o = next->g;
-      if (o.c != pl->g.k || o.h != pl->g.p || o.w != pl->g.q || o.n != pl->g.n)
+      if (o.c != pl->g.k || o.h != pl->g.p || o.w != pl->g.q || o.n != pl->g.n || o.cpg != pl->g.cpg)
         throw_invalid("conv plan: next layer input does not match this layer's output");
       p.o_plane_len = o.plane_len; p.o_Hl = o.Hl; p.o_Wl = o.Wl; p.o_ph = o.ph; p.o_pw = o.pw;
       p.o_sh = o.sh; p.o_sw = o.sw; p.o_nph_w = o.nph_w; p.o_c16 = o.c16;
     } else {
       // identity consumer geometry: 1x1, stride 1, pad 0
       abed_layer_shape s1{pl->shape.n, pl->shape.k, pl->shape.p, pl->shape.q, 1, 1, 1, 1, 1, 0, 0, pl->shape.p, pl->shape.q};
-      const ActGeom o = make_geom(s1);
+      const ActGeom o = make_geom(s1, pl->g.cpg);
       p.o_plane_len = o.plane_len; p.o_Hl = o.Hl; p.o_Wl = o.Wl; p.o_ph = 0; p.o_pw = 0;
       p.o_sh = 1; p.o_sw = 1; p.o_nph_w = 1; p.o_c16 = o.c16;
     }
@@ -203,7 +210,14 @@ void plan_run(abed_conv_plan* pl, const int8_t* packed, const abed_epilog_params
   if (pl->checks & ABED_CHECK_IC) cuda_check(cudaMemsetAsync(pl->d_acc + 4, 0, pl->shape.k * 8, st), "memset ic");
   if (out_mode == ABED_OUT_I8_COMPARE) cuda_check(cudaMemsetAsync(pl->d_acc + 1, 0, 8, st), "memset cmp");
   p.rhs_mode = 0;
-  if ((pl->checks & (ABED_CHECK_FIC | ABED_CHECK_IC)) && !pl->reuse_input_checksum) {
+  if (fmode && (pl->checks & ABED_CHECK_FIC) && !pl->reuse_input_checksum) {
+    // float mode: the input-checksum warps compute rhs = sum x * G in-kernel
+    const ActGeom& g = pl->g;
+    const int64_t cells = (int64_t)g.n_phase * g.c16 * g.Hl * g.Wl;
+    const int64_t want = 2LL * conv_tc_grid(p, num_sms()) * 64;
+    p.rhs_mode = 1;
+    p.rhs_nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(g.n, (want + cells - 1) / cells));
+  } else if (!fmode && (pl->checks & (ABED_CHECK_FIC | ABED_CHECK_IC)) && !pl->reuse_input_checksum) {
     // input checksum of the pristine input (FR option)
     const ActGeom& g = pl->g;
     if (pl->checks & ABED_CHECK_IC) {
@@ -299,6 +313,7 @@ int abed_conv_plan_destroy(abed_conv_plan* pl) {
   cudaFree(pl->d_wpk); cudaFree(pl->d_filters); cudaFree(pl->d_fsum); cudaFree(pl->d_ic);
   cudaFree(pl->d_bsum); cudaFree(pl->d_ficw); cudaFree(pl->d_ficw8); cudaFree(pl->d_fc_part); cudaFree(pl->d_tile_sem);
   cudaFree(pl->d_cta_rec); cudaFree(pl->d_kacc); cudaFree(pl->d_outcome);
+  cudaFree(pl->d_facc); cudaFree(pl->d_rhs_f); cudaFree(pl->d_ficwf); cudaFree(pl->d_fsum_f);
   cudaFree(pl->d_acc); cudaFree(pl->d_zero_bias);
   delete pl;
   return ABED_OK;

@@ -27,9 +27,12 @@
 // init, TMEM allocation and the resident-filter prefetch overlap the previous
 // kernel's tail; activations, outputs and accumulators are touched only after
 // griddepcontrol.wait.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "abed_b200.h"
 #include "conv_tc.cuh"
@@ -116,6 +119,24 @@ __device__ __forceinline__ void fc_note(FcRec& r, int64_t key, int64_t lhs, int6
     r.rhs = rhs;
   }
 }
+// exact (int64) or float-mode (f64) sums travel through int64 slots as bits
+__device__ __forceinline__ int64_t acc_bits(int64_t v) { return v; }
+__device__ __forceinline__ int64_t acc_bits(double v) { return __double_as_longlong(v); }
+template <typename T>
+__device__ __forceinline__ T bits_acc(int64_t b) {
+  if constexpr (std::is_same_v<T, double>)
+    return __longlong_as_double(b);
+  else
+    return b;
+}
+// fc_verify (exact, checksum.hpp:211-236) / fc_verify_f32 (|lhs - rhs| <= tau, :541-565)
+template <int DT, typename T>
+__device__ __forceinline__ bool fc_mismatch(T lhs, T rhs, double tau) {
+  if constexpr (DT == DT_I8)
+    return lhs != rhs;
+  else
+    return !(fabs(static_cast<double>(lhs) - static_cast<double>(rhs)) <= tau);
+}
 __device__ __forceinline__ FcRec fc_warp_reduce(FcRec r) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -137,6 +158,34 @@ __device__ __forceinline__ long long warp_sum(long long s) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   return s;
+}
+
+__device__ __forceinline__ double warp_sum_d(double s) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  return s;
+}
+
+// two floats -> two 16-bit storage values (fp16 or bf16, round to nearest even)
+template <int DT>
+__device__ __forceinline__ uint32_t pack_h2(float a, float b) {
+  if constexpr (DT == DT_BF16) {
+    const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<const uint32_t*>(&h);
+  } else {
+    const __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<const uint32_t*>(&h);
+  }
+}
+// one 32-bit word of two 16-bit storage values -> two floats
+template <int DT>
+__device__ __forceinline__ float2 unpack_h2(uint32_t w) {
+  if constexpr (DT == DT_BF16) {
+    return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
+  } else {
+    __half2 h = *reinterpret_cast<const __half2*>(&w);
+    return __half22float2(h);
+  }
 }
 
 __device__ __forceinline__ void write_outcome_dev(abed_verify_outcome* o, int mismatch, int has_locus, int64_t l0,
@@ -203,8 +252,13 @@ __device__ __forceinline__ int64_t epi_chunk(const ConvTcParams& p, const EpiCtx
   }
   if (EPI == EPI_PACKED || EPI == EPI_COMPARE) {
     int32_t y[16];
+    if (p.dbg & 16) {  // timing experiment: skip the requantise math
 #pragma unroll
-    for (int j = 0; j < 16; ++j) y[j] = requant_i8(a[j], p.scale, b[j], RELU ? 1 : 0);
+      for (int j = 0; j < 16; ++j) y[j] = a[j];
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) y[j] = requant_i8(a[j], p.scale, b[j], RELU ? 1 : 0);
+    }
     if (SLOW) {
 #pragma unroll
       for (int j = 0; j < 16; ++j)
@@ -244,6 +298,71 @@ __device__ __forceinline__ int64_t epi_chunk(const ConvTcParams& p, const EpiCtx
   return sum;
 }
 
+// Float mode (fp16 / bf16 operands): one 16-channel chunk of f32 accumulators.
+// Row sum in f64 (checksum.hpp:524 reduce_all_f64 / :541 fc_verify_f32 reduce
+// in double); epilog v = fma(acc, scale, bias), ReLU, then f32 NCHW or 16-bit
+// packed output (8 channels per 16-byte pixel).
+template <int DT, int EPI, bool RELU, bool SUMS, bool SLOW>
+__device__ __forceinline__ double epi_chunk_h(const ConvTcParams& p, const EpiCtx& e, uint32_t (&v)[16],
+                                              const float (&b)[16], int k0) {
+  if (SLOW) {
+    if (e.fault_row && e.fk_k >= k0 && e.fk_k < k0 + 16) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (k0 + j == e.fk_k) v[j] ^= 1u << p.fault_bit;
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (k0 + j >= p.K) v[j] = 0u;
+  }
+  float a[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) a[j] = __uint_as_float(v[j]);
+  double sum = 0.0;
+  if (SUMS) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) sum += static_cast<double>(a[j]);
+  }
+  if (EPI == EPI_PACKED || EPI == EPI_COMPARE) {
+    float y[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      y[j] = __fmaf_rn(a[j], p.scale, b[j]);
+      if (RELU) y[j] = fmaxf(y[j], 0.0f);
+      if (SLOW && k0 + j >= p.K) y[j] = 0.0f;
+    }
+    const uint4 lo = make_uint4(pack_h2<DT>(y[0], y[1]), pack_h2<DT>(y[2], y[3]), pack_h2<DT>(y[4], y[5]),
+                                pack_h2<DT>(y[6], y[7]));
+    const uint4 hi = make_uint4(pack_h2<DT>(y[8], y[9]), pack_h2<DT>(y[10], y[11]), pack_h2<DT>(y[12], y[13]),
+                                pack_h2<DT>(y[14], y[15]));
+    const int64_t plane_bytes = p.o_plane_len * 16;
+    uint4* dst0 = reinterpret_cast<uint4*>(e.pk_row + static_cast<int64_t>(k0 >> 3) * plane_bytes);
+    uint4* dst1 = reinterpret_cast<uint4*>(e.pk_row + static_cast<int64_t>((k0 >> 3) + 1) * plane_bytes);
+    if (EPI == EPI_PACKED) {
+      if (e.valid) {
+        *dst0 = lo;
+        *dst1 = hi;
+      }
+    } else if (e.valid) {
+      const uint4 r0 = *dst0, r1 = *dst1;
+      const bool same = r0.x == lo.x && r0.y == lo.y && r0.z == lo.z && r0.w == lo.w && r1.x == hi.x &&
+                        r1.y == hi.y && r1.z == hi.z && r1.w == hi.w;
+      if (!same) atomicAdd(p.cmp_count, 1ull);
+    }
+  } else if (EPI == EPI_NCHW) {
+    if (e.valid) {
+      float* o = static_cast<float*>(p.out) + e.nchw_row + static_cast<int64_t>(k0) * e.PQ;
+      for (int j = 0; j < 16; ++j)
+        if (k0 + j < p.K) {
+          float f = __fmaf_rn(a[j], p.scale, b[j]);
+          if (RELU && f < 0.0f) f = 0.0f;
+          o[j * e.PQ] = f;
+        }
+    }
+  }
+  return sum;
+}
+
 __device__ __forceinline__ void load_bias16(const ConvTcParams& p, const EpiCtx& e, int k0, float (&b)[16]) {
   if (e.bias_smem) {
     const float4* b4 = reinterpret_cast<const float4*>(e.bias_smem + k0);
@@ -261,27 +380,53 @@ __device__ __forceinline__ void load_bias16(const ConvTcParams& p, const EpiCtx&
   }
 }
 
-// Chunks [c_lo, c_hi) of one row, 16 columns per step.  TMEM loads are software
-// pipelined (the next chunk's tcgen05.ld is in flight while this one is
+// Chunks [c_lo, c_hi) of one row, 32 columns per step.  TMEM loads are software
+// pipelined (the next step's tcgen05.ld is in flight while this one is
 // processed) and the biases are read before the wait.  The loop body is not
 // unrolled across steps, so the epilogue stays resident in the instruction cache.
-template <int EPI, bool RELU, bool SUMS, bool SLOW>
-__device__ __forceinline__ int64_t epi_columns(const ConvTcParams& p, const EpiCtx& e, uint32_t t_row, int k_base,
-                                               int c_lo, int c_hi) {
-  int64_t row_sum = 0;
-  if (c_lo >= c_hi) return row_sum;
-  uint32_t v[16];
-  tmem_ld16(t_row + c_lo * 16, v);
-#pragma unroll 1
-  for (int c = c_lo; c < c_hi; ++c) {
-    float b[16];
-    load_bias16(p, e, k_base + c * 16, b);
-    tmem_ld_wait();
-    int32_t a[16];
+// An odd trailing chunk is loaded as a 16-column step.
+template <int DT, int EPI, bool RELU, bool SUMS, bool SLOW>
+__device__ __forceinline__ std::conditional_t<DT == DT_I8, int64_t, double> epi_columns(
+    const ConvTcParams& p, const EpiCtx& e, uint32_t t_row, int k_base, int c_lo, int c_hi) {
+  std::conditional_t<DT == DT_I8, int64_t, double> row_sum = 0;
+  auto chunk = [&](uint32_t (&v)[16], const float (&b)[16], int k0) {
+    if constexpr (DT == DT_I8) {
+      int32_t a[16];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) a[j] = static_cast<int32_t>(v[j]);
-    if (c + 1 < c_hi) tmem_ld16(t_row + (c + 1) * 16, v);
-    row_sum += epi_chunk<EPI, RELU, SUMS, SLOW>(p, e, a, b, k_base + c * 16);
+      for (int j = 0; j < 16; ++j) a[j] = static_cast<int32_t>(v[j]);
+      row_sum += epi_chunk<EPI, RELU, SUMS, SLOW>(p, e, a, b, k0);
+    } else {
+      row_sum += epi_chunk_h<DT, EPI, RELU, SUMS, SLOW>(p, e, v, b, k0);
+    }
+  };
+  const int pairs_end = c_lo + ((c_hi - c_lo) & ~1);
+  if (c_lo < pairs_end) {
+    uint32_t v[32];
+    tmem_ld32(t_row + c_lo * 16, v);
+#pragma unroll 1
+    for (int c = c_lo; c < pairs_end; c += 2) {
+      float b[16];
+      load_bias16(p, e, k_base + c * 16, b);
+      tmem_ld_wait();
+      uint32_t a0[16], a1[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        a0[j] = v[j];
+        a1[j] = v[16 + j];
+      }
+      if (c + 2 < pairs_end) tmem_ld32(t_row + (c + 2) * 16, v);
+      chunk(a0, b, k_base + c * 16);
+      load_bias16(p, e, k_base + (c + 1) * 16, b);
+      chunk(a1, b, k_base + (c + 1) * 16);
+    }
+  }
+  if (pairs_end < c_hi) {
+    uint32_t v[16];
+    tmem_ld16(t_row + pairs_end * 16, v);
+    float b[16];
+    load_bias16(p, e, k_base + pairs_end * 16, b);
+    tmem_ld_wait();
+    chunk(v, b, k_base + pairs_end * 16);
   }
   return row_sum;
 }
@@ -303,9 +448,14 @@ struct MmaEnv {
   long long t_entry;
 };
 
+template <int DT>
 __device__ __forceinline__ void issue_one(uint32_t d_tmem, uint32_t a_hi, uint32_t b_hi, uint32_t ao, uint32_t bo,
                                           uint32_t idesc, uint32_t accum) {
-  mma_i8_w(d_tmem, (static_cast<uint64_t>(a_hi) << 32) | ao, (static_cast<uint64_t>(b_hi) << 32) | bo, idesc, accum);
+  const uint64_t ad = (static_cast<uint64_t>(a_hi) << 32) | ao, bd = (static_cast<uint64_t>(b_hi) << 32) | bo;
+  if constexpr (DT == DT_I8)
+    mma_i8_w(d_tmem, ad, bd, idesc, accum);  // K = 32 int8, s32 accumulate
+  else
+    mma_f16_w(d_tmem, ad, bd, idesc, accum);  // K = 16 fp16/bf16, f32 accumulate
 }
 
 // The MMA warp.  Per stage: every tap (r, s) x channel-group pair g; tap (r, s)
@@ -317,13 +467,14 @@ __device__ __forceinline__ void issue_one(uint32_t d_tmem, uint32_t a_hi, uint32
 // a loop that recomputes offsets from runtime geometry costs 85-128 cycles of
 // issue per MMA (tools/mma_microbench3.cu), more than the MMA itself.
 // R == 0: generic runtime loop (any filter size / stride).
-template <int R, int S, int SH, int SW, int GPS>
+template <int DT, int R, int S, int SH, int SW, int GPS>
 __device__ __forceinline__ void mma_warp_run(const ConvTcParams& p, const MmaEnv& v) {
   constexpr int NM = R > 0 ? R * S * (GPS / 2) : 1;
   const uint32_t strip16 = p.strip_pix;  // channel-group stride of the A strips (16-B units)
   const uint32_t blbo16 = p.block_n_tot;
   // the planner keeps block_n_tot <= 256: one MMA spans the N tile
-  const uint32_t idesc = make_idesc_i8(static_cast<uint32_t>(p.block_n_tot));
+  const uint32_t idesc = DT == DT_I8 ? make_idesc_i8(static_cast<uint32_t>(p.block_n_tot))
+                                     : make_idesc_f16(static_cast<uint32_t>(p.block_n_tot), DT == DT_BF16);
   uint32_t aoff[NM], boff[NM];
   if (R > 0) {
     constexpr int NPH_W = S < SW ? S : SW;
@@ -358,8 +509,7 @@ __device__ __forceinline__ void mma_warp_run(const ConvTcParams& p, const MmaEnv
       tc_fence_after();
       const uint32_t d_tmem = v.tmem_base + as * v.acc_cols;
       for (int ks = 0; ks < p.k_stages; ++ks) {
-        if ((p.dbg & 4) && (u * p.k_stages + ks) >= p.n_stages) {
-        } else if (v.trace) {
+        if (v.trace) {
           const long long w0 = clock64();
           mbar_wait(&v.full[stage], phase);
           const long long w1 = clock64();
@@ -379,7 +529,7 @@ __device__ __forceinline__ void mma_warp_run(const ConvTcParams& p, const MmaEnv
         if (R > 0) {
 #pragma unroll
           for (int i = 0; i < NM; ++i)
-            issue_one(d_tmem, a_hi, b_hi, a_lo + aoff[i], b_lo + boff[i], idesc, i > 0 ? 1u : accum);
+            issue_one<DT>(d_tmem, a_hi, b_hi, a_lo + aoff[i], b_lo + boff[i], idesc, i > 0 ? 1u : accum);
         } else {
           const uint32_t ph_row = static_cast<uint32_t>(p.nph_w * p.gps) * strip16;
           const uint32_t ph_col = static_cast<uint32_t>(p.gps) * strip16;
@@ -391,7 +541,7 @@ __device__ __forceinline__ void mma_warp_run(const ConvTcParams& p, const MmaEnv
             for (int sc = 0; sc < p.S; ++sc) {
               const uint32_t ao = roff + s_ph * ph_col + s_q;
               for (int g = 0; g < p.gps; g += 2) {
-                issue_one(d_tmem, a_hi, b_hi, ao + g * strip16, bo + g * blbo16, idesc, accum);
+                issue_one<DT>(d_tmem, a_hi, b_hi, ao + g * strip16, bo + g * blbo16, idesc, accum);
                 accum = 1u;
               }
               bo += static_cast<uint32_t>(p.gps) * blbo16;
@@ -406,7 +556,7 @@ __device__ __forceinline__ void mma_warp_run(const ConvTcParams& p, const MmaEnv
             }
           }
         }
-        if (!(p.dbg & 4)) mma_commit_w(&v.empty[stage]);
+        mma_commit_w(&v.empty[stage]);
         if (++stage == p.n_stages) {
           stage = 0;
           phase ^= 1u;
@@ -431,8 +581,9 @@ enum MmaPattern : int {
   PAT_1x1_S1_G4 = 5, PAT_1x1_S1_G2 = 6, PAT_1x1_S2_G4 = 7, PAT_1x1_S2_G2 = 8,
 };
 
-template <int EPI, bool FC, bool FIC>
+template <int DT, int EPI, bool FC, bool FIC>
 __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __grid_constant__ ConvTcParams p) {
+  using Acc = std::conditional_t<DT == DT_I8, int64_t, double>;  // exact int / f64 float-mode sums
   extern __shared__ __align__(128) uint8_t smem[];
   const SmemLayout L = smem_layout(p);
   uint8_t* sA = smem + L.a_off;
@@ -518,29 +669,34 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
           bulk_g2s_evict_last_w(sB + o, src + o, sz, bres, pol_b);
         }
       }
+      const uint32_t strip_bytes = p.strip_pix * 16u;
+      const uint32_t bytes = L.a_stage_bytes + (p.b_resident ? 0u : p.b_stage_bytes);
+      // streamed filters: the first ring fill's B blocks do not depend on the
+      // previous kernel either, so they are requested before the PDL wait too
+      const int total_stages = n_units * p.k_stages;
+      const int pre = p.b_resident ? 0 : (total_stages < p.n_stages ? total_stages : p.n_stages);
+      for (int i = 0; i < pre; ++i) {
+        int mt, nt;
+        decode_tile(p, i / p.k_stages, mt, nt);
+        const int ks = i % p.k_stages;
+        mbar_arrive_expect_tx_w(&full[i], bytes);
+        const int8_t* src = p.wpk + (static_cast<int64_t>(nt) * p.k_stages + ks) * p.b_stage_bytes;
+        bulk_g2s_evict_last_w(sB + i * p.b_stage_bytes, src, p.b_stage_bytes, &full[i], pol_b);
+      }
       pdl_wait();
       int stage = 0;
       uint32_t phase = 0;
-      const uint32_t strip_bytes = p.strip_pix * 16u;
-      const uint32_t bytes = L.a_stage_bytes + (p.b_resident ? 0u : p.b_stage_bytes);
       if (trace && lane == 0) trace[8] = clock64() - t_entry;
       for (int u = 0; u < n_units; ++u) {
         int mt, nt;
         decode_tile(p, u, mt, nt);
         const int64_t m0 = static_cast<int64_t>(mt) * kBlockM;
         for (int ks = 0; ks < p.k_stages; ++ks) {
-          if ((p.dbg & 4) && (u * p.k_stages + ks) >= p.n_stages) break;
-          mbar_wait(&empty[stage], phase ^ 1u);
-          if ((p.dbg & 2) && (u * p.k_stages + ks) >= p.n_stages) {
-            // timing experiment: stop copying once the ring is full
-            mbar_arrive_expect_tx_w(&full[stage], 0);
-            if (++stage == p.n_stages) {
-              stage = 0;
-              phase ^= 1u;
-            }
-            continue;
+          const bool prefetched = u * p.k_stages + ks < pre;
+          if (!prefetched) {
+            mbar_wait(&empty[stage], phase ^ 1u);
+            mbar_arrive_expect_tx_w(&full[stage], bytes);
           }
-          mbar_arrive_expect_tx_w(&full[stage], bytes);
           uint8_t* dstA = sA + stage * L.a_stage_bytes;
           for (int ph = 0; ph < p.n_phase; ++ph) {
             for (int g = 0; g < p.gps; ++g) {
@@ -549,7 +705,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
               bulk_g2s_w(dstA + (ph * p.gps + g) * strip_bytes, src, strip_bytes, &full[stage]);
             }
           }
-          if (!p.b_resident) {
+          if (!p.b_resident && !prefetched) {
             const int8_t* src = p.wpk + (static_cast<int64_t>(nt) * p.k_stages + ks) * p.b_stage_bytes;
             bulk_g2s_evict_last_w(sB + stage * p.b_stage_bytes, src, p.b_stage_bytes, &full[stage], pol_b);
           }
@@ -583,15 +739,15 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
     v.trace = trace;
     v.t_entry = t_entry;
     switch (p.mma_pattern) {
-      case PAT_3x3_S1_G4: mma_warp_run<3, 3, 1, 1, 4>(p, v); break;
-      case PAT_3x3_S1_G2: mma_warp_run<3, 3, 1, 1, 2>(p, v); break;
-      case PAT_3x3_S2_G4: mma_warp_run<3, 3, 2, 2, 4>(p, v); break;
-      case PAT_3x3_S2_G2: mma_warp_run<3, 3, 2, 2, 2>(p, v); break;
-      case PAT_1x1_S1_G4: mma_warp_run<1, 1, 1, 1, 4>(p, v); break;
-      case PAT_1x1_S1_G2: mma_warp_run<1, 1, 1, 1, 2>(p, v); break;
-      case PAT_1x1_S2_G4: mma_warp_run<1, 1, 2, 2, 4>(p, v); break;
-      case PAT_1x1_S2_G2: mma_warp_run<1, 1, 2, 2, 2>(p, v); break;
-      default: mma_warp_run<0, 0, 1, 1, 2>(p, v); break;
+      case PAT_3x3_S1_G4: mma_warp_run<DT, 3, 3, 1, 1, 4>(p, v); break;
+      case PAT_3x3_S1_G2: mma_warp_run<DT, 3, 3, 1, 1, 2>(p, v); break;
+      case PAT_3x3_S2_G4: mma_warp_run<DT, 3, 3, 2, 2, 4>(p, v); break;
+      case PAT_3x3_S2_G2: mma_warp_run<DT, 3, 3, 2, 2, 2>(p, v); break;
+      case PAT_1x1_S1_G4: mma_warp_run<DT, 1, 1, 1, 1, 4>(p, v); break;
+      case PAT_1x1_S1_G2: mma_warp_run<DT, 1, 1, 1, 1, 2>(p, v); break;
+      case PAT_1x1_S2_G4: mma_warp_run<DT, 1, 1, 2, 2, 4>(p, v); break;
+      case PAT_1x1_S2_G2: mma_warp_run<DT, 1, 1, 2, 2, 2>(p, v); break;
+      default: mma_warp_run<DT, 0, 0, 1, 1, 2>(p, v); break;
     }
   } else if (warp < 2 + kEpiWarps) {
     // ------------------------------------------------------------ epilogue
@@ -621,7 +777,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
     }
     const uint32_t HlWl = static_cast<uint32_t>(p.Hl) * p.Wl;
     FcRec fc{0, kNoKey, 0, 0};
-    long long fic_sum = 0;
+    Acc fic_sum = 0;
     long long tr_wait = 0, tr_acc = 0, tr_proc = 0;  // diagnostics (registers)
     const int nch = p.block_n >> 4;  // 16-column chunks of real output channels
     const int h0 = (nch + 1) >> 1;
@@ -673,14 +829,14 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
       if (FC && half == 0) tmem_ld4(t_row + p.block_n, dig);
       // fast path: no fault hook, no filler channels, no IC column sums (warp-uniform)
       const bool slow = p.fault_key >= 0 || (p.check & CHECK_IC) || k_base + c_hi * 16 > p.K;
-      int64_t row_sum = 0;
+      Acc row_sum = 0;
       if (p.dbg & 1) {
       } else if (!slow) {
-        row_sum = p.relu ? epi_columns<EPI, true, FC || FIC, false>(p, e, t_row, k_base, c_lo, c_hi)
-                         : epi_columns<EPI, false, FC || FIC, false>(p, e, t_row, k_base, c_lo, c_hi);
+        row_sum = p.relu ? epi_columns<DT, EPI, true, FC || FIC, false>(p, e, t_row, k_base, c_lo, c_hi)
+                         : epi_columns<DT, EPI, false, FC || FIC, false>(p, e, t_row, k_base, c_lo, c_hi);
       } else {
-        row_sum = p.relu ? epi_columns<EPI, true, FC || FIC, true>(p, e, t_row, k_base, c_lo, c_hi)
-                         : epi_columns<EPI, false, FC || FIC, true>(p, e, t_row, k_base, c_lo, c_hi);
+        row_sum = p.relu ? epi_columns<DT, EPI, true, FC || FIC, true>(p, e, t_row, k_base, c_lo, c_hi)
+                         : epi_columns<DT, EPI, false, FC || FIC, true>(p, e, t_row, k_base, c_lo, c_hi);
       }
       // accumulator consumed: hand the TMEM stage back to the MMA warp
       tc_fence_before();
@@ -691,23 +847,31 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
       if (FIC) fic_sum += row_sum;
       if (FC) {
         // combine the two column halves of each row
-        if (half == 1) s_rowsum[row] = row_sum;
+        if (half == 1) s_rowsum[row] = acc_bits(row_sum);
         named_bar(kBarQuarter0 + quarter, 64);
         if (half == 0) {
-          row_sum += s_rowsum[row];
-          // checksum.hpp:179-196 recombination of the (balanced) digit columns
-          const int64_t extra = valid ? static_cast<int64_t>(static_cast<int32_t>(dig[0])) +
-                                            (static_cast<int64_t>(static_cast<int32_t>(dig[1])) << 8) +
-                                            (static_cast<int64_t>(static_cast<int32_t>(dig[2])) << 16)
-                                      : 0;
+          row_sum += bits_acc<Acc>(s_rowsum[row]);
+          Acc extra = 0;
+          if (valid) {
+            if constexpr (DT == DT_I8) {
+              // checksum.hpp:179-196 recombination of the (balanced) digit columns
+              extra = static_cast<int64_t>(static_cast<int32_t>(dig[0])) +
+                      (static_cast<int64_t>(static_cast<int32_t>(dig[1])) << 8) +
+                      (static_cast<int64_t>(static_cast<int32_t>(dig[2])) << 16);
+            } else {
+              // float mode: the filter checksum rides as hi + lo + lo2 split rows
+              extra = static_cast<double>(__uint_as_float(dig[0])) + static_cast<double>(__uint_as_float(dig[1])) +
+                      static_cast<double>(__uint_as_float(dig[2]));
+            }
+          }
           if (p.n_tiles == 1) {
-            if (valid && row_sum != extra) fc_note(fc, key, row_sum, extra);
+            if (valid && fc_mismatch<DT>(row_sum, extra, p.tau_fc)) fc_note(fc, key, acc_bits(row_sum), acc_bits(extra));
           } else {
             // row partial of this N tile; the CTA that completes the M tile's
             // last N tile checks the full-channel sums (fc_verify, :211-236)
             int64_t* part = p.fc_part + (static_cast<int64_t>(nt) * p.m_tiles * kBlockM + m) * 2;
-            part[0] = row_sum;
-            part[1] = extra;
+            part[0] = acc_bits(row_sum);
+            part[1] = acc_bits(extra);
             __threadfence();
             named_bar(kBarHalf0, 128);
             if (row == 0) {
@@ -718,13 +882,13 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
             if (s_tile_last) {
               __threadfence();
               if (valid) {
-                int64_t l = 0, r = 0;
+                Acc l = 0, r = 0;
                 for (int t = 0; t < p.n_tiles; ++t) {
                   const int64_t* q = p.fc_part + (static_cast<int64_t>(t) * p.m_tiles * kBlockM + m) * 2;
-                  l += __ldcg(q);
-                  r += __ldcg(q + 1);
+                  l += bits_acc<Acc>(__ldcg(q));
+                  r += bits_acc<Acc>(__ldcg(q + 1));
                 }
-                if (l != r) fc_note(fc, key, l, r);
+                if (fc_mismatch<DT>(l, r, p.tau_fc)) fc_note(fc, key, acc_bits(l), acc_bits(r));
               }
               if (row == 0) p.tile_sem[mt] = 0u;  // ready for the next run
             }
@@ -745,8 +909,13 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
       if (lane == 0) s_fc[ew] = w;
     }
     if (FIC) {
-      const long long w = warp_sum(fic_sum);
-      if (lane == 0) s_lhs[ew] = w;
+      if constexpr (DT == DT_I8) {
+        const long long w = warp_sum(fic_sum);
+        if (lane == 0) s_lhs[ew] = w;
+      } else {
+        const double w = warp_sum_d(fic_sum);
+        if (lane == 0) s_lhs[ew] = __double_as_longlong(w);
+      }
     }
   } else {
     // ------------------------------------------------------------ input checksum
@@ -756,7 +925,50 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
     // chunk costs 12 dp4a; every image load of a work item is issued before use.
     const int rw = warp - (2 + kEpiWarps);
     long long acc = 0;
-    if (FIC && p.rhs_mode) {
+    double facc_rhs = 0.0;
+    if (DT != DT_I8 && FIC && p.rhs_mode) {
+      // float mode: G in f32 [plane][pix][8]; 8 fp16/bf16 values per 16-byte
+      // chunk, f32 FMAs per work item, f64 across items (reduce in double like
+      // input_checksum_f64 / fic_dot_f64, checksum.hpp:496-535)
+      pdl_wait();
+      const int64_t HlWl = static_cast<int64_t>(p.Hl) * p.Wl;
+      const int nsplit = p.rhs_nsplit;
+      const int64_t total = static_cast<int64_t>(p.n_phase) * p.c16 * HlWl * nsplit;
+      const int64_t stride = static_cast<int64_t>(gridDim.x) * (kRhsWarps * 32);
+      for (int64_t idx = static_cast<int64_t>(blockIdx.x) * (kRhsWarps * 32) + rw * 32 + lane; idx < total;
+           idx += stride) {
+        const int64_t pix = idx % HlWl;
+        const int64_t rest = idx / HlWl;
+        const int split = static_cast<int>(rest % nsplit);
+        const int64_t plane = rest / nsplit;
+        const float4* gw = reinterpret_cast<const float4*>(p.ficwf) + (plane * HlWl + pix) * 2;
+        const float4 ga = __ldg(gw), gb = __ldg(gw + 1);
+        const uint4* src = reinterpret_cast<const uint4*>(p.act) + plane * p.plane_len + pix;
+        const int n0 = static_cast<int>(static_cast<int64_t>(p.N) * split / nsplit);
+        const int n1 = static_cast<int>(static_cast<int64_t>(p.N) * (split + 1) / nsplit);
+        float item = 0.0f;
+        for (int n = n0; n < n1; n += 4) {
+          uint4 x[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            x[j] = n + j < n1 ? __ldcg(src + static_cast<int64_t>(n + j) * HlWl) : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float2 x0 = unpack_h2<DT>(x[j].x), x1 = unpack_h2<DT>(x[j].y), x2 = unpack_h2<DT>(x[j].z),
+                         x3 = unpack_h2<DT>(x[j].w);
+            item = __fmaf_rn(x0.x, ga.x, item);
+            item = __fmaf_rn(x0.y, ga.y, item);
+            item = __fmaf_rn(x1.x, ga.z, item);
+            item = __fmaf_rn(x1.y, ga.w, item);
+            item = __fmaf_rn(x2.x, gb.x, item);
+            item = __fmaf_rn(x2.y, gb.y, item);
+            item = __fmaf_rn(x3.x, gb.z, item);
+            item = __fmaf_rn(x3.y, gb.w, item);
+          }
+        }
+        facc_rhs += static_cast<double>(item);
+      }
+    } else if (DT == DT_I8 && FIC && p.rhs_mode) {
       pdl_wait();
       const int64_t HlWl = static_cast<int64_t>(p.Hl) * p.Wl;
       const int nsplit = p.rhs_nsplit;
@@ -805,7 +1017,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
       pdl_wait();
     }
     if (FIC) {
-      const long long w = warp_sum(acc);
+      const long long w = DT == DT_I8 ? warp_sum(acc) : __double_as_longlong(warp_sum_d(facc_rhs));
       if (lane == 0) s_rhs[rw] = w;
     }
   }
@@ -842,10 +1054,17 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
         rec[3] = r.rhs;
       }
       if (FIC) {
-        long long l = 0;
-        for (int w = 0; w < kEpiWarps; ++w) l += s_lhs[w];
-        atomicAdd(&p.kacc[0], static_cast<unsigned long long>(l));
-        if (p.rhs_mode) atomicAdd(&p.kacc[1], static_cast<unsigned long long>(s_rhs[0] + s_rhs[1]));
+        if constexpr (DT == DT_I8) {
+          long long l = 0;
+          for (int w = 0; w < kEpiWarps; ++w) l += s_lhs[w];
+          atomicAdd(&p.kacc[0], static_cast<unsigned long long>(l));
+          if (p.rhs_mode) atomicAdd(&p.kacc[1], static_cast<unsigned long long>(s_rhs[0] + s_rhs[1]));
+        } else {
+          double l = 0.0;
+          for (int w = 0; w < kEpiWarps; ++w) l += __longlong_as_double(s_lhs[w]);
+          atomicAdd(&p.facc[0], l);
+          if (p.rhs_mode) atomicAdd(&p.facc[1], __longlong_as_double(s_rhs[0]) + __longlong_as_double(s_rhs[1]));
+        }
       }
       __threadfence();
       const unsigned long long ticket = atomicAdd(&p.kacc[2], 1ull);
@@ -873,13 +1092,31 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
         r = fc_warp_reduce(r);
         if (lane == 0) {
           const int64_t PQ = static_cast<int64_t>(p.P) * p.Q;
-          if (r.cnt == 0)
+          if (r.cnt == 0) {
             write_outcome_dev(out + 0, 0, 0, 0, 0, 0, 0, 0, 0);
-          else
+          } else if (DT == DT_I8) {
             write_outcome_dev(out + 0, 1, 1, r.key / PQ, (r.key % PQ) / p.Q, r.key % p.Q, r.lhs, r.rhs, r.cnt);
+          } else {
+            // fc_verify_f32: the float pair of the first failing position (:557-561)
+            write_outcome_dev(out + 0, 1, 1, r.key / PQ, (r.key % PQ) / p.Q, r.key % p.Q, 0, 0, r.cnt);
+            out[0].lhs_f = __longlong_as_double(r.lhs);
+            out[0].rhs_f = __longlong_as_double(r.rhs);
+          }
         }
       }
-      if (FIC && lane == 0) {
+      if (DT != DT_I8 && FIC && lane == 0) {
+        const double lhs = __ldcg(&p.facc[0]);
+        const double rhs = p.rhs_mode ? __ldcg(&p.facc[1]) : __ldcg(p.rhs_ext_f);
+        // float_verify (checksum.hpp:474-481): mismatch unless |lhs - rhs| <= tau
+        const int bad = !(fabs(lhs - rhs) <= p.tau_fic);
+        write_outcome_dev(out + 1, bad, 0, 0, 0, 0, 0, 0, bad);
+        out[1].lhs_f = lhs;
+        out[1].rhs_f = rhs;
+        if (p.rhs_mode) *p.rhs_ext_f = rhs;
+        p.facc[0] = 0.0;
+        p.facc[1] = 0.0;
+      }
+      if (DT == DT_I8 && FIC && lane == 0) {
         const long long lhs = static_cast<long long>(__ldcg(&p.kacc[0]));
         const long long rhs = p.rhs_mode ? static_cast<long long>(__ldcg(&p.kacc[1]))
                                          : static_cast<long long>(__ldcg(p.rhs_ext));
@@ -895,6 +1132,11 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
       }
     }
   }
+  if (trace && threadIdx.x == 0) {
+    uint64_t gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    trace[14] = static_cast<int64_t>(gt);
+  }
 }
 
 }  // namespace abed_dev
@@ -908,10 +1150,10 @@ using abed_dev::ConvTcParams;
 
 uint32_t conv_tc_smem_bytes(const ConvTcParams& p) { return abed_dev::smem_layout(p).total; }
 
-template <int EPI, bool FC, bool FIC>
+template <int DT, int EPI, bool FC, bool FIC>
 static cudaError_t launch_variant(const ConvTcParams& p, int grid, bool pdl, cudaStream_t stream) {
   static bool attr_done = false;
-  auto kern = abed_dev::conv_i8_tc_kernel<EPI, FC, FIC>;
+  auto kern = abed_dev::conv_i8_tc_kernel<DT, EPI, FC, FIC>;
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, abed_dev::kConvDynSmemMax);
     if (e != cudaSuccess) return e;
@@ -930,13 +1172,13 @@ static cudaError_t launch_variant(const ConvTcParams& p, int grid, bool pdl, cud
   return cudaLaunchKernelEx(&cfg, kern, p);
 }
 
-template <int EPI>
+template <int DT, int EPI>
 static cudaError_t launch_epi(const ConvTcParams& p, int grid, bool pdl, cudaStream_t st) {
   const bool fc = (p.check & abed_dev::CHECK_FC) != 0, fic = (p.check & abed_dev::CHECK_FIC) != 0;
-  if (fc && fic) return launch_variant<EPI, true, true>(p, grid, pdl, st);
-  if (fc) return launch_variant<EPI, true, false>(p, grid, pdl, st);
-  if (fic) return launch_variant<EPI, false, true>(p, grid, pdl, st);
-  return launch_variant<EPI, false, false>(p, grid, pdl, st);
+  if (fc && fic) return launch_variant<DT, EPI, true, true>(p, grid, pdl, st);
+  if (fc) return launch_variant<DT, EPI, true, false>(p, grid, pdl, st);
+  if (fic) return launch_variant<DT, EPI, false, true>(p, grid, pdl, st);
+  return launch_variant<DT, EPI, false, false>(p, grid, pdl, st);
 }
 
 int conv_tc_grid(const ConvTcParams& p, int num_sms) {
@@ -953,13 +1195,24 @@ int conv_tc_grid(const ConvTcParams& p, int num_sms) {
   return grid;
 }
 
+template <int DT>
+static cudaError_t launch_dt(const ConvTcParams& p, int grid, bool pdl, cudaStream_t stream) {
+  switch (p.out_mode) {
+    case abed_dev::OUT_NONE: return launch_epi<DT, abed_dev::EPI_NONE>(p, grid, pdl, stream);
+    case abed_dev::OUT_I8_PACKED:
+    case abed_dev::OUT_H_PACKED: return launch_epi<DT, abed_dev::EPI_PACKED>(p, grid, pdl, stream);
+    case abed_dev::OUT_I8_COMPARE:
+    case abed_dev::OUT_H_COMPARE: return launch_epi<DT, abed_dev::EPI_COMPARE>(p, grid, pdl, stream);
+    default: return launch_epi<DT, abed_dev::EPI_NCHW>(p, grid, pdl, stream);
+  }
+}
+
 cudaError_t conv_tc_launch(const ConvTcParams& p, int num_sms, bool pdl, cudaStream_t stream) {
   const int grid = conv_tc_grid(p, num_sms);
-  switch (p.out_mode) {
-    case abed_dev::OUT_NONE: return launch_epi<abed_dev::EPI_NONE>(p, grid, pdl, stream);
-    case abed_dev::OUT_I8_PACKED: return launch_epi<abed_dev::EPI_PACKED>(p, grid, pdl, stream);
-    case abed_dev::OUT_I8_COMPARE: return launch_epi<abed_dev::EPI_COMPARE>(p, grid, pdl, stream);
-    default: return launch_epi<abed_dev::EPI_NCHW>(p, grid, pdl, stream);
+  switch (p.dtype) {
+    case abed_dev::DT_F16: return launch_dt<abed_dev::DT_F16>(p, grid, pdl, stream);
+    case abed_dev::DT_BF16: return launch_dt<abed_dev::DT_BF16>(p, grid, pdl, stream);
+    default: return launch_dt<abed_dev::DT_I8>(p, grid, pdl, stream);
   }
 }
 

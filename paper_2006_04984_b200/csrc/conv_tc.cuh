@@ -31,6 +31,8 @@ constexpr int kStages_host = kStages;
 // dynamic smem cap for the conv kernel: 227 KB minus its static smem (bias, reductions)
 constexpr int kConvDynSmemMax = 232448 - 12288;
 
+enum DType : int { DT_I8 = 0, DT_F16 = 1, DT_BF16 = 2 };
+
 enum OutMode : int {
   OUT_NONE = 0,        // checks only (no activation written)
   OUT_I32_NCHW = 1,    // raw ConvOut, reference layout N x K x P x Q
@@ -38,6 +40,8 @@ enum OutMode : int {
   OUT_F32_NCHW = 3,    // epilog -> f32, reference layout
   OUT_I8_PACKED = 4,   // epilog -> int8 straight into the next layer's strip planes
   OUT_I8_COMPARE = 5,  // epilog -> int8 compared against `out` (duplication check)
+  OUT_H_PACKED = 6,    // float mode: epilog -> fp16/bf16 into the next layer's strip planes
+  OUT_H_COMPARE = 7,   // float mode: epilog -> fp16/bf16 compared against `out`
 };
 
 enum CheckBits : int {
@@ -54,7 +58,8 @@ struct ActGeom {
   int p, q;                // output extents
   int nph_h, nph_w;        // stride phases actually touched by taps
   int n_phase;             // nph_h * nph_w
-  int c16;                 // channel groups of 16 (even, zero padded)
+  int c16;                 // 16-byte channel groups (even, zero padded)
+  int cpg;                 // channels per 16-byte group: 16 (int8) or 8 (fp16/bf16)
   int Hl, Wl;              // M-space rows per image / pixels per row
   int max_shift;           // largest tap pixel shift
   int m_tiles;             // ceil(m_total / 128)
@@ -115,8 +120,15 @@ struct ConvTcParams {
   int64_t fault_key;  // -1 = none
   int fault_bit;
   // ---- diagnostics: per-CTA clock timeline (kTraceSlots int64 per CTA) or nullptr
+  // ---- float mode: fp16 / bf16 operands, f32 accumulators, f64 reductions and
+  // absolute thresholds (checksum.hpp:474-595 float_verify semantics)
+  int dtype;                   // 0 int8, 1 fp16, 2 bf16
+  double tau_fc, tau_fic;
+  double* facc;                // [0] FIC lhs, [1] FIC rhs (in-kernel)
+  double* rhs_ext_f;           // FIC rhs of the pristine input (read: rhs_mode 0, stored: rhs_mode 1)
+  const float* ficwf;          // G as f32 [phase][c16][Hl*Wl][8]
   int64_t* trace;
-  int dbg;  // diagnostics: bit 0 = epilogue skips TMEM reads and processing
+  int dbg;  // diagnostics: bit 0 = epilogue skips its work, bit 3 = no accumulator handshake
 };
 // trace slots: 0 globaltimer at entry, 1 clock at entry, 2 setup done, 3 first
 // stage ready (MMA warp), 4 last MMA commit, 5 epilogue done, 6 units, 7 producer

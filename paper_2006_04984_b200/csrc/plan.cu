@@ -24,7 +24,7 @@ using abed_dev::ConvTcParams;
 
 static inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
-ActGeom make_geom(const abed_layer_shape& s) {
+ActGeom make_geom(const abed_layer_shape& s, int cpg) {
   ActGeom g{};
   g.n = (int)s.n; g.c = (int)s.c; g.h = (int)s.h; g.w = (int)s.w;
   g.k = (int)s.k; g.r = (int)s.r; g.s = (int)s.s;
@@ -33,8 +33,9 @@ ActGeom make_geom(const abed_layer_shape& s) {
   g.nph_h = std::min(g.sh, g.r);
   g.nph_w = std::min(g.sw, g.s);
   g.n_phase = g.nph_h * g.nph_w;
-  g.c16 = (int)ceil_div(g.c, 16);
-  if (g.c16 & 1) g.c16 += 1;  // one MMA consumes 32 channels
+  g.cpg = cpg;
+  g.c16 = (int)ceil_div(g.c, cpg);
+  if (g.c16 & 1) g.c16 += 1;  // one MMA consumes two 16-byte channel groups (32 bytes of K)
   auto extent = [](int P, int H, int R, int st, int pad, int nph) {
     auto zero_lead = [&](int a) { return pad > a ? (int)ceil_div(pad - a, st) : 0; };
     int L = P;
