@@ -35,6 +35,13 @@ RESNET50_3X3 = (
     + [("layer3.0.conv2", 256, 28, 28, 256, 2)] + [(f"layer3.{i}.conv2", 256, 14, 14, 256, 1) for i in range(1, 6)]
     + [("layer4.0.conv2", 512, 14, 14, 512, 2)] + [(f"layer4.{i}.conv2", 512, 7, 7, 512, 1) for i in range(1, 3)]
 )
+# BASELINE configs[2]: VGG-16 conv stack (network_config.hpp:163-184), 3x3 s1 p1,
+# FP16 at batch 64; conv1_1 (C=3) excluded as in SURVEY.md 8(d)
+VGG16_3X3 = [("conv1_2", 64, 224, 64), ("conv2_1", 64, 112, 128), ("conv2_2", 128, 112, 128),
+             ("conv3_1", 128, 56, 256), ("conv3_2", 256, 56, 256), ("conv3_3", 256, 56, 256),
+             ("conv4_1", 256, 28, 512), ("conv4_2", 512, 28, 512), ("conv4_3", 512, 28, 512),
+             ("conv5_1", 512, 14, 512), ("conv5_2", 512, 14, 512), ("conv5_3", 512, 14, 512)]
+VGG_BATCH = 64
 BATCH = 32
 METRIC = "ABED conv TOPS & overhead % vs unprotected/duplication; detection coverage"
 WORKLOAD = "resnet50-3x3-convs-int8-b32 (16 layers, fused bias+ReLU+requant, FIC-protected)"
@@ -207,6 +214,105 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def measure_vgg16_fp16(args, dev, stream, flush, world, dist):
+    """BASELINE configs[2]: the 12 VGG-16 3x3 convs (C >= 64) in FP16 on tensor
+    cores (f32 accumulate), batch 64 per GPU, epilog ReLU -> fp16 packed output,
+    unprotected / FC / FIC (absolute thresholds, float_verify semantics) /
+    full duplication.  Thresholds from the f32-accumulation error bound:
+    tau = (CRS + 32) * 2^-22 * max|x| * sum|f| (FC per pixel; FIC times N*P*Q)."""
+    import torch
+
+    from paper_2006_04984_b200 import abi, api
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(2006_04984)
+    layers = []
+    flops = 0
+    for name, c, hw, k in VGG16_3X3:
+        ls = api.layer_shape(VGG_BATCH, c, hw, hw, k, 3, 3, 1, 1, 1, 1)
+        x = torch.empty(ls.input_dims(), dtype=torch.float32, device=dev).uniform_(-1, 1, generator=gen)
+        f = torch.empty(ls.filter_dims(), dtype=torch.float32, device=dev).uniform_(-1, 1, generator=gen) * 0.05
+        sum_f = float(f.abs().sum())
+        crs = c * 9
+        tau_fc = (crs + k + 32) * 2.0 ** -22 * sum_f
+        tau_fic = (crs + 32) * 2.0 ** -22 * sum_f * ls.p * ls.q * VGG_BATCH
+        L = {"name": name, "ls": ls}
+        L["plans"] = {"unprotected": api.ConvPlanH(ls, f, abi.F16, 0),
+                      "fc": api.ConvPlanH(ls, f, abi.F16, abi.CHECK_FC, tau_fc, tau_fic),
+                      "fic": api.ConvPlanH(ls, f, abi.F16, abi.CHECK_FIC, tau_fc, tau_fic)}
+        L["packed"] = L["plans"]["unprotected"].pack(x)
+        del x
+        L["out"] = L["plans"]["unprotected"].packed_buffer() if False else None
+        # identity consumer of the fp16 output: 8 channels per 16-byte pixel
+        out_elems = VGG_BATCH * ((k + 15) // 16 * 16) * (ls.p + 1) * (ls.q + 1) + (1 << 16)
+        L["out"] = torch.zeros(out_elems * 2, dtype=torch.int8, device=dev)
+        L["ep"] = {kk: pl.epilog_params(1.0, None, True) for kk, pl in L["plans"].items()}
+        flops += 2 * VGG_BATCH * k * ls.p * ls.q * crs
+        layers.append(L)
+    torch.cuda.synchronize()
+
+    def step(variant):
+        for L in layers:
+            if variant == "dup":
+                pl = L["plans"]["unprotected"]
+                pl.run(L["packed"], L["out"], abi.OUT_H_PACKED, ep=L["ep"]["unprotected"])
+                pl.run(L["packed"], L["out"], abi.OUT_H_COMPARE, ep=L["ep"]["unprotected"])
+            else:
+                pl = L["plans"][variant]
+                pl.run(L["packed"], L["out"], abi.OUT_H_PACKED, ep=L["ep"][variant])
+
+    with torch.cuda.stream(stream):
+        for v in ("unprotected", "fc", "fic", "dup"):
+            step(v)
+    torch.cuda.synchronize()
+    graphs = {}
+    for v in ("unprotected", "fc", "fic", "dup"):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            step(v)
+        graphs[v] = g
+    res = {}
+    steps = max(3, min(args.steps, 10))
+    for v in ("unprotected", "fc", "dup", "fic"):
+        for _ in range(max(3, args.warmup)):
+            flush.zero_()
+            graphs[v].replay()
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        ts = []
+        cur = torch.cuda.current_stream()
+        for _ in range(steps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(cur)
+            graphs[v].replay()
+            e1.record(cur)
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        ms = statistics.mean(ts)
+        if dist:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = t.item()
+        res[v] = {"tflops": round(flops * world / (ms * 1e-3) / 1e12, 2), "ms_per_step": round(ms, 4)}
+    fails = 0
+    for L in layers:
+        for v in ("fc", "fic"):
+            pl = L["plans"][v]
+            pl.finalize()
+            fails += sum(o.status for o in pl.outcomes()[:2])
+    u = res["unprotected"]["ms_per_step"]
+    return {"workload": "vgg16-3x3-convs-fp16-b64 (12 layers, C>=64; f32 accumulate, ReLU, fp16 packed out)",
+            "dtype": "fp16 operands, f32 accumulation (tcgen05 kind::f16)", "global_batch": VGG_BATCH * world,
+            "gflop_per_step": round(flops * world / 1e9, 1), "variants": res,
+            "overhead_pct": {"fic_vs_unprotected": round(100 * (res["fic"]["ms_per_step"] / u - 1), 2),
+                             "fc_vs_unprotected": round(100 * (res["fc"]["ms_per_step"] / u - 1), 2),
+                             "duplication_vs_unprotected": round(100 * (res["dup"]["ms_per_step"] / u - 1), 2)},
+            "tau": "absolute, (CRS+32)*2^-22*max|x|*sum|f| (FC per pixel; FIC x N*P*Q)",
+            "fault_free_verdicts_failed": fails,
+            "peak_note": "fp16 dense peak = MEASURED_PEAKS bf16_tflops (or the 1590 fallback)"}
+
+
 # ---------------------------------------------------------------- GPU arm
 def run_ours(args, world, rank, local):
     import ctypes as C
@@ -319,6 +425,10 @@ def run_ours(args, world, rank, local):
         if v == "fic":
             clocks = clk
 
+    vgg = None
+    if not args.skip_vgg:
+        vgg = measure_vgg16_fp16(args, dev, stream, flush, world, dist)
+
     # verdicts of the last FIC run (fault-free => all pass)
     fails = 0
     for L in layers:
@@ -327,24 +437,35 @@ def run_ours(args, world, rank, local):
         fails += sum(o.status for o in pl.outcomes())
 
     # ------------------------------------------------ roofline of the dominant kernel
-    # conv kernel alone per layer (input checksum reused): CUDA events on the launching stream
-    conv_ms = []
-    for L in layers:
-        pl = L["plans"]["fic"]
-        abi.call("abed_conv_plan_set_reuse_input_checksum", pl.handle, 1)
-        ts = []
-        for i in range(max(3, args.steps)):
-            flush.zero_()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            cur = torch.cuda.current_stream()
-            e0.record(cur)
-            pl.run(L["packed"], L["out"], abi.OUT_I8_PACKED, ep=L["ep"]["fic"], stream=C.c_void_p(cur.cuda_stream))
-            e1.record(cur)
-            torch.cuda.synchronize()
-            if i:
-                ts.append(e0.elapsed_time(e1))
-        abi.call("abed_conv_plan_set_reuse_input_checksum", pl.handle, 0)
-        conv_ms.append(statistics.mean(ts))
+    # the FIC conv kernel of each layer (the whole per-layer FIC work: conv, checks,
+    # input checksum, verdict) timed as a captured graph of R back-to-back launches
+    # after an L2 flush, CUDA events on the launching stream; per-launch = total / R
+    R = 10
+
+    def per_layer_ms(variant):
+        out = []
+        for L in layers:
+            pl = L["plans"][variant]
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                for _ in range(R):
+                    pl.run(L["packed"], L["out"], abi.OUT_I8_PACKED, ep=L["ep"][variant])
+            ts = []
+            for i in range(4):
+                flush.zero_()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                cur = torch.cuda.current_stream()
+                e0.record(cur)
+                g.replay()
+                e1.record(cur)
+                torch.cuda.synchronize()
+                if i:
+                    ts.append(e0.elapsed_time(e1) / R)
+            out.append(statistics.mean(ts))
+        return out
+
+    conv_ms = per_layer_ms("fic")
+    unprot_ms = per_layer_ms("unprotected")
     conv_tops = total_ops() / (sum(conv_ms) * 1e-3) / 1e12
     bf16 = peaks.get("bf16_tflops")
     peak = 2.0 * bf16 if bf16 else 2.0 * 1590.0
@@ -356,12 +477,14 @@ def run_ours(args, world, rank, local):
         pass
     roofline = {"bound": "tensor", "achieved": round(conv_tops, 2), "peak": round(peak, 1), "unit": "TFLOP/s",
                 "frac": round(conv_tops / peak, 4), "traffic": ncu.get("traffic_bytes_per_launch"),
-                "kernel": "conv_i8_tc_kernel (FIC epilogue)",
+                "kernel": "conv_i8_tc_kernel<int8, packed out, FIC> (conv + input-checksum warps + output sums + verdict)",
                 "peak_source": ("2 x MEASURED_PEAKS.json bf16_tflops (burst): tcgen05 kind::i8 issues K=32 at the "
                                 "kind::f16 K=16 rate (tools/mma_microbench.cu)" if bf16 else "2 x fallback bf16 1590"),
                 "frac_of_nominal_4500": round(conv_tops / PEAK_INT8_NOMINAL, 4),
                 "conv_share_of_step": round(sum(conv_ms) / res["fic"]["ms"], 3),
-                "per_layer_conv_us": [round(t * 1e3, 2) for t in conv_ms]}
+                "per_layer_conv_us": [round(t * 1e3, 2) for t in conv_ms],
+                "per_layer_unprotected_us": [round(t * 1e3, 2) for t in unprot_ms],
+                "timing": f"per layer: graph of {R} back-to-back launches after an L2 flush, CUDA events / {R}"}
 
     # ------------------------------------------------ e2e through the C ABI with host buffers
     e2e = None
@@ -473,6 +596,7 @@ def run_ours(args, world, rank, local):
         "detection": {"layer": "cfg1 1x64x56x56 K=64 3x3 p1, ones data, scale 0.05, trials %d" % trials, **det},
         "fault_free_verdicts_failed": fails,
         "int8_peak_nominal_tops": PEAK_INT8_NOMINAL,
+        "cfg3_vgg16_fp16": vgg,
     }
     print(json.dumps(line), flush=True)
     if dist:
@@ -489,6 +613,7 @@ def main():
     ap.add_argument("--campaign-trials", type=int, default=1000)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--skip-vgg", action="store_true", help="skip the VGG-16 FP16 block (BASELINE configs[2])")
     args = ap.parse_args()
     world, rank, local = dist_setup()
     if args.impl == "reference":
