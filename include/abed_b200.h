@@ -265,9 +265,14 @@ int abed_pack_input(const abed_conv_plan* plan, const int8_t* input_nchw, int8_t
 int abed_conv_plan_run(abed_conv_plan* plan, const int8_t* packed_input, const abed_epilog_params* params,
                        int32_t out_mode, void* out, const abed_conv_plan* next, int64_t fault_key,
                        int32_t fault_bit, void* stream);
-/* Reduces the run's per-tile records into reference VerifyOutcomes (device side),
- * asynchronously; outcome_dev points to 3 device abed_verify_outcome {FC, FIC, IC}. */
+/* Reduces the last run's per-CTA records into reference VerifyOutcomes (device
+ * side, one small launch), asynchronously; outcome_dev points to 3 device
+ * abed_verify_outcome {FC, FIC, IC}. */
 int abed_conv_plan_finalize(abed_conv_plan* plan, abed_verify_outcome* outcome_dev, void* stream);
+/* One launch that finalizes n plans (e.g. every layer of a network pass):
+ * outcomes_dev[3*i .. 3*i+2] receive plan i's {FC, FIC, IC} VerifyOutcomes. */
+int abed_conv_plan_finalize_many(abed_conv_plan* const* plans, int32_t n, abed_verify_outcome* outcomes_dev,
+                                 void* stream);
 /* reuse = 1: later runs keep the input checksum / FIC right-hand side computed by
  * an earlier run instead of recomputing it from the (possibly corrupted) input;
  * the run is then exactly one kernel launch (fault campaigns, kernel timing). */

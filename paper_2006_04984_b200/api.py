@@ -357,6 +357,26 @@ class ConvPlan:
         return tuple(res)
 
 
+class PlanSet:
+    """Verdicts of a whole pass: one finalize launch for many plans
+    (abed_conv_plan_finalize_many); outcomes()[i] = plan i's (FC, FIC, IC)."""
+
+    def __init__(self, plans):
+        self.plans = list(plans)
+        self._arr = (C.c_void_p * len(self.plans))(*[pl.handle.value for pl in self.plans])
+        self._out = torch.zeros(3 * len(self.plans) * C.sizeof(VerifyOutcome), dtype=torch.uint8, device="cuda")
+
+    def finalize(self, stream=None):
+        call("abed_conv_plan_finalize_many", C.cast(self._arr, C.c_void_p), len(self.plans), _p(self._out),
+             stream or _stream())
+
+    def outcomes(self):
+        host = self._out.cpu().numpy()
+        res = (VerifyOutcome * (3 * len(self.plans)))()
+        C.memmove(res, host.ctypes.data, C.sizeof(res))
+        return [tuple(res[3 * i:3 * i + 3]) for i in range(len(self.plans))]
+
+
 # ------------------------------------------------------------------ float mode on tensor cores
 class ConvPlanH(ConvPlan):
     """Float-mode protected layer (checksum.hpp:471-595 semantics on tcgen05

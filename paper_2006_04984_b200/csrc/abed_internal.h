@@ -71,6 +71,8 @@ int conv_tc_grid(const abed_dev::ConvTcParams& p, int num_sms);
 int mma_pattern_of(const abed_dev::ActGeom& g, int gps);
 // pdl: launch with programmatic stream serialization (griddepcontrol in the kernel)
 cudaError_t conv_tc_launch(const abed_dev::ConvTcParams& p, int num_sms, bool pdl, cudaStream_t stream);
+// reduces the per-CTA verdict records of n plans (one block each)
+cudaError_t verdict_launch(const abed_dev::VerdictJob* jobs, int n, cudaStream_t stream);
 
 }  // namespace abed_host
 
@@ -90,6 +92,7 @@ void plan_init_common(abed_conv_plan* pl, const abed_layer_shape& shape, int che
 void plan_run(abed_conv_plan* pl, const int8_t* packed, const abed_epilog_params* ep, int out_mode, void* out,
               const abed_conv_plan* next, int64_t fault_key, int fault_bit, cudaStream_t st);
 void plan_finalize(abed_conv_plan* pl, abed_verify_outcome* out_dev, cudaStream_t st);
+abed_dev::VerdictJob plan_verdict_job(const abed_conv_plan* pl, abed_verify_outcome* out_dev);
 // ref_kernels.cu
 void dev_gen_input_checksum(const int8_t* x, const abed_layer_shape& s, int32_t* sums, cudaStream_t st);
 void dev_epilog(const int32_t* in, abed_dims4 d, const abed_epilog_params* p, void* out, cudaStream_t st);
@@ -120,6 +123,7 @@ struct abed_conv_plan {
   // right-hand side of an earlier run (fault campaigns: checksums come from
   // the pristine input, faults.hpp:111-115)
   int reuse_input_checksum = 0;
+  int last_rhs_mode = 0;        // rhs_mode of the last run (its verdict reduction needs it)
   // float mode (fp16 / bf16 operands, f32 accumulators; abi_f16.cu)
   int dtype = 0;                 // abed_dev::DT_I8 / DT_F16 / DT_BF16
   double tau_fc = 0.0, tau_fic = 0.0;

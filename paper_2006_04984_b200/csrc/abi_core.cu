@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <vector>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -88,7 +89,7 @@ void plan_init_common(abed_conv_plan* pl, const abed_layer_shape& shape, int che
     cuda_check(cudaMalloc(&pl->d_tile_sem, (size_t)p.m_tiles * 4), "cudaMalloc(tile_sem)");
     cuda_check(cudaMemset(pl->d_tile_sem, 0, (size_t)p.m_tiles * 4), "memset tile_sem");
   }
-  cuda_check(cudaMalloc(&pl->d_cta_rec, (size_t)conv_tc_grid(p, num_sms()) * 4 * 8), "cudaMalloc(cta_rec)");
+  cuda_check(cudaMalloc(&pl->d_cta_rec, (size_t)conv_tc_grid(p, num_sms()) * abed_dev::kCtaRec * 8), "cudaMalloc(cta_rec)");
   cuda_check(cudaMalloc(&pl->d_kacc, 4 * 8), "cudaMalloc(kacc)");
   cuda_check(cudaMemset(pl->d_kacc, 0, 4 * 8), "memset kacc");
   cuda_check(cudaMalloc(&pl->d_outcome, 3 * sizeof(abed_verify_outcome)), "cudaMalloc(outcome)");
@@ -245,16 +246,32 @@ void plan_run(abed_conv_plan* pl, const int8_t* packed, const abed_epilog_params
       }
     }
   }
+  pl->last_rhs_mode = p.rhs_mode;
   cuda_check(conv_tc_launch(p, num_sms(), pl->pdl != 0, st), "conv_i8_tc launch");
 }
 
+abed_dev::VerdictJob plan_verdict_job(const abed_conv_plan* pl, abed_verify_outcome* out_dev) {
+  abed_dev::VerdictJob j{};
+  j.rec = pl->d_cta_rec;
+  j.grid = conv_tc_grid(pl->base, num_sms());
+  j.P = pl->g.p;
+  j.Q = pl->g.q;
+  j.dtype = pl->dtype;
+  j.checks = pl->checks & (ABED_CHECK_FC | ABED_CHECK_FIC);
+  j.rhs_mode = pl->last_rhs_mode;
+  j.rhs_ext = pl->d_acc;
+  j.rhs_ext_f = pl->d_rhs_f;
+  j.tau_fic = pl->tau_fic;
+  j.out = out_dev;
+  return j;
+}
+
 void plan_finalize(abed_conv_plan* pl, abed_verify_outcome* out_dev, cudaStream_t st) {
-  // FC and FIC verdicts were written by the conv kernel's last CTA
-  const int lo = (pl->checks & ABED_CHECK_FC) ? 0 : 1, hi = (pl->checks & ABED_CHECK_FIC) ? 2 : 1;
-  if (hi > lo)
-    cuda_check(cudaMemcpyAsync(out_dev + lo, pl->d_outcome + lo, (hi - lo) * sizeof(abed_verify_outcome),
-                               cudaMemcpyDeviceToDevice, st),
-               "outcome copy");
+  // FC / FIC: reduce the conv kernel's per-CTA records into VerifyOutcomes
+  if (pl->checks & (ABED_CHECK_FC | ABED_CHECK_FIC)) {
+    const abed_dev::VerdictJob j = plan_verdict_job(pl, out_dev);
+    cuda_check(verdict_launch(&j, 1, st), "verdict");
+  }
   if (pl->checks & ABED_CHECK_IC)
     ic_finalize_kernel<<<1, 256, 0, st>>>(pl->d_acc + 4, pl->d_filters, pl->d_ic, pl->shape.k,
                                           pl->shape.c * pl->shape.r * pl->shape.s, out_dev + 2);
@@ -345,6 +362,22 @@ int abed_conv_plan_run(abed_conv_plan* pl, const int8_t* packed, const abed_epil
 }
 int abed_conv_plan_finalize(abed_conv_plan* pl, abed_verify_outcome* outcome_dev, void* stream) {
   return guarded([&] { plan_finalize(pl, outcome_dev, (cudaStream_t)stream); });
+}
+int abed_conv_plan_finalize_many(abed_conv_plan* const* plans, int32_t n, abed_verify_outcome* outcomes_dev,
+                                 void* stream) {
+  return guarded([&] {
+    if (n < 0) throw_invalid("finalize_many: negative plan count");
+    std::vector<abed_dev::VerdictJob> jobs;
+    for (int i = 0; i < n; ++i) {
+      abed_conv_plan* pl = plans[i];
+      if (pl->checks & (ABED_CHECK_FC | ABED_CHECK_FIC)) jobs.push_back(plan_verdict_job(pl, outcomes_dev + 3 * i));
+      if (pl->checks & ABED_CHECK_IC)
+        ic_finalize_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(pl->d_acc + 4, pl->d_filters, pl->d_ic, pl->shape.k,
+                                                               pl->shape.c * pl->shape.r * pl->shape.s,
+                                                               outcomes_dev + 3 * i + 2);
+    }
+    cuda_check(verdict_launch(jobs.data(), (int)jobs.size(), (cudaStream_t)stream), "verdict");
+  });
 }
 int abed_conv_plan_set_reuse_input_checksum(abed_conv_plan* pl, int32_t reuse) {
   return guarded([&] { pl->reuse_input_checksum = reuse ? 1 : 0; });

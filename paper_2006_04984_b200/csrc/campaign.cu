@@ -156,6 +156,13 @@ void ctx_make(GpuTrialCtx& c, const abed_layer_shape& s, const int8_t* x, const 
   c.plan->reuse_input_checksum = 0;
   c.plan->pdl = 0;  // trials patch filter storage right before each run
   plan_run(c.plan, c.packed, &c.ep, kind == ABED_F32 ? ABED_OUT_F32_NCHW : ABED_OUT_I8_NCHW, c.golden, nullptr, -1, 0, st);
+  {
+    // the verdict reduction of the golden run keeps its FIC rhs (pristine input
+    // checksum) for the trials, which reuse it (faults.hpp:111-115)
+    Dev<abed_verify_outcome> scratch(3);
+    plan_finalize(c.plan, scratch.p, st);
+    cuda_check(cudaStreamSynchronize(st), "golden verdict");
+  }
   c.plan->reuse_input_checksum = 1;
   cuda_check(cudaStreamSynchronize(st), "golden run");
 }

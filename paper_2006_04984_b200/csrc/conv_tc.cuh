@@ -105,7 +105,7 @@ struct ConvTcParams {
   int check;
   int64_t* fc_part;            // [n_tiles][m_tiles*128][2] {sum_k, extra} row partials (n_tiles > 1)
   unsigned int* tile_sem;      // [m_tiles] tiles-done counters for the cross-N-tile FC check
-  int64_t* cta_rec;            // [gridDim][4] FC per-CTA {count, first key, lhs, rhs}
+  int64_t* cta_rec;            // [gridDim][kCtaRec] per-CTA {FC count, first key, lhs, rhs, FIC lhs, FIC rhs}
   unsigned long long* kacc;    // [0] FIC lhs, [1] FIC rhs (in-kernel), [2] CTA done ticket
   unsigned long long* rhs_ext;  // FIC rhs of the pristine input: read (rhs_mode 0) or stored (rhs_mode 1)
   int rhs_mode;                // 1: input-checksum warps compute the FIC rhs in this kernel
@@ -135,5 +135,21 @@ struct ConvTcParams {
 // done, 8 first copy issued, 9 summed MMA-warp wait cycles on `full`, 10 summed
 // epilogue-warp wait cycles on the accumulator
 constexpr int kTraceSlots = 16;
+constexpr int kCtaRec = 6;  // int64 slots per CTA in ConvTcParams::cta_rec
+
+// one plan's verdict reduction (verdict_kernel, conv_tc.cu)
+struct VerdictJob {
+  const int64_t* rec;  // [grid][kCtaRec] records of the last run
+  int grid, P, Q, dtype, checks, rhs_mode;
+  unsigned long long* rhs_ext;
+  double* rhs_ext_f;
+  double tau_fic;
+  void* out;           // abed_verify_outcome[3] {FC, FIC, IC}
+};
+constexpr int kMaxVerdictJobs = 32;
+struct VerdictBatch {
+  int n;
+  VerdictJob job[kMaxVerdictJobs];
+};
 
 }  // namespace abed_dev

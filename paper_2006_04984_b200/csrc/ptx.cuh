@@ -255,6 +255,15 @@ __device__ __forceinline__ void pdl_launch_dependents() {
 }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+// grid-scope ticket: atomic add with acquire-release semantics (the release
+// orders this thread's earlier global stores before the increment; the acquire
+// makes every earlier releaser's stores visible to the last arriver)
+__device__ __forceinline__ unsigned long long atom_add_acq_rel_gpu(unsigned long long* addr, unsigned long long v) {
+  unsigned long long old;
+  asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], %2;" : "=l"(old) : "l"(addr), "l"(v) : "memory");
+  return old;
+}
+
 // named barrier over `count` threads (count multiple of 32)
 __device__ __forceinline__ void named_bar(uint32_t id, uint32_t count) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");

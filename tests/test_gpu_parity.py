@@ -221,3 +221,31 @@ def test_fic_convout_detection_exhaustive_on_gpu():
             plan.run(packed, None, abi.OUT_NONE, ep=None, fault_key=idx, fault_bit=bit)
             plan.finalize()
             assert plan.outcomes()[1].status == 1, (idx, bit)
+
+
+def test_finalize_many_matches_per_plan_and_oracle(ora):
+    # one verdict launch for a pass of several layers (abed_conv_plan_finalize_many)
+    shapes = [(2, 64, 12, 12, 64, 3, 3, 1, 1, 1, 1), (1, 32, 9, 9, 256, 3, 3, 2, 2, 1, 1),
+              (2, 16, 8, 8, 24, 1, 1, 1, 1, 0, 0)]
+    plans, inputs = [], []
+    for i, sh in enumerate(shapes):
+        ls = api.layer_shape(*sh)
+        x, f = device_data(ls, 40 + i)
+        pl = api.ConvPlan(ls, f, abi.CHECK_FC | abi.CHECK_FIC)
+        pl.run(pl.pack(x), None, abi.OUT_NONE, ep=None, fault_key=(5 if i == 1 else -1), fault_bit=30)
+        plans.append(pl)
+        inputs.append((ls, x, f))
+    ps = api.PlanSet(plans)
+    ps.finalize()
+    many = ps.outcomes()
+    for pl, got, (ls, x, f) in zip(plans, many, inputs):
+        pl.finalize()
+        one = pl.outcomes()
+        for a, b in zip(got[:2], one[:2]):
+            assert (a.status, a.has_locus, tuple(a.locus), a.lhs, a.rhs) == (b.status, b.has_locus, tuple(b.locus), b.lhs, b.rhs)
+        xh, fh = x.cpu().numpy(), f.cpu().numpy()
+        exp = ora.fic_dot(ora.gen_filter_checksum(fh), ora.gen_input_checksum(xh, ls))
+        assert got[1].rhs == exp
+    assert many[0][0].status == 0 and many[0][1].status == 0
+    assert many[1][0].status == 1 and many[1][1].status == 1  # the injected ConvOut fault
+    assert many[2][0].status == 0 and many[2][1].status == 0
