@@ -42,6 +42,11 @@ VGG16_3X3 = [("conv1_2", 64, 224, 64), ("conv2_1", 64, 112, 128), ("conv2_2", 12
              ("conv4_1", 256, 28, 512), ("conv4_2", 512, 28, 512), ("conv4_3", 512, 28, 512),
              ("conv5_1", 512, 14, 512), ("conv5_2", 512, 14, 512), ("conv5_3", 512, 14, 512)]
 VGG_BATCH = 64
+# BASELINE configs[3]: MobileNetV2 inverted-residual blocks, INT8, batch 32 --
+# a builder-defined table: (C_in, H=W, expansion, C_out, dw stride);
+# each block = pw expand 1x1 (tensor cores) -> dw 3x3 (CUDA cores) -> pw project 1x1,
+# chained through the packed layout
+MBV2_BLOCKS = [(16, 112, 6, 24, 2), (24, 56, 6, 24, 1), (32, 28, 6, 32, 1), (64, 14, 6, 64, 1), (160, 7, 6, 160, 1)]
 BATCH = 32
 METRIC = "ABED conv TOPS & overhead % vs unprotected/duplication; detection coverage"
 WORKLOAD = "resnet50-3x3-convs-int8-b32 (16 layers, fused bias+ReLU+requant, FIC-protected)"
@@ -312,6 +317,106 @@ def measure_vgg16_fp16(args, dev, stream, flush, world, dist):
             "peak_note": "fp16 dense peak = MEASURED_PEAKS bf16_tflops (or the 1590 fallback)"}
 
 
+def measure_mobilenetv2_int8(args, dev, stream, flush, world, dist):
+    """BASELINE configs[3]: 5 MobileNetV2 blocks (15 layers: pointwise on tcgen05,
+    depthwise on CUDA cores), INT8 at batch 32 per GPU, bias + ReLU6-free ReLU +
+    requant, unprotected / FIC (every layer) / duplication, chained through the
+    packed layout (low arithmetic intensity: the checksum-overhead stress case)."""
+    import torch
+
+    from paper_2006_04984_b200 import abi, api
+    layers, ops, seed = [], 0, 900
+    for ci, hw, t, co, st in MBV2_BLOCKS:
+        e = ci * t
+        ho = (hw + 2 - 3) // st + 1
+        shapes = [("pw", api.layer_shape(BATCH, ci, hw, hw, e, 1, 1, 1, 1, 0, 0)),
+                  ("dw", api.layer_shape(BATCH, e, hw, hw, e, 3, 3, st, st, 1, 1)),
+                  ("pw", api.layer_shape(BATCH, e, ho, ho, co, 1, 1, 1, 1, 0, 0))]
+        block = []
+        for kind, ls in shapes:
+            seed += 1
+            if kind == "pw":
+                f = api.fill_random_i8(ls.k * ls.c, api.derive_seed(seed, 2)).view(ls.filter_dims())
+                mk = lambda ch, ls=ls, f=f: api.ConvPlan(ls, f, ch)  # noqa: E731
+                ops += 2 * ls.n * ls.k * ls.p * ls.q * ls.c
+            else:
+                f = api.fill_random_i8(ls.c * 9, api.derive_seed(seed, 2)).view(ls.c, 1, 3, 3)
+                mk = lambda ch, ls=ls, f=f: api.ConvPlanDW(ls, f, ch)  # noqa: E731
+                ops += 2 * ls.n * ls.k * ls.p * ls.q * 9
+            L = {"kind": kind, "ls": ls, "plans": {"unprotected": mk(0), "fic": mk(abi.CHECK_FIC)}}
+            L["ep"] = {v: pl.epilog_params(0.02, None, True) for v, pl in L["plans"].items()}
+            block.append(L)
+        # activation buffers: block input (fresh data), then each layer writes the next one's input
+        x = api.fill_random_i8(shapes[0][1].n * ci * hw * hw, api.derive_seed(seed, 1)).view(shapes[0][1].input_dims())
+        block[0]["in"] = block[0]["plans"]["unprotected"].pack(x)
+        for a, b in zip(block, block[1:]):
+            a["out"] = b["plans"]["unprotected"].packed_buffer()
+            a["next"] = b
+            b["in"] = a["out"]
+        last = block[-1]["ls"]
+        block[-1]["out"] = torch.zeros(last.n * ((last.k + 15) // 16 * 16) * (last.p + 1) * (last.q + 1) + (1 << 16),
+                                       dtype=torch.int8, device=dev)
+        block[-1]["next"] = None
+        layers += block
+    sets = {"fic": api.PlanSet([L["plans"]["fic"] for L in layers])}
+
+    def step(variant):
+        for L in layers:
+            nxt = L["next"]["plans"]["unprotected"] if L["next"] else None
+            if variant == "dup":
+                pl = L["plans"]["unprotected"]
+                pl.run(L["in"], L["out"], abi.OUT_I8_PACKED, ep=L["ep"]["unprotected"], next_plan=nxt)
+                pl.run(L["in"], L["out"], abi.OUT_I8_COMPARE, ep=L["ep"]["unprotected"], next_plan=nxt)
+            else:
+                pl = L["plans"][variant]
+                pl.run(L["in"], L["out"], abi.OUT_I8_PACKED, ep=L["ep"][variant], next_plan=nxt)
+        if variant in sets:
+            sets[variant].finalize()
+
+    with torch.cuda.stream(stream):
+        for v in ("unprotected", "fic", "dup"):
+            step(v)
+    torch.cuda.synchronize()
+    graphs = {}
+    for v in ("unprotected", "fic", "dup"):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            step(v)
+        graphs[v] = g
+    res = {}
+    for v in ("unprotected", "dup", "fic"):
+        for _ in range(max(3, args.warmup)):
+            flush.zero_()
+            graphs[v].replay()
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        ts = []
+        cur = torch.cuda.current_stream()
+        for _ in range(max(3, args.steps)):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(cur)
+            graphs[v].replay()
+            e1.record(cur)
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        ms = statistics.mean(ts)
+        if dist:
+            tt = torch.tensor([ms], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ms = tt.item()
+        res[v] = {"tops": round(ops * world / (ms * 1e-3) / 1e12, 2), "ms_per_step": round(ms, 4)}
+    fails = sum(oc[1].status for oc in sets["fic"].outcomes())
+    u = res["unprotected"]["ms_per_step"]
+    return {"workload": "mobilenetv2-5-blocks-int8-b32 (15 layers: pw 1x1 tcgen05 + dw 3x3 CUDA cores, chained)",
+            "blocks": [list(b) for b in MBV2_BLOCKS], "global_batch": BATCH * world,
+            "gop_per_step": round(ops * world / 1e9, 2), "variants": res,
+            "overhead_pct": {"fic_vs_unprotected": round(100 * (res["fic"]["ms_per_step"] / u - 1), 2),
+                             "duplication_vs_unprotected": round(100 * (res["dup"]["ms_per_step"] / u - 1), 2)},
+            "fault_free_verdicts_failed": fails}
+
+
 # ---------------------------------------------------------------- GPU arm
 def run_ours(args, world, rank, local):
     import ctypes as C
@@ -431,6 +536,9 @@ def run_ours(args, world, rank, local):
     vgg = None
     if not args.skip_vgg:
         vgg = measure_vgg16_fp16(args, dev, stream, flush, world, dist)
+    mbv2 = None
+    if not args.skip_mbv2:
+        mbv2 = measure_mobilenetv2_int8(args, dev, stream, flush, world, dist)
 
     # verdicts of the last FC / FIC passes (fault-free => all pass)
     fails = sum(o.status for oc in sets["fic"].outcomes() for o in oc[:2]) + \
@@ -597,6 +705,7 @@ def run_ours(args, world, rank, local):
         "fault_free_verdicts_failed": fails,
         "int8_peak_nominal_tops": PEAK_INT8_NOMINAL,
         "cfg3_vgg16_fp16": vgg,
+        "cfg4_mobilenetv2_int8": mbv2,
     }
     print(json.dumps(line), flush=True)
     if dist:
@@ -614,6 +723,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--skip-vgg", action="store_true", help="skip the VGG-16 FP16 block (BASELINE configs[2])")
+    ap.add_argument("--skip-mbv2", action="store_true", help="skip the MobileNetV2 INT8 block (BASELINE configs[3])")
     args = ap.parse_args()
     world, rank, local = dist_setup()
     if args.impl == "reference":

@@ -279,6 +279,14 @@ int abed_conv_plan_finalize_many(abed_conv_plan* const* plans, int32_t n, abed_v
 int abed_conv_plan_set_reuse_input_checksum(abed_conv_plan* plan, int32_t reuse);
 /* duplication baseline: mismatch count of the last OUT_I8_COMPARE run (synchronous) */
 int abed_conv_plan_compare_count(abed_conv_plan* plan, int64_t* count);
+/* ---- depthwise conv (MobileNetV2; no reference counterpart).
+ * shape.k == shape.c, filters C x 1 x R x S int8 (device).  checks: 0 or
+ * ABED_CHECK_FIC (the FIC identity holds by linearity with the depthwise filter
+ * as its own filter checksum).  The plan uses the strip-plane layout and the
+ * plan API (abed_pack_input, abed_conv_plan_run with ABED_OUT_I8_* modes,
+ * next-layer packed output in both directions, finalize). */
+int abed_conv_plan_create_dw(const abed_layer_shape* shape, const int8_t* filters, int32_t checks,
+                             abed_conv_plan** plan);
 /* ---- float mode on tensor cores (fp16 / bf16 operands, f32 accumulation).
  * The reference's float mode (checksum.hpp:471-595: f32 operands, f64 checksum
  * reductions, Pass iff |lhs - rhs| <= tau) on tcgen05 kind::f16: filters (device

@@ -118,6 +118,33 @@ int ora_conv_f32(const float* x, const float* f, const abed_layer_shape* ls, flo
   ORA_CONV_BODY(float, XIDX, FIDX, o[p * Q + q] = fmaf(xv, fv, o[p * Q + q]))
   return ORA_OK;
 }
+/* Depthwise conv (no reference counterpart -- parity unpinned):
+ * conv_reference (convolution.hpp:78-111) with one filter per channel,
+ * out[n,c,p,q] = sum_{r,s} x[n,c,..] f[c,0,r,s], halo skipped, int32. */
+int ora_dwconv_i8(const int8_t* x, const int8_t* f, const abed_layer_shape* ls, int32_t* out) {
+  const int64_t P = ls->p, Q = ls->q, H = ls->h, W = ls->w, C = ls->c, R = ls->r, S = ls->s;
+  if (ls->k != ls->c) return ORA_INVALID;
+  for (int64_t n = 0; n < ls->n; ++n)
+    for (int64_t c = 0; c < C; ++c) {
+      int32_t* o = out + (n * C + c) * P * Q;
+      for (int64_t i = 0; i < P * Q; ++i) o[i] = 0;
+      for (int64_t r = 0; r < R; ++r)
+        for (int64_t s = 0; s < S; ++s) {
+          const int32_t fv = f[(c * R + r) * S + s];
+          for (int64_t p = 0; p < P; ++p) {
+            const int64_t hi = p * ls->stride_h - ls->pad_h + r;
+            if (hi < 0 || hi >= H) continue;
+            for (int64_t q = 0; q < Q; ++q) {
+              const int64_t wi = q * ls->stride_w - ls->pad_w + s;
+              if (wi < 0 || wi >= W) continue;
+              o[p * Q + q] += (int32_t)x[((n * C + c) * H + hi) * W + wi] * fv;
+            }
+          }
+        }
+    }
+  return ORA_OK;
+}
+
 /* Float mode on tensor cores (no reference counterpart -- parity unpinned, see
  * DESIGN.md): conv_reference (convolution.hpp:78-111) with f64 accumulation, the
  * exact-as-possible value the fp16/bf16 tensor-core conv approximates (x, f are

@@ -50,6 +50,7 @@ int ora_conv_i8(const int8_t* x, const int8_t* f, const abed_layer_shape* ls, in
 int ora_conv_i8_w32_i64(const int8_t* x, const int32_t* f, const abed_layer_shape* ls, int64_t* out);
 int ora_conv_x32_i8_i64(const int32_t* x, const int8_t* f, const abed_layer_shape* ls, int64_t* out);
 int ora_conv_f32(const float* x, const float* f, const abed_layer_shape* ls, float* out);
+int ora_dwconv_i8(const int8_t* x, const int8_t* f, const abed_layer_shape* ls, int32_t* out);
 int ora_conv_f64(const float* x, const float* f, const abed_layer_shape* ls, double* out);
 /* convolution.hpp:353-387 */
 int ora_epilog(const int32_t* convout, abed_dims4 d, float scale, const float* bias, int64_t bias_len,

@@ -167,6 +167,14 @@ class Oracle:
         self._chk(fn(ptr(np.ascontiguousarray(x, np.float32)), ptr(np.ascontiguousarray(f, np.float32)), C.byref(ls), ptr(out)))
         return out
 
+    def dwconv_i8(self, x, f, ls):
+        """Depthwise conv_reference (one filter per channel), int32."""
+        out = np.empty(ls.output_dims(), np.int32)
+        fn = self._f("dwconv_i8")
+        fn.argtypes = [P, P, C.POINTER(LayerShape), P]
+        self._chk(fn(ptr(np.ascontiguousarray(x, np.int8)), ptr(np.ascontiguousarray(f, np.int8)), C.byref(ls), ptr(out)))
+        return out
+
     def conv_f64(self, x, f, ls):
         """conv_reference with f64 accumulation (float mode on tensor cores: the
         value an fp16/bf16 x f32-accumulate conv approximates)."""

@@ -357,6 +357,20 @@ class ConvPlan:
         return tuple(res)
 
 
+class ConvPlanDW(ConvPlan):
+    """Depthwise layer (one filter per channel, K == C, filters C x 1 x R x S int8)
+    on the strip-plane layout; checks 0 or abi.CHECK_FIC."""
+
+    def __init__(self, ls: LayerShape, filters: torch.Tensor, checks: int = 0):
+        self.ls = ls
+        self.checks = checks
+        self.handle = C.c_void_p()
+        call("abed_conv_plan_create_dw", C.byref(ls), _p(filters), checks, C.byref(self.handle))
+        self.info = abi.PlanInfo()
+        call("abed_conv_plan_info", self.handle, C.byref(self.info))
+        self._outcomes = torch.zeros(3 * C.sizeof(VerifyOutcome), dtype=torch.uint8, device="cuda")
+
+
 class PlanSet:
     """Verdicts of a whole pass: one finalize launch for many plans
     (abed_conv_plan_finalize_many); outcomes()[i] = plan i's (FC, FIC, IC)."""

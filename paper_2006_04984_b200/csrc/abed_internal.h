@@ -84,6 +84,11 @@ void require_device();
 int grid_for(int64_t n, int threads);
 void validate_shape(const abed_layer_shape& s);
 abed_conv_plan* plan_create(const abed_layer_shape& shape, const int8_t* filters, int checks, int force_bn);
+// dwconv.cu: depthwise plan (shares abed_conv_plan; dispatched by plan_run)
+abed_conv_plan* plan_create_dw(const abed_layer_shape& shape, const int8_t* filters, int checks);
+void plan_run_dw(abed_conv_plan* pl, const int8_t* packed, const abed_epilog_params* ep, int out_mode, void* out,
+                 const abed_conv_plan* next, int64_t fault_key, int fault_bit, cudaStream_t st);
+int dw_grid();
 // abi_f16.cu: float-mode plan (fp16 / bf16 operands from f32 filters)
 abed_conv_plan* plan_create_h(const abed_layer_shape& shape, const float* filters, int elem_kind, int checks,
                               double tau_fc, double tau_fic, int force_bn);
@@ -131,6 +136,9 @@ struct abed_conv_plan {
   double* d_rhs_f = nullptr;     // FIC rhs of the pristine input (f64)
   float* d_ficwf = nullptr;      // G as f32 [phase][c16][Hl*Wl][8]
   double* d_fsum_f = nullptr;    // filter checksum (c,r,s) of the rounded filters, f64
+  // depthwise plan (dwconv.cu): one filter per channel, CUDA-core kernel, FIC only
+  int dw = 0;
+  uint32_t* d_dwf = nullptr;     // packed depthwise filters [c16][16][quads]
   // programmatic dependent launch of the conv kernel (its prologue overlaps the
   // previous kernel); off for fault campaigns, which patch filter storage
   // right before a run

@@ -152,6 +152,10 @@ abed_conv_plan* plan_create(const abed_layer_shape& shape, const int8_t* filters
 
 void plan_run(abed_conv_plan* pl, const int8_t* packed, const abed_epilog_params* ep, int out_mode, void* out,
               const abed_conv_plan* next, int64_t fault_key, int fault_bit, cudaStream_t st) {
+  if (pl->dw) {
+    plan_run_dw(pl, packed, ep, out_mode, out, next, fault_key, fault_bit, st);
+    return;
+  }
   ConvTcParams p = pl->base;
   p.act = packed;
   p.wpk = pl->d_wpk;
@@ -253,7 +257,7 @@ void plan_run(abed_conv_plan* pl, const int8_t* packed, const abed_epilog_params
 abed_dev::VerdictJob plan_verdict_job(const abed_conv_plan* pl, abed_verify_outcome* out_dev) {
   abed_dev::VerdictJob j{};
   j.rec = pl->d_cta_rec;
-  j.grid = conv_tc_grid(pl->base, num_sms());
+  j.grid = pl->dw ? dw_grid() : conv_tc_grid(pl->base, num_sms());
   j.P = pl->g.p;
   j.Q = pl->g.q;
   j.dtype = pl->dtype;
@@ -330,7 +334,7 @@ int abed_conv_plan_destroy(abed_conv_plan* pl) {
   cudaFree(pl->d_wpk); cudaFree(pl->d_filters); cudaFree(pl->d_fsum); cudaFree(pl->d_ic);
   cudaFree(pl->d_bsum); cudaFree(pl->d_ficw); cudaFree(pl->d_ficw8); cudaFree(pl->d_fc_part); cudaFree(pl->d_tile_sem);
   cudaFree(pl->d_cta_rec); cudaFree(pl->d_kacc); cudaFree(pl->d_outcome);
-  cudaFree(pl->d_facc); cudaFree(pl->d_rhs_f); cudaFree(pl->d_ficwf); cudaFree(pl->d_fsum_f);
+  cudaFree(pl->d_facc); cudaFree(pl->d_rhs_f); cudaFree(pl->d_ficwf); cudaFree(pl->d_fsum_f); cudaFree(pl->d_dwf);
   cudaFree(pl->d_acc); cudaFree(pl->d_zero_bias);
   delete pl;
   return ABED_OK;

@@ -1,0 +1,109 @@
+"""Depthwise INT8 conv (MobileNetV2, BASELINE configs[3]) against the oracle.
+
+No reference counterpart (parity unpinned): the oracle restates
+conv_reference (convolution.hpp:78-111) with one filter per channel; the FIC
+identity is the reference's by linearity, so its rhs is checked against the
+reference-pinned gen_input_checksum / fic_dot restatements with the depthwise
+filter as the filter checksum.  All integer: bit-exact.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle.pyoracle import Oracle
+from paper_2006_04984_b200 import abi, api
+
+pytestmark = pytest.mark.gpu
+
+DW_SHAPES = [
+    # n, c, h, w, k(=c), r, s, sh, sw, ph, pw
+    (2, 144, 14, 14, 144, 3, 3, 1, 1, 1, 1),
+    (2, 96, 15, 13, 96, 3, 3, 2, 2, 1, 1),
+    (1, 40, 9, 9, 40, 3, 3, 1, 1, 1, 1),   # ragged channel group
+    (1, 32, 11, 11, 32, 5, 5, 1, 1, 2, 2),
+]
+
+
+@pytest.fixture(scope="module")
+def ora():
+    return Oracle("ora")
+
+
+def data(ls, seed):
+    x = api.fill_random_i8(ls.n * ls.c * ls.h * ls.w, api.derive_seed(seed, 1)).view(ls.input_dims())
+    f = api.fill_random_i8(ls.c * ls.r * ls.s, api.derive_seed(seed, 2)).view(ls.c, 1, ls.r, ls.s)
+    return x, f
+
+
+@pytest.mark.parametrize("shape", DW_SHAPES)
+def test_dwconv_bit_exact(ora, shape):
+    ls = api.layer_shape(*shape)
+    x, f = data(ls, 77)
+    plan = api.ConvPlanDW(ls, f, abi.CHECK_FIC)
+    packed = plan.pack(x)
+    out = torch.empty(ls.output_dims(), dtype=torch.int32, device="cuda")
+    plan.run(packed, out, abi.OUT_I32_NCHW, ep=None)
+    xh, fh = x.cpu().numpy(), f.cpu().numpy()
+    want = ora.dwconv_i8(xh, fh, ls)
+    assert np.array_equal(out.cpu().numpy(), want)
+    plan.finalize()
+    fic = plan.outcomes()[1]
+    # fic_dot(f as the filter checksum, gen_input_checksum) == sum of outputs
+    rhs = ora.fic_dot(fh.reshape(-1).astype(np.int32), ora.gen_input_checksum(xh, ls))
+    assert fic.status == 0 and fic.lhs == fic.rhs == rhs == int(want.astype(np.int64).sum())
+    # epilog output
+    bias = np.linspace(-2, 2, ls.k).astype(np.float32)
+    y = torch.empty(ls.output_dims(), dtype=torch.int8, device="cuda")
+    plan.run(packed, y, abi.OUT_I8_NCHW, scale=0.01, bias=bias, relu=True)
+    assert np.array_equal(y.cpu().numpy(), ora.epilog(want, 0.01, bias))
+
+
+def test_dw_fault_detection(ora):
+    ls = api.layer_shape(2, 64, 10, 10, 64, 3, 3, 1, 1, 1, 1)
+    x, f = data(ls, 5)
+    plan = api.ConvPlanDW(ls, f, abi.CHECK_FIC)
+    packed = plan.pack(x)
+    for key, bit in [(0, 0), (ls.nkpq() // 2, 7), (ls.nkpq() - 1, 31)]:
+        plan.run(packed, None, abi.OUT_NONE, ep=None, fault_key=key, fault_bit=bit)
+        plan.finalize()
+        assert plan.outcomes()[1].status == 1, (key, bit)
+    plan.run(packed, None, abi.OUT_NONE, ep=None)
+    plan.finalize()
+    assert plan.outcomes()[1].status == 0
+    with pytest.raises(abi.AbedError):
+        api.ConvPlanDW(ls, f, abi.CHECK_FC)
+
+
+def test_mobilenet_block_chained(ora):
+    """pw expand (tensor cores) -> dw 3x3 (CUDA cores) -> pw project, every
+    layer FIC-protected, activations handed over in the packed layout."""
+    n, c, hw, t = 2, 24, 14, 6
+    e = c * t
+    pw1 = api.layer_shape(n, c, hw, hw, e, 1, 1, 1, 1, 0, 0)
+    dw = api.layer_shape(n, e, hw, hw, e, 3, 3, 1, 1, 1, 1)
+    pw2 = api.layer_shape(n, e, hw, hw, c, 1, 1, 1, 1, 0, 0)
+    x, _ = data(pw1, 1)
+    f1 = api.fill_random_i8(e * c, api.derive_seed(2, 2)).view(pw1.filter_dims())
+    _, fd = data(dw, 3)
+    f2 = api.fill_random_i8(c * e, api.derive_seed(4, 2)).view(pw2.filter_dims())
+    p1 = api.ConvPlan(pw1, f1, abi.CHECK_FIC)
+    pd = api.ConvPlanDW(dw, fd, abi.CHECK_FIC)
+    p2 = api.ConvPlan(pw2, f2, abi.CHECK_FIC)
+    b1 = np.linspace(-1, 1, e).astype(np.float32)
+    bd = np.linspace(-1, 1, e).astype(np.float32)
+    b2 = np.linspace(-1, 1, c).astype(np.float32)
+    a1 = p1.pack(x)
+    a2 = pd.packed_buffer()
+    a3 = p2.packed_buffer()
+    p1.run(a1, a2, abi.OUT_I8_PACKED, scale=0.02, bias=b1, relu=True, next_plan=pd)
+    pd.run(a2, a3, abi.OUT_I8_PACKED, scale=0.03, bias=bd, relu=True, next_plan=p2)
+    y = torch.empty(pw2.output_dims(), dtype=torch.int8, device="cuda")
+    p2.run(a3, y, abi.OUT_I8_NCHW, scale=0.02, bias=b2, relu=False)
+    ps = api.PlanSet([p1, pd, p2])
+    ps.finalize()
+    assert all(oc[1].status == 0 for oc in ps.outcomes())
+    xh = x.cpu().numpy()
+    h1 = ora.epilog(ora.conv_i8(xh, f1.cpu().numpy(), pw1), 0.02, b1)
+    h2 = ora.epilog(ora.dwconv_i8(h1, fd.cpu().numpy(), dw), 0.03, bd)
+    want = ora.epilog(ora.conv_i8(h2, f2.cpu().numpy(), pw2), 0.02, b2, relu=False)
+    assert np.array_equal(y.cpu().numpy(), want)
