@@ -426,6 +426,11 @@ def run_ours(args, world, rank, local):
     from paper_2006_04984_b200 import abi, api
 
     torch.cuda.set_device(local)
+    # per-GPU batch: BASELINE configs[1] (32 per GPU, weak scaling) by default;
+    # --global-batch B shards a fixed batch over the ranks (configs[4]: 1024, strong)
+    rb = args.global_batch // world if args.global_batch else BATCH
+    if args.global_batch and args.global_batch % world:
+        raise SystemExit("--global-batch must be divisible by the number of GPUs")
     abi.check(abi.load().abed_device_check())
     dist = None
     if world > 1:
@@ -438,7 +443,7 @@ def run_ours(args, world, rank, local):
     # ------------------------------------------------ layers, data, plans
     layers = []
     for li, (name, c, h, w, k, st) in enumerate(RESNET50_3X3):
-        ls = api.layer_shape(BATCH, c, h, w, k, 3, 3, st, st, 1, 1)
+        ls = api.layer_shape(rb, c, h, w, k, 3, 3, st, st, 1, 1)
         seed = 1000 * (rank + 1) + li  # each rank owns its own batch shard
         x = api.fill_random_i8(ls.n * ls.c * ls.h * ls.w, api.derive_seed(seed, 1)).view(ls.input_dims())
         f = api.fill_random_i8(ls.k * ls.c * ls.r * ls.s, api.derive_seed(seed, 2)).view(ls.filter_dims())
@@ -524,7 +529,7 @@ def run_ours(args, world, rank, local):
             ms = t.item()
         return ms, clocks
 
-    ops_step = total_ops() * world
+    ops_step = total_ops(rb) * world
     res = {}
     sampler = ClockSampler(local)
     for v in ("unprotected", "fc", "dup", "fic"):
@@ -574,7 +579,7 @@ def run_ours(args, world, rank, local):
 
     conv_ms = per_layer_ms("fic")
     unprot_ms = per_layer_ms("unprotected")
-    conv_tops = total_ops() / (sum(conv_ms) * 1e-3) / 1e12
+    conv_tops = total_ops(rb) / (sum(conv_ms) * 1e-3) / 1e12
     bf16 = peaks.get("bf16_tflops")
     peak = 2.0 * bf16 if bf16 else 2.0 * 1590.0
     ncu = {}
@@ -683,11 +688,12 @@ def run_ours(args, world, rank, local):
         "warmup": args.warmup,
         "ms_per_step": round(fic["ms"], 4),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong" if args.global_batch else "weak",
         "vs_baseline": None,
         "dtype": "int8",
         "data": "synthetic: SplitMix64 int8 activations/filters generated on device; bias linspace(-2,2), scale 0.05",
-        "config": {"workload": WORKLOAD, "global_batch": BATCH * world, "per_gpu_batch": BATCH, "layers": 16,
+        "config": {"workload": WORKLOAD if not args.global_batch else WORKLOAD.replace("-b32", f"-b{rb * world}"),
+                   "global_batch": rb * world, "per_gpu_batch": rb, "layers": 16,
                    "scheme": "FIC-FR in one kernel per layer (input-checksum warps re-read the stored input: x.G with dp4a; epilogue output sums; per-CTA verdict records) + one verdict launch per pass for all 16 VerifyOutcomes",
                    "parallelism": f"dp{world} (batch shards, NCCL error-count all-reduce)",
                    "l2": "flushed (512 MiB memset) before every timed step", "timing": "CUDA graph replay, CUDA events"},
@@ -724,6 +730,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--skip-vgg", action="store_true", help="skip the VGG-16 FP16 block (BASELINE configs[2])")
     ap.add_argument("--skip-mbv2", action="store_true", help="skip the MobileNetV2 INT8 block (BASELINE configs[3])")
+    ap.add_argument("--global-batch", type=int, default=0,
+                    help="shard this fixed ResNet-50 batch over the GPUs (BASELINE configs[4]: 1024); default 32 per GPU")
     args = ap.parse_args()
     world, rank, local = dist_setup()
     if args.impl == "reference":

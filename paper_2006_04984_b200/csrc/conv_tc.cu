@@ -781,6 +781,17 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
     const int nch = p.block_n >> 4;  // 16-column chunks of real output channels
     const int h0 = (nch + 1) >> 1;
     const int c_lo = half ? h0 : 0, c_hi = half ? nch : h0;
+    // per-unit coordinates without integer division: exact float-reciprocal
+    // quotients (every operand < 2^24), shifts for the 1/2-strided consumer
+    const float rcp_hlwl = 1.0f / static_cast<float>(HlWl), rcp_wl = 1.0f / static_cast<float>(p.Wl);
+    auto fdiv = [](uint32_t a, uint32_t d, float rcp) {
+      uint32_t q = __float2uint_rz(__fmul_rz(__uint2float_rz(a), rcp));
+      if (q * d > a) --q;
+      else if ((q + 1u) * d <= a) ++q;
+      return q;
+    };
+    const bool o_pow2 = (p.o_sh == 1 || p.o_sh == 2) && (p.o_sw == 1 || p.o_sw == 2);
+    const int o_shh = p.o_sh == 2 ? 1 : 0, o_shw = p.o_sw == 2 ? 1 : 0;
     for (int u = 0; u < n_units; ++u) {
       int mt, nt;
       decode_tile(p, u, mt, nt);
@@ -788,9 +799,9 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
       uint32_t n_img = 0, pp = 0, qq = 0;
       bool valid = m < static_cast<uint64_t>(p.m_total);
       if (valid) {
-        n_img = m / HlWl;
+        n_img = fdiv(m, HlWl, rcp_hlwl);
         const uint32_t rem = m - n_img * HlWl;
-        pp = rem / p.Wl;
+        pp = fdiv(rem, static_cast<uint32_t>(p.Wl), rcp_wl);
         qq = rem - pp * p.Wl;
         valid = pp < static_cast<uint32_t>(p.P) && qq < static_cast<uint32_t>(p.Q);
       }
@@ -799,8 +810,19 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
       e.fault_row = valid && p.fault_key >= 0 && n_img == fk_n && (key - static_cast<int64_t>(n_img) * e.PQ) == fk_pq;
       if (EPI == EPI_PACKED || EPI == EPI_COMPARE) {
         const int hh = pp + p.o_ph, ww = qq + p.o_pw;
-        const int a_ph = hh % p.o_sh, b_ph = ww % p.o_sw;
-        const int64_t t = (static_cast<int64_t>(n_img) * p.o_Hl + hh / p.o_sh) * p.o_Wl + ww / p.o_sw;
+        int a_ph, b_ph, hq, wq;
+        if (o_pow2) {
+          a_ph = hh & o_shh;
+          b_ph = ww & o_shw;
+          hq = hh >> o_shh;
+          wq = ww >> o_shw;
+        } else {
+          a_ph = hh % p.o_sh;
+          b_ph = ww % p.o_sw;
+          hq = hh / p.o_sh;
+          wq = ww / p.o_sw;
+        }
+        const int64_t t = (static_cast<int64_t>(n_img) * p.o_Hl + hq) * p.o_Wl + wq;
         e.pk_row = static_cast<int8_t*>(p.out) +
                    (static_cast<int64_t>(a_ph * p.o_nph_w + b_ph) * p.o_c16 * p.o_plane_len + t) * 16;
       } else if (EPI == EPI_NCHW) {

@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--only", default="")
     ap.add_argument("--dbg", type=int, default=0, help="debug flags (bit 0: epilogue skips its work)")
     ap.add_argument("--fresh-rhs", action="store_true", help="FIC: recompute the input checksum every run")
+    ap.add_argument("--batch", type=int, default=BATCH)
     a = ap.parse_args()
     checks = {"unprotected": 0, "fc": abi.CHECK_FC, "fic": abi.CHECK_FIC}[a.variant]
     only = set(a.only.split(",")) if a.only else None
@@ -35,7 +36,7 @@ def main():
     for li, (name, c, h, w, k, st) in enumerate(RESNET50_3X3):
         if only and name not in only:
             continue
-        ls = api.layer_shape(BATCH, c, h, w, k, 3, 3, st, st, 1, 1)
+        ls = api.layer_shape(a.batch, c, h, w, k, 3, 3, st, st, 1, 1)
         x = api.fill_random_i8(ls.n * ls.c * ls.h * ls.w, api.derive_seed(li, 1)).view(ls.input_dims())
         f = api.fill_random_i8(ls.k * ls.c * ls.r * ls.s, api.derive_seed(li, 2)).view(ls.filter_dims())
         pl = api.ConvPlan(ls, f, checks)
