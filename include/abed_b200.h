@@ -269,6 +269,13 @@ int abed_conv_plan_run(abed_conv_plan* plan, const int8_t* packed_input, const a
  * side, one small launch), asynchronously; outcome_dev points to 3 device
  * abed_verify_outcome {FC, FIC, IC}. */
 int abed_conv_plan_finalize(abed_conv_plan* plan, abed_verify_outcome* outcome_dev, void* stream);
+/* FIC-AF (fused_conv_epilog's next-layer input-checksum tap, checksum.hpp:605-631):
+ * on = 1 marks that this int8 FIC plan's right-hand side is produced by the
+ * previous layer's epilogue, i.e. that layer runs with out_mode
+ * ABED_OUT_I8_PACKED and next = this plan; its stored int8 outputs are dotted
+ * with this plan's position weights as they are written.  The FR input pass is
+ * then skipped; finalize consumes (and resets) the accumulated value. */
+int abed_conv_plan_set_af_input(abed_conv_plan* plan, int32_t on);
 /* One launch that finalizes n plans (e.g. every layer of a network pass):
  * outcomes_dev[3*i .. 3*i+2] receive plan i's {FC, FIC, IC} VerifyOutcomes. */
 int abed_conv_plan_finalize_many(abed_conv_plan* const* plans, int32_t n, abed_verify_outcome* outcomes_dev,

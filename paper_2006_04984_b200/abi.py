@@ -177,6 +177,7 @@ SIGNATURES = {
     "abed_conv_plan_set_tau": (C.c_int, [P, C.c_double, C.c_double]),
     "abed_conv_plan_finalize_many": (C.c_int, [P, i32, P, P]),
     "abed_conv_plan_create_dw": (C.c_int, [SHP, P, i32, C.POINTER(P)]),
+    "abed_conv_plan_set_af_input": (C.c_int, [P, i32]),
     "abed_conv_plan_set_reuse_input_checksum": (C.c_int, [P, i32]),
 }
 

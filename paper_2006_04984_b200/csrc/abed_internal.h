@@ -129,6 +129,10 @@ struct abed_conv_plan {
   // the pristine input, faults.hpp:111-115)
   int reuse_input_checksum = 0;
   int last_rhs_mode = 0;        // rhs_mode of the last run (its verdict reduction needs it)
+  // FIC-AF: this layer's FIC rhs is accumulated by the previous layer's epilogue
+  // (which is run with next = this plan); the verdict consumes and resets it
+  int af_input = 0;
+  unsigned long long* d_af_acc = nullptr;
   // float mode (fp16 / bf16 operands, f32 accumulators; abi_f16.cu)
   int dtype = 0;                 // abed_dev::DT_I8 / DT_F16 / DT_BF16
   double tau_fc = 0.0, tau_fic = 0.0;

@@ -98,6 +98,8 @@ void plan_init_common(abed_conv_plan* pl, const abed_layer_shape& shape, int che
   cuda_check(cudaMemset(pl->d_acc, 0, (4 + shape.k) * 8), "memset acc");
   cuda_check(cudaMalloc(&pl->d_zero_bias, shape.k * 4), "cudaMalloc(bias)");
   cuda_check(cudaMemset(pl->d_zero_bias, 0, shape.k * 4), "memset bias");
+  cuda_check(cudaMalloc(&pl->d_af_acc, 8), "cudaMalloc(af_acc)");
+  cuda_check(cudaMemset(pl->d_af_acc, 0, 8), "memset af_acc");
 }
 
 abed_conv_plan* plan_create(const abed_layer_shape& shape, const int8_t* filters, int checks, int force_bn) {
@@ -193,6 +195,12 @@ void plan_run(abed_conv_plan* pl, const int8_t* packed, const abed_epilog_params
         throw_invalid("conv plan: next layer input does not match this layer's output");
       p.o_plane_len = o.plane_len; p.o_Hl = o.Hl; p.o_Wl = o.Wl; p.o_ph = o.ph; p.o_pw = o.pw;
       p.o_sh = o.sh; p.o_sw = o.sw; p.o_nph_w = o.nph_w; p.o_c16 = o.c16;
+      if (out_mode == ABED_OUT_I8_PACKED && next->af_input && (next->checks & ABED_CHECK_FIC)) {
+        // FIC-AF: accumulate the consumer's rhs from the values this epilogue stores
+        p.af_ficw8 = next->d_ficw8;
+        p.af_acc = next->d_af_acc;
+        p.af_HlWl = (int64_t)o.Hl * o.Wl;
+      }
     } else {
       // identity consumer geometry: 1x1, stride 1, pad 0
       abed_layer_shape s1{pl->shape.n, pl->shape.k, pl->shape.p, pl->shape.q, 1, 1, 1, 1, 1, 0, 0, pl->shape.p, pl->shape.q};
@@ -215,7 +223,9 @@ void plan_run(abed_conv_plan* pl, const int8_t* packed, const abed_epilog_params
   if (pl->checks & ABED_CHECK_IC) cuda_check(cudaMemsetAsync(pl->d_acc + 4, 0, pl->shape.k * 8, st), "memset ic");
   if (out_mode == ABED_OUT_I8_COMPARE) cuda_check(cudaMemsetAsync(pl->d_acc + 1, 0, 8, st), "memset cmp");
   p.rhs_mode = 0;
-  if (fmode && (pl->checks & ABED_CHECK_FIC) && !pl->reuse_input_checksum) {
+  if (!fmode && pl->af_input && (pl->checks & ABED_CHECK_FIC) && !pl->reuse_input_checksum) {
+    p.rhs_mode = 2;  // FIC-AF: the producer's epilogue supplies the rhs
+  } else if (fmode && (pl->checks & ABED_CHECK_FIC) && !pl->reuse_input_checksum) {
     // float mode: the input-checksum warps compute rhs = sum x * G in-kernel
     const ActGeom& g = pl->g;
     const int64_t cells = (int64_t)g.n_phase * g.c16 * g.Hl * g.Wl;
@@ -264,6 +274,7 @@ abed_dev::VerdictJob plan_verdict_job(const abed_conv_plan* pl, abed_verify_outc
   j.checks = pl->checks & (ABED_CHECK_FC | ABED_CHECK_FIC);
   j.rhs_mode = pl->last_rhs_mode;
   j.rhs_ext = pl->d_acc;
+  j.af_acc = pl->d_af_acc;
   j.rhs_ext_f = pl->d_rhs_f;
   j.tau_fic = pl->tau_fic;
   j.out = out_dev;
@@ -335,6 +346,7 @@ int abed_conv_plan_destroy(abed_conv_plan* pl) {
   cudaFree(pl->d_bsum); cudaFree(pl->d_ficw); cudaFree(pl->d_ficw8); cudaFree(pl->d_fc_part); cudaFree(pl->d_tile_sem);
   cudaFree(pl->d_cta_rec); cudaFree(pl->d_kacc); cudaFree(pl->d_outcome);
   cudaFree(pl->d_facc); cudaFree(pl->d_rhs_f); cudaFree(pl->d_ficwf); cudaFree(pl->d_fsum_f); cudaFree(pl->d_dwf);
+  cudaFree(pl->d_af_acc);
   cudaFree(pl->d_acc); cudaFree(pl->d_zero_bias);
   delete pl;
   return ABED_OK;
@@ -366,6 +378,16 @@ int abed_conv_plan_run(abed_conv_plan* pl, const int8_t* packed, const abed_epil
 }
 int abed_conv_plan_finalize(abed_conv_plan* pl, abed_verify_outcome* outcome_dev, void* stream) {
   return guarded([&] { plan_finalize(pl, outcome_dev, (cudaStream_t)stream); });
+}
+int abed_conv_plan_set_af_input(abed_conv_plan* pl, int32_t on) {
+  return guarded([&] {
+    if (on) {
+      if (!(pl->checks & ABED_CHECK_FIC) || pl->dtype != abed_dev::DT_I8)
+        throw_invalid("FIC-AF: the consumer must be an int8 plan with the FIC check");
+      if (!pl->ficw8_ok) throw_invalid("FIC-AF: the position-weight map exceeds the 3-digit range");
+    }
+    pl->af_input = on ? 1 : 0;
+  });
 }
 int abed_conv_plan_finalize_many(abed_conv_plan* const* plans, int32_t n, abed_verify_outcome* outcomes_dev,
                                  void* stream) {

@@ -210,6 +210,8 @@ struct EpiCtx {
   int64_t nchw_row;        // EPI_NCHW: element (n, 0, p, q)
   int fk_k;                // ConvOut fault channel (or -1)
   bool chunk32, valid, fault_row;
+  const uint4* af_row;     // FIC-AF: next layer's digit cell of this pixel, group 0 (nullptr: off)
+  int64_t af_gstride;      // uint4 stride between channel groups of the digit planes
 };
 
 // One 16-channel chunk of one row: (slow path only: fault hook, filler trim,
@@ -217,7 +219,7 @@ struct EpiCtx {
 // contribution to the row sum.  b = the chunk's 16 biases.
 template <int EPI, bool RELU, bool SUMS, bool SLOW>
 __device__ __forceinline__ int64_t epi_chunk(const ConvTcParams& p, const EpiCtx& e, int32_t (&a)[16],
-                                             const float (&b)[16], int k0) {
+                                             const float (&b)[16], int k0, long long& af_out) {
   if (SLOW) {
     if (e.fault_row && e.fk_k >= k0 && e.fk_k < k0 + 16) {
 #pragma unroll
@@ -268,7 +270,27 @@ __device__ __forceinline__ int64_t epi_chunk(const ConvTcParams& p, const EpiCtx
                                  pack4(y[8], y[9], y[10], y[11]), pack4(y[12], y[13], y[14], y[15]));
     uint4* dst = reinterpret_cast<uint4*>(e.pk_row + static_cast<int64_t>(k0 >> 4) * p.o_plane_len * 16);
     if (EPI == EPI_PACKED) {
-      if (e.valid) *dst = val;
+      if (e.valid) {
+        *dst = val;
+        if (e.af_row) {  // FIC-AF: the next layer's rhs from the stored values (12 dp4a)
+          const uint4* gd = e.af_row + static_cast<int64_t>(k0 >> 4) * e.af_gstride;
+          const uint4 g0 = __ldg(gd), g1 = __ldg(gd + 1), g2 = __ldg(gd + 2);
+          int32_t d0 = 0, d1 = 0, d2 = 0;
+          d0 = __dp4a(static_cast<int>(val.x), static_cast<int>(g0.x), d0);
+          d0 = __dp4a(static_cast<int>(val.y), static_cast<int>(g0.y), d0);
+          d0 = __dp4a(static_cast<int>(val.z), static_cast<int>(g0.z), d0);
+          d0 = __dp4a(static_cast<int>(val.w), static_cast<int>(g0.w), d0);
+          d1 = __dp4a(static_cast<int>(val.x), static_cast<int>(g1.x), d1);
+          d1 = __dp4a(static_cast<int>(val.y), static_cast<int>(g1.y), d1);
+          d1 = __dp4a(static_cast<int>(val.z), static_cast<int>(g1.z), d1);
+          d1 = __dp4a(static_cast<int>(val.w), static_cast<int>(g1.w), d1);
+          d2 = __dp4a(static_cast<int>(val.x), static_cast<int>(g2.x), d2);
+          d2 = __dp4a(static_cast<int>(val.y), static_cast<int>(g2.y), d2);
+          d2 = __dp4a(static_cast<int>(val.z), static_cast<int>(g2.z), d2);
+          d2 = __dp4a(static_cast<int>(val.w), static_cast<int>(g2.w), d2);
+          af_out += static_cast<long long>(d0) + (static_cast<long long>(d1) << 8) + (static_cast<long long>(d2) << 16);
+        }
+      }
     } else if (e.valid) {
       const uint4 ref = *dst;
       if (ref.x != val.x || ref.y != val.y || ref.z != val.z || ref.w != val.w) atomicAdd(p.cmp_count, 1ull);
@@ -387,14 +409,14 @@ __device__ __forceinline__ void load_bias16(const ConvTcParams& p, const EpiCtx&
 // An odd trailing chunk is loaded as a 16-column step.
 template <int DT, int EPI, bool RELU, bool SUMS, bool SLOW>
 __device__ __forceinline__ std::conditional_t<DT == DT_I8, int64_t, double> epi_columns(
-    const ConvTcParams& p, const EpiCtx& e, uint32_t t_row, int k_base, int c_lo, int c_hi) {
+    const ConvTcParams& p, const EpiCtx& e, uint32_t t_row, int k_base, int c_lo, int c_hi, long long& af_out) {
   std::conditional_t<DT == DT_I8, int64_t, double> row_sum = 0;
   auto chunk = [&](uint32_t (&v)[16], const float (&b)[16], int k0) {
     if constexpr (DT == DT_I8) {
       int32_t a[16];
 #pragma unroll
       for (int j = 0; j < 16; ++j) a[j] = static_cast<int32_t>(v[j]);
-      row_sum += epi_chunk<EPI, RELU, SUMS, SLOW>(p, e, a, b, k0);
+      row_sum += epi_chunk<EPI, RELU, SUMS, SLOW>(p, e, a, b, k0, af_out);
     } else {
       row_sum += epi_chunk_h<DT, EPI, RELU, SUMS, SLOW>(p, e, v, b, k0);
     }
@@ -777,6 +799,9 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
     const uint32_t HlWl = static_cast<uint32_t>(p.Hl) * p.Wl;
     FcRec fc{0, kNoKey, 0, 0};
     Acc fic_sum = 0;
+    long long af_sum = 0;  // FIC-AF: this thread's share of the next layer's rhs
+    e.af_row = nullptr;
+    e.af_gstride = p.af_HlWl * 3;
     long long tr_wait = 0, tr_acc = 0, tr_proc = 0;  // diagnostics (registers)
     const int nch = p.block_n >> 4;  // 16-column chunks of real output channels
     const int h0 = (nch + 1) >> 1;
@@ -825,6 +850,10 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
         const int64_t t = (static_cast<int64_t>(n_img) * p.o_Hl + hq) * p.o_Wl + wq;
         e.pk_row = static_cast<int8_t*>(p.out) +
                    (static_cast<int64_t>(a_ph * p.o_nph_w + b_ph) * p.o_c16 * p.o_plane_len + t) * 16;
+        if (EPI == EPI_PACKED && DT == DT_I8 && p.af_ficw8)
+          e.af_row = reinterpret_cast<const uint4*>(p.af_ficw8) +
+                     (static_cast<int64_t>(a_ph * p.o_nph_w + b_ph) * p.o_c16 * p.af_HlWl +
+                      static_cast<int64_t>(hq) * p.o_Wl + wq) * 3;
       } else if (EPI == EPI_NCHW) {
         e.nchw_row = static_cast<int64_t>(n_img) * p.K * e.PQ + static_cast<int64_t>(pp) * p.Q + qq;
       }
@@ -854,13 +883,13 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
       if (p.dbg & 1) {
       } else if (!slow) {
         if (p.dbg & 64)
-          row_sum = epi_columns<DT, EPI, true, false, false>(p, e, t_row, k_base, c_lo, c_hi);
+          row_sum = epi_columns<DT, EPI, true, false, false>(p, e, t_row, k_base, c_lo, c_hi, af_sum);
         else
-          row_sum = p.relu ? epi_columns<DT, EPI, true, FC || FIC, false>(p, e, t_row, k_base, c_lo, c_hi)
-                           : epi_columns<DT, EPI, false, FC || FIC, false>(p, e, t_row, k_base, c_lo, c_hi);
+          row_sum = p.relu ? epi_columns<DT, EPI, true, FC || FIC, false>(p, e, t_row, k_base, c_lo, c_hi, af_sum)
+                           : epi_columns<DT, EPI, false, FC || FIC, false>(p, e, t_row, k_base, c_lo, c_hi, af_sum);
       } else {
-        row_sum = p.relu ? epi_columns<DT, EPI, true, FC || FIC, true>(p, e, t_row, k_base, c_lo, c_hi)
-                         : epi_columns<DT, EPI, false, FC || FIC, true>(p, e, t_row, k_base, c_lo, c_hi);
+        row_sum = p.relu ? epi_columns<DT, EPI, true, FC || FIC, true>(p, e, t_row, k_base, c_lo, c_hi, af_sum)
+                         : epi_columns<DT, EPI, false, FC || FIC, true>(p, e, t_row, k_base, c_lo, c_hi, af_sum);
       }
       // accumulator consumed: hand the TMEM stage back to the MMA warp
       tc_fence_before();
@@ -922,6 +951,12 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
         named_bar(kBarQuarter0 + quarter, 64);
       }
     }
+    if (EPI == EPI_PACKED && DT == DT_I8 && p.af_ficw8) {
+      // FIC-AF partial of this warp straight into the next layer's accumulator
+      // (fire-and-forget reduction; the next layer's verdict reads and resets it)
+      const long long w = warp_sum(af_sum);
+      if (lane == 0 && w != 0) atomicAdd(p.af_acc, static_cast<unsigned long long>(w));
+    }
     if (trace && warp == 2 && lane == 0) {
       trace[10] = tr_wait;
       trace[11] = tr_acc;
@@ -950,7 +985,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
     const int rw = warp - (2 + kEpiWarps);
     long long acc = 0;
     double facc_rhs = 0.0;
-    if (DT != DT_I8 && FIC && p.rhs_mode) {
+    if (DT != DT_I8 && FIC && p.rhs_mode == 1) {
       // float mode: G in f32 [plane][pix][8]; 8 fp16/bf16 values per 16-byte
       // chunk, f32 FMAs per work item, f64 across items (reduce in double like
       // input_checksum_f64 / fic_dot_f64, checksum.hpp:496-535)
@@ -992,7 +1027,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
         }
         facc_rhs += static_cast<double>(item);
       }
-    } else if (DT == DT_I8 && FIC && p.rhs_mode) {
+    } else if (DT == DT_I8 && FIC && p.rhs_mode == 1) {
       pdl_wait();
       const int64_t HlWl = static_cast<int64_t>(p.Hl) * p.Wl;
       const int nsplit = p.rhs_nsplit;
@@ -1180,7 +1215,13 @@ __global__ void __launch_bounds__(256) verdict_kernel(const __grid_constant__ Ve
   }
   if (j.checks & CHECK_FIC) {
     if (j.dtype == DT_I8) {
-      const long long rhs = j.rhs_mode ? Rr : static_cast<long long>(*j.rhs_ext);
+      long long rhs;
+      if (j.rhs_mode == 2) {
+        rhs = static_cast<long long>(*j.af_acc);
+        *j.af_acc = 0ull;  // consumed: the next pass's producer accumulates afresh
+      } else {
+        rhs = j.rhs_mode ? Rr : static_cast<long long>(*j.rhs_ext);
+      }
       // checksum.hpp:287-294: Pass reports lhs = rhs = sum
       write_outcome_dev(out + 1, L != rhs ? 1 : 0, 0, 0, 0, 0, L, rhs, L != rhs ? 1 : 0);
       // kept for later runs that reuse the pristine input checksum (campaigns)

@@ -108,11 +108,18 @@ struct ConvTcParams {
   int64_t* cta_rec;            // [gridDim][kCtaRec] per-CTA {FC count, first key, lhs, rhs, FIC lhs, FIC rhs}
   unsigned long long* kacc;    // [0] FIC lhs, [1] FIC rhs (in-kernel), [2] CTA done ticket
   unsigned long long* rhs_ext;  // FIC rhs of the pristine input: read (rhs_mode 0) or stored (rhs_mode 1)
-  int rhs_mode;                // 1: input-checksum warps compute the FIC rhs in this kernel
+  int rhs_mode;                // 1: input-checksum warps compute the FIC rhs in this kernel,
+                               // 2: AF -- the previous layer's epilogue produced it (af accumulator)
   int rhs_nsplit;              // image split of the rhs work items
   const int8_t* ficw8;         // FIC weight map G as balanced base-256 digits
                                // [phase][c16][Hl*Wl][3 digits][16 channels] (|G| < 2^23)
   void* outcome;               // abed_verify_outcome[3] {FC, FIC, IC}: FC and FIC written here
+  // FIC-AF (fused_conv_epilog's next-layer input checksum tap, checksum.hpp:605-631,
+  // cost_model "AF"): the epilogue accumulates the NEXT layer's FIC rhs
+  // sum y * G_next from the int8 values it stores; nullptr = off
+  const int8_t* af_ficw8;      // next layer's G digit planes [phase][c16][Hl*Wl][3][16]
+  unsigned long long* af_acc;  // next layer's AF rhs accumulator (reset by its verdict)
+  int64_t af_HlWl;             // next layer's pixels per image plane
   unsigned long long* ic_sum;  // [K] per-channel output sums (atomic, integer => deterministic)
   unsigned long long* cmp_count;  // OUT_I8_COMPARE mismatch count
   // ---- fault hook (ConvOut target): flip `fault_bit` of output element
@@ -142,6 +149,7 @@ struct VerdictJob {
   const int64_t* rec;  // [grid][kCtaRec] records of the last run
   int grid, P, Q, dtype, checks, rhs_mode;
   unsigned long long* rhs_ext;
+  unsigned long long* af_acc;  // rhs_mode 2: read, then reset for the next pass
   double* rhs_ext_f;
   double tau_fic;
   void* out;           // abed_verify_outcome[3] {FC, FIC, IC}

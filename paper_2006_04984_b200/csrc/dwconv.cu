@@ -49,6 +49,10 @@ struct DwParams {
   unsigned long long* cmp_count;
   int64_t fault_key;
   int fault_bit;
+  // FIC-AF producer side (see ConvTcParams::af_*)
+  const int8_t* af_ficw8;
+  unsigned long long* af_acc;
+  int64_t af_HlWl;
 };
 
 // 4x4 byte transpose of four taps (a, b, c, d: one byte per channel) so that
@@ -71,6 +75,7 @@ __device__ __forceinline__ int32_t dw_requant(int32_t acc, float scale, float bi
 template <int EPI>  // 0 none, 1 NCHW (int8 / int32 / f32 per out_mode), 2 packed, 3 compare
 __global__ void __launch_bounds__(256) dwconv_i8_kernel(const __grid_constant__ DwParams p) {
   __shared__ long long s_red[8];
+  long long af = 0;
   const uint32_t HlWl = static_cast<uint32_t>(p.Hl) * p.Wl;
   const int64_t PQ = static_cast<int64_t>(p.P) * p.Q;
   long long fic = 0;
@@ -144,6 +149,26 @@ __global__ void __launch_bounds__(256) dwconv_i8_kernel(const __grid_constant__ 
       const uint4 val = make_uint4(w[0], w[1], w[2], w[3]);
       if (EPI == 2) {
         *dst = val;
+        if (p.af_ficw8) {  // FIC-AF: the next layer's rhs from the stored values
+          const uint4* gd = reinterpret_cast<const uint4*>(p.af_ficw8) +
+                            ((static_cast<int64_t>((hh % p.o_sh) * p.o_nph_w + (ww % p.o_sw)) * p.o_c16 + g) * p.af_HlWl +
+                             static_cast<int64_t>(hh / p.o_sh) * p.o_Wl + ww / p.o_sw) * 3;
+          const uint4 g0 = __ldg(gd), g1 = __ldg(gd + 1), g2 = __ldg(gd + 2);
+          int32_t d0 = 0, d1 = 0, d2 = 0;
+          d0 = __dp4a(static_cast<int>(val.x), static_cast<int>(g0.x), d0);
+          d0 = __dp4a(static_cast<int>(val.y), static_cast<int>(g0.y), d0);
+          d0 = __dp4a(static_cast<int>(val.z), static_cast<int>(g0.z), d0);
+          d0 = __dp4a(static_cast<int>(val.w), static_cast<int>(g0.w), d0);
+          d1 = __dp4a(static_cast<int>(val.x), static_cast<int>(g1.x), d1);
+          d1 = __dp4a(static_cast<int>(val.y), static_cast<int>(g1.y), d1);
+          d1 = __dp4a(static_cast<int>(val.z), static_cast<int>(g1.z), d1);
+          d1 = __dp4a(static_cast<int>(val.w), static_cast<int>(g1.w), d1);
+          d2 = __dp4a(static_cast<int>(val.x), static_cast<int>(g2.x), d2);
+          d2 = __dp4a(static_cast<int>(val.y), static_cast<int>(g2.y), d2);
+          d2 = __dp4a(static_cast<int>(val.z), static_cast<int>(g2.z), d2);
+          d2 = __dp4a(static_cast<int>(val.w), static_cast<int>(g2.w), d2);
+          af += static_cast<long long>(d0) + (static_cast<long long>(d1) << 8) + (static_cast<long long>(d2) << 16);
+        }
       } else {
         const uint4 r = *dst;
         if (r.x != val.x || r.y != val.y || r.z != val.z || r.w != val.w) atomicAdd(p.cmp_count, 1ull);
@@ -164,6 +189,11 @@ __global__ void __launch_bounds__(256) dwconv_i8_kernel(const __grid_constant__ 
         }
       }
     }
+  }
+  if (EPI == 2 && p.af_ficw8) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) af += __shfl_xor_sync(0xffffffffu, af, o);
+    if ((threadIdx.x & 31) == 0 && af != 0) atomicAdd(p.af_acc, static_cast<unsigned long long>(af));
   }
   if (p.fic) {
 #pragma unroll
@@ -249,7 +279,18 @@ abed_conv_plan* plan_create_dw(const abed_layer_shape& shape, const int8_t* filt
       cuda_check(cudaMalloc(&pl->d_ficw, nw * 4), "cudaMalloc(ficw)");
       fic_weight_kernel<<<grid_for(nw, 256), 256>>>(pl->d_fsum, g, pl->d_ficw);
       cuda_check(cudaGetLastError(), "fic_weight");
+      cuda_check(cudaMalloc(&pl->d_ficw8, nw * 3), "cudaMalloc(ficw8)");
+      int* d_big = nullptr;
+      cuda_check(cudaMalloc(&d_big, 4), "cudaMalloc(flag)");
+      cuda_check(cudaMemset(d_big, 0, 4), "memset flag");
+      fic_weight_digits_kernel<<<grid_for(nw, 256), 256>>>(pl->d_ficw, nw / 16, pl->d_ficw8, d_big);
+      int big = 0;
+      cuda_check(cudaMemcpy(&big, d_big, 4, cudaMemcpyDeviceToHost), "flag d2h");
+      cudaFree(d_big);
+      pl->ficw8_ok = big ? 0 : 1;
     }
+    cuda_check(cudaMalloc(&pl->d_af_acc, 8), "cudaMalloc(af_acc)");
+    cuda_check(cudaMemset(pl->d_af_acc, 0, 8), "memset af_acc");
     cuda_check(cudaDeviceSynchronize(), "plan_create_dw sync");
   } catch (...) {
     abed_conv_plan_destroy(pl);
@@ -305,6 +346,11 @@ void plan_run_dw(abed_conv_plan* pl, const int8_t* packed, const abed_epilog_par
     }
     p.o_plane_len = o.plane_len; p.o_Hl = o.Hl; p.o_Wl = o.Wl; p.o_ph = o.ph; p.o_pw = o.pw;
     p.o_sh = o.sh; p.o_sw = o.sw; p.o_nph_w = o.nph_w; p.o_c16 = o.c16;
+    if (next && out_mode == ABED_OUT_I8_PACKED && next->af_input && (next->checks & ABED_CHECK_FIC)) {
+      p.af_ficw8 = next->d_ficw8;
+      p.af_acc = next->d_af_acc;
+      p.af_HlWl = (int64_t)o.Hl * o.Wl;
+    }
     if (out_mode == ABED_OUT_I8_COMPARE) cuda_check(cudaMemsetAsync(pl->d_acc + 1, 0, 8, st), "memset cmp");
   }
   p.fic = (pl->checks & ABED_CHECK_FIC) ? 1 : 0;
@@ -312,7 +358,8 @@ void plan_run_dw(abed_conv_plan* pl, const int8_t* packed, const abed_epilog_par
   p.cmp_count = pl->d_acc + 1;
   p.fault_key = fault_key;
   p.fault_bit = fault_bit;
-  if (p.fic && !pl->reuse_input_checksum) {
+  const bool af_in = p.fic && pl->af_input && !pl->reuse_input_checksum;
+  if (p.fic && !pl->reuse_input_checksum && !af_in) {
     // FR: input checksum dot of the stored input, one pass ahead of the conv
     cuda_check(cudaMemsetAsync(pl->d_acc, 0, 8, st), "memset rhs");
     const int64_t cells = (int64_t)g.n_phase * g.c16 * g.Hl * g.Wl;
@@ -320,7 +367,7 @@ void plan_run_dw(abed_conv_plan* pl, const int8_t* packed, const abed_epilog_par
     fic_rhs_kernel<<<grid_for(cells * nsplit, 256), 256, 0, st>>>(packed, g, pl->d_ficw, nsplit, pl->d_acc);
     cuda_check(cudaGetLastError(), "fic_rhs");
   }
-  pl->last_rhs_mode = 0;  // the verdict reads the rhs from d_acc[0]
+  pl->last_rhs_mode = af_in ? 2 : 0;  // AF accumulator, or the FR rhs in d_acc[0]
   const int grid = dw_grid();
   switch (out_mode) {
     case ABED_OUT_NONE: abed_dev::dwconv_i8_kernel<0><<<grid, 256, 0, st>>>(p); break;
