@@ -343,7 +343,10 @@ def measure_mobilenetv2_int8(args, dev, stream, flush, world, dist):
                 f = api.fill_random_i8(ls.c * 9, api.derive_seed(seed, 2)).view(ls.c, 1, 3, 3)
                 mk = lambda ch, ls=ls, f=f: api.ConvPlanDW(ls, f, ch)  # noqa: E731
                 ops += 2 * ls.n * ls.k * ls.p * ls.q * 9
-            L = {"kind": kind, "ls": ls, "plans": {"unprotected": mk(0), "fic": mk(abi.CHECK_FIC)}}
+            L = {"kind": kind, "ls": ls, "plans": {"unprotected": mk(0), "fic": mk(abi.CHECK_FIC),
+                                                    "fic_af": mk(abi.CHECK_FIC)}}
+            if block:  # FIC-AF: rhs accumulated by the producing layer's epilogue
+                L["plans"]["fic_af"].set_af_input(True)
             L["ep"] = {v: pl.epilog_params(0.02, None, True) for v, pl in L["plans"].items()}
             block.append(L)
         # activation buffers: block input (fresh data), then each layer writes the next one's input
@@ -358,11 +361,12 @@ def measure_mobilenetv2_int8(args, dev, stream, flush, world, dist):
                                        dtype=torch.int8, device=dev)
         block[-1]["next"] = None
         layers += block
-    sets = {"fic": api.PlanSet([L["plans"]["fic"] for L in layers])}
+    VARIANTS = ("unprotected", "fic", "fic_af", "dup")
+    sets = {v: api.PlanSet([L["plans"][v] for L in layers]) for v in ("fic", "fic_af")}
 
     def step(variant):
         for L in layers:
-            nxt = L["next"]["plans"]["unprotected"] if L["next"] else None
+            nxt = L["next"]["plans"]["fic_af" if variant == "fic_af" else "unprotected"] if L["next"] else None
             if variant == "dup":
                 pl = L["plans"]["unprotected"]
                 pl.run(L["in"], L["out"], abi.OUT_I8_PACKED, ep=L["ep"]["unprotected"], next_plan=nxt)
@@ -374,17 +378,17 @@ def measure_mobilenetv2_int8(args, dev, stream, flush, world, dist):
             sets[variant].finalize()
 
     with torch.cuda.stream(stream):
-        for v in ("unprotected", "fic", "dup"):
+        for v in VARIANTS:
             step(v)
     torch.cuda.synchronize()
     graphs = {}
-    for v in ("unprotected", "fic", "dup"):
+    for v in VARIANTS:
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=stream):
             step(v)
         graphs[v] = g
     res = {}
-    for v in ("unprotected", "dup", "fic"):
+    for v in VARIANTS:
         for _ in range(max(3, args.warmup)):
             flush.zero_()
             graphs[v].replay()
@@ -407,12 +411,14 @@ def measure_mobilenetv2_int8(args, dev, stream, flush, world, dist):
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             ms = tt.item()
         res[v] = {"tops": round(ops * world / (ms * 1e-3) / 1e12, 2), "ms_per_step": round(ms, 4)}
-    fails = sum(oc[1].status for oc in sets["fic"].outcomes())
+    fails = sum(oc[1].status for v in ("fic", "fic_af") for oc in sets[v].outcomes())
     u = res["unprotected"]["ms_per_step"]
     return {"workload": "mobilenetv2-5-blocks-int8-b32 (15 layers: pw 1x1 tcgen05 + dw 3x3 CUDA cores, chained)",
+            "fic_af": "FIC with each in-block layer's input checksum accumulated by the producing epilogue",
             "blocks": [list(b) for b in MBV2_BLOCKS], "global_batch": BATCH * world,
             "gop_per_step": round(ops * world / 1e9, 2), "variants": res,
             "overhead_pct": {"fic_vs_unprotected": round(100 * (res["fic"]["ms_per_step"] / u - 1), 2),
+                             "fic_af_vs_unprotected": round(100 * (res["fic_af"]["ms_per_step"] / u - 1), 2),
                              "duplication_vs_unprotected": round(100 * (res["dup"]["ms_per_step"] / u - 1), 2)},
             "fault_free_verdicts_failed": fails}
 
