@@ -284,6 +284,15 @@ int abed_conv_plan_finalize_many(abed_conv_plan* const* plans, int32_t n, abed_v
  * an earlier run instead of recomputing it from the (possibly corrupted) input;
  * the run is then exactly one kernel launch (fault campaigns, kernel timing). */
 int abed_conv_plan_set_reuse_input_checksum(abed_conv_plan* plan, int32_t reuse);
+/* Where an int8 FIC plan's in-kernel input checksum (the FIC right-hand side,
+ * gen_input_checksum + fic_dot, checksum.hpp:248-285) reads the input from:
+ * ABED_RHS_REREAD (default) reads the stored input a second time (the cost
+ * model's "FR" option); ABED_RHS_STAGED dots the activation tiles the conv
+ * kernel has already staged in shared memory (each M tile owns 128 plane pixels
+ * of every strip), so the input is read from HBM once.  Both are exact and
+ * bit-identical; see DESIGN.md for the measured trade-off. */
+enum { ABED_RHS_STAGED = 0, ABED_RHS_REREAD = 1 };
+int abed_conv_plan_set_input_checksum_source(abed_conv_plan* plan, int32_t source);
 /* duplication baseline: mismatch count of the last OUT_I8_COMPARE run (synchronous) */
 int abed_conv_plan_compare_count(abed_conv_plan* plan, int64_t* count);
 /* ---- depthwise conv (MobileNetV2; no reference counterpart).

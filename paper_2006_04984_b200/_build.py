@@ -6,6 +6,7 @@ Incremental: an object is rebuilt when its .cu or any csrc header is newer.
 """
 from __future__ import annotations
 
+import concurrent.futures
 import glob
 import os
 import subprocess
@@ -37,7 +38,7 @@ def build(verbose: bool = False) -> str:
     headers = glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h")) + \
         glob.glob(os.path.join(ROOT, "include", "*.h"))
     hdr_mtime = max((os.path.getmtime(h) for h in headers), default=0)
-    objs = []
+    objs, cmds = [], []
     for src in sources:
         obj = os.path.join(BUILD, os.path.basename(src).replace(".cu", ".o"))
         objs.append(obj)
@@ -46,7 +47,10 @@ def build(verbose: bool = False) -> str:
         cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
         if verbose:
             print(" ".join(cmd))
-        _run(cmd)
+        cmds.append(cmd)
+    # translation units are independent: compile them concurrently
+    with concurrent.futures.ThreadPoolExecutor(max(1, min(len(cmds), os.cpu_count() or 1))) as ex:
+        list(ex.map(_run, cmds))
     if not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
         _run([NVCC, *ARCH, "-shared", "-o", LIB, *objs])
     return LIB

@@ -21,6 +21,8 @@ TARGET_INPUT, TARGET_FILTER, TARGET_CONVOUT = 0, 1, 2
 DETECTED, SDC, MASKED, DETECTED_BENIGN = 0, 1, 2, 3
 DATA_ONES, DATA_RANDOM_I8 = 0, 1
 CHECK_FC, CHECK_FIC, CHECK_IC = 1, 2, 4
+# FIC input-checksum source (abed_conv_plan_set_input_checksum_source)
+RHS_STAGED, RHS_REREAD = 0, 1
 OUT_NONE, OUT_I32_NCHW, OUT_I8_NCHW, OUT_F32_NCHW, OUT_I8_PACKED, OUT_I8_COMPARE, OUT_H_PACKED, OUT_H_COMPARE = range(8)
 F16, BF16 = 4, 5  # float mode on tensor cores: 16-bit operand storage kinds
 
@@ -179,6 +181,7 @@ SIGNATURES = {
     "abed_conv_plan_create_dw": (C.c_int, [SHP, P, i32, C.POINTER(P)]),
     "abed_conv_plan_set_af_input": (C.c_int, [P, i32]),
     "abed_conv_plan_set_reuse_input_checksum": (C.c_int, [P, i32]),
+    "abed_conv_plan_set_input_checksum_source": (C.c_int, [P, i32]),
 }
 
 _lib = None

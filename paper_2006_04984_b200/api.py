@@ -349,6 +349,10 @@ class ConvPlan:
     def finalize(self, stream=None):
         call("abed_conv_plan_finalize", self.handle, _p(self._outcomes), stream or _stream())
 
+    def set_input_checksum_source(self, source: int = abi.RHS_STAGED):
+        """FIC rhs from the staged activation tiles (default) or a re-read of the input (FR)."""
+        call("abed_conv_plan_set_input_checksum_source", self.handle, source)
+
     def set_af_input(self, on: bool = True):
         """FIC-AF: this layer's FIC rhs comes from the previous layer's epilogue."""
         call("abed_conv_plan_set_af_input", self.handle, 1 if on else 0)

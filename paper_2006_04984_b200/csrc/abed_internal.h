@@ -5,6 +5,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "../../include/abed_b200.h"
 #include "conv_tc.cuh"
@@ -41,7 +42,8 @@ int guarded(Fn&& fn) {
 abed_dev::ActGeom make_geom(const abed_layer_shape& s, int cpg = 16);
 int geom_strip_pix(const abed_dev::ActGeom& g);
 int64_t geom_packed_bytes(const abed_dev::ActGeom& g);
-bool choose_tiling(const abed_dev::ActGeom& g, bool fc, int force_block_n, abed_dev::ConvTcParams& p);
+bool choose_tiling(const abed_dev::ActGeom& g, bool fc, int force_block_n, abed_dev::ConvTcParams& p,
+                   uint32_t reserve = 0);
 int num_sms();
 
 __global__ void pack_input_kernel(const int8_t* x, abed_dev::ActGeom g, int8_t* out);
@@ -53,6 +55,7 @@ __global__ void box_sum_dot_kernel(const int32_t* bsum, abed_dev::ActGeom g, con
                                    int32_t* ic_out, unsigned long long* fic_rhs);
 __global__ void fic_weight_kernel(const int32_t* fsum, abed_dev::ActGeom g, int32_t* G);
 __global__ void fic_weight_digits_kernel(const int32_t* G, int64_t cells, int8_t* G8, int* too_big);
+__global__ void fic_class_table_kernel(const int8_t* G8, abed_dev::ActGeom g, const int* rep, int n_rep, int8_t* T8);
 __global__ void fic_rhs_kernel(const int8_t* act, abed_dev::ActGeom g, const int32_t* G, int nsplit,
                                unsigned long long* rhs);
 __global__ void fc_finalize_rec_kernel(const int64_t* rec, int m_tiles, int P, int Q, abed_verify_outcome* out);
@@ -83,6 +86,8 @@ int set_error(int code, const std::string& msg);
 void require_device();
 int grid_for(int64_t n, int threads);
 void validate_shape(const abed_layer_shape& s);
+void build_fic_classes(abed_conv_plan* pl);
+uint32_t fic_classes_host(abed_conv_plan* pl);
 abed_conv_plan* plan_create(const abed_layer_shape& shape, const int8_t* filters, int checks, int force_bn);
 // dwconv.cu: depthwise plan (shares abed_conv_plan; dispatched by plan_run)
 abed_conv_plan* plan_create_dw(const abed_layer_shape& shape, const int8_t* filters, int checks);
@@ -117,6 +122,18 @@ struct abed_conv_plan {
   int32_t* d_ficw = nullptr;    // FIC position weights G [phase][c16][Hl*Wl][16] (offline)
   int8_t* d_ficw8 = nullptr;    // G as 3 balanced base-256 digit planes [phase][c16][Hl*Wl][3][16]
   int ficw8_ok = 0;             // every |G| < 2^23 (3 digits are exact)
+  int8_t* d_ficc8 = nullptr;    // G class table [phase][nrc][ncc][c16][3][16] (FIC-SM)
+  uint8_t* d_rowcls = nullptr;  // [nph_h][Hl] / [nph_w][Wl] row / column classes
+  uint8_t* d_colcls = nullptr;
+  int nrc = 0, ncc = 0;
+  std::vector<uint8_t> h_rowcls, h_colcls;  // host copies (FIC-SM)
+  std::vector<int> h_rep;                    // representative plane pixel per class pair
+  // FIC input checksum source: ABED_RHS_REREAD (default; the input-checksum warps
+  // read the stored input a second time, "FR") or ABED_RHS_STAGED (they dot the
+  // A stages already in shared memory).  Measured on B200 at batch 32 / 256 / 1024
+  // the staged source is slower (its 4 shared-memory loads per 16-byte chunk
+  // compete with the SS-mode MMA operand reads and it holds stages), so FR is default.
+  int rhs_src = ABED_RHS_REREAD;
   int64_t* d_fc_part = nullptr;     // FC row partials per N tile (n_tiles > 1)
   unsigned int* d_tile_sem = nullptr;  // FC tiles-done counters per M tile
   int64_t* d_cta_rec = nullptr;     // FC per-CTA records

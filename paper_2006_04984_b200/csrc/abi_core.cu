@@ -64,8 +64,17 @@ void plan_init_common(abed_conv_plan* pl, const abed_layer_shape& shape, int che
   const ActGeom& g = pl->g;
   ConvTcParams& p = pl->base;
   std::memset(&p, 0, sizeof(p));
-  if (!choose_tiling(g, (checks & ABED_CHECK_FC) != 0, force_bn, p))
-    throw_invalid("conv: no tiling fits shared memory for this layer");
+  // int8 FIC: shared memory for the staged input checksum's class table
+  const uint32_t fic_smem = (cpg == 16 && (checks & ABED_CHECK_FIC)) ? fic_classes_host(pl) : 0u;
+  bool tiled = choose_tiling(g, (checks & ABED_CHECK_FC) != 0, force_bn, p, fic_smem);
+  if (tiled && fic_smem) {
+    p.fic_smem = fic_smem;
+    p.fic_tab_bytes = (uint32_t)(pl->h_rep.size() * g.c16 * 48);
+  } else if (fic_smem) {
+    pl->h_rep.clear();  // no room: FIC keeps the FR re-read
+    tiled = choose_tiling(g, (checks & ABED_CHECK_FC) != 0, force_bn, p);
+  }
+  if (!tiled) throw_invalid("conv: no tiling fits shared memory for this layer");
   p.plane_len = g.plane_len;
   p.n_phase = g.n_phase;
   p.c16 = g.c16;
@@ -100,6 +109,93 @@ void plan_init_common(abed_conv_plan* pl, const abed_layer_shape& shape, int che
   cuda_check(cudaMemset(pl->d_zero_bias, 0, shape.k * 4), "memset bias");
   cuda_check(cudaMalloc(&pl->d_af_acc, 8), "cudaMalloc(af_acc)");
   cuda_check(cudaMemset(pl->d_af_acc, 0, 8), "memset af_acc");
+}
+
+// FIC-SM class table.  A phase row i is reached by the filter rows
+// {r : r % sh == a, 0 <= i - r / sh < P} (the same test fic_weight_kernel applies
+// per pixel); rows with equal sets share one class, likewise columns, so G is a
+// function of (phase, row class, column class, channel).  The table copies G
+// from one representative pixel per class pair (rows / columns never reached
+// get a class whose G is zero).
+uint32_t fic_classes_host(abed_conv_plan* pl) {
+  const ActGeom& g = pl->g;
+  if (g.n_phase > 4) return 0;  // the kernel's staged path handles up to 2 x 2 stride phases
+  auto classes = [](int L, int R, int st, int P, int nph, std::vector<uint8_t>& cls, std::vector<int>& rep, int& ncls) {
+    cls.assign((size_t)nph * L, 0);
+    ncls = 0;
+    std::vector<std::vector<uint64_t>> masks(nph);
+    std::vector<std::vector<int>> reps(nph);
+    for (int a = 0; a < nph; ++a) {
+      for (int i = 0; i < L; ++i) {
+        uint64_t m = 0;
+        for (int r = 0; r < R; ++r)
+          if (r % st == a && i - r / st >= 0 && i - r / st < P) m |= uint64_t(1) << r;
+        int id = -1;
+        for (size_t k = 0; k < masks[a].size(); ++k)
+          if (masks[a][k] == m) id = (int)k;
+        if (id < 0) {
+          id = (int)masks[a].size();
+          masks[a].push_back(m);
+          reps[a].push_back(i);
+        }
+        cls[(size_t)a * L + i] = (uint8_t)std::min(id, 255);
+      }
+      ncls = std::max(ncls, (int)masks[a].size());
+    }
+    rep.assign((size_t)nph * ncls, -1);
+    for (int a = 0; a < nph; ++a)
+      for (size_t k = 0; k < reps[a].size(); ++k) rep[(size_t)a * ncls + k] = reps[a][k];
+  };
+  std::vector<int> rrep, crep;
+  int nrc = 0, ncc = 0;
+  classes(g.Hl, g.r, g.sh, g.p, g.nph_h, pl->h_rowcls, rrep, nrc);
+  classes(g.Wl, g.s, g.sw, g.q, g.nph_w, pl->h_colcls, crep, ncc);
+  // + one all-zero cell that pixels outside the images point at (branch-free kernel loop)
+  const uint64_t tab = ((uint64_t)g.n_phase * nrc * ncc + 1) * g.c16 * 48;
+  if (nrc > 255 || ncc > 255 || tab > 48 * 1024) return 0;  // keep the FR re-read
+  // representative plane pixel (or -1) of every (phase, row class, column class)
+  pl->h_rep.assign((size_t)g.n_phase * nrc * ncc, -1);
+  for (int ph = 0; ph < g.n_phase; ++ph) {
+    const int a = ph / g.nph_w, b = ph % g.nph_w;
+    for (int i = 0; i < nrc; ++i)
+      for (int j = 0; j < ncc; ++j) {
+        const int ri = rrep[(size_t)a * nrc + i], cj = crep[(size_t)b * ncc + j];
+        if (ri >= 0 && cj >= 0) pl->h_rep[((size_t)ph * nrc + i) * ncc + j] = ri * g.Wl + cj;
+      }
+  }
+  pl->h_rep.push_back(-1);  // the zero cell
+  pl->nrc = nrc;
+  pl->ncc = ncc;
+  return (uint32_t)(tab + ((pl->h_rowcls.size() + 15) & ~size_t(15)) + ((pl->h_colcls.size() + 15) & ~size_t(15)));
+}
+
+// FIC-SM class table.  A phase row i is reached by the filter rows
+// {r : r % sh == a, 0 <= i - r / sh < P} (the test fic_weight_kernel applies per
+// pixel); rows with equal sets share one class, likewise columns, so G is a
+// function of (phase, row class, column class, channel).  The table copies G
+// from one representative pixel per class pair (rows / columns never reached
+// get a class whose G is zero).  The conv kernel keeps the table and the class
+// arrays in shared memory (ConvTcParams::fic_smem, reserved by choose_tiling).
+void build_fic_classes(abed_conv_plan* pl) {
+  // one buffer [table | row classes (16-B padded) | column classes (padded)],
+  // copied into shared memory by one bulk copy per CTA
+  const ActGeom& g = pl->g;
+  const std::vector<int>& rep = pl->h_rep;
+  const ConvTcParams& p = pl->base;
+  int* d_rep = nullptr;
+  cuda_check(cudaMalloc(&d_rep, rep.size() * 4), "cudaMalloc(rep)");
+  cuda_check(cudaMemcpy(d_rep, rep.data(), rep.size() * 4, cudaMemcpyHostToDevice), "rep h2d");
+  const int64_t cells = (int64_t)rep.size() * g.c16;
+  cuda_check(cudaMalloc(&pl->d_ficc8, p.fic_smem), "cudaMalloc(ficc8)");
+  cuda_check(cudaMemset(pl->d_ficc8, 0, p.fic_smem), "memset ficc8");
+  fic_class_table_kernel<<<grid_for(cells * 48), 256>>>(pl->d_ficw8, g, d_rep, (int)rep.size(), pl->d_ficc8);
+  cuda_check(cudaGetLastError(), "fic_class_table");
+  pl->d_rowcls = reinterpret_cast<uint8_t*>(pl->d_ficc8) + p.fic_tab_bytes;
+  pl->d_colcls = pl->d_rowcls + ((pl->h_rowcls.size() + 15) & ~size_t(15));
+  cuda_check(cudaMemcpy(pl->d_rowcls, pl->h_rowcls.data(), pl->h_rowcls.size(), cudaMemcpyHostToDevice), "rowcls h2d");
+  cuda_check(cudaMemcpy(pl->d_colcls, pl->h_colcls.data(), pl->h_colcls.size(), cudaMemcpyHostToDevice), "colcls h2d");
+  cuda_check(cudaDeviceSynchronize(), "fic classes sync");
+  cudaFree(d_rep);
 }
 
 abed_conv_plan* plan_create(const abed_layer_shape& shape, const int8_t* filters, int checks, int force_bn) {
@@ -143,6 +239,7 @@ abed_conv_plan* plan_create(const abed_layer_shape& shape, const int8_t* filters
       cudaFree(d_big);
       pl->ficw8_ok = big ? 0 : 1;
       cuda_check(cudaGetLastError(), "fic_weight");
+      if (pl->ficw8_ok && !pl->h_rep.empty()) build_fic_classes(pl);
     }
     cuda_check(cudaDeviceSynchronize(), "plan_create sync");
   } catch (...) {
@@ -245,7 +342,16 @@ void plan_run(abed_conv_plan* pl, const int8_t* packed, const abed_epilog_params
       cuda_check(cudaGetLastError(), "input checksum");
     } else {
       const int64_t cells = (int64_t)g.n_phase * g.c16 * g.Hl * g.Wl;
-      if (pl->ficw8_ok) {
+      if (pl->ficw8_ok && pl->d_ficc8 && pl->rhs_src == ABED_RHS_STAGED && g.n_phase <= 4) {
+        // FIC only: rhs = sum x * G computed by the conv kernel's input-checksum
+        // warps from the activation tiles already staged for the MMAs
+        p.rhs_mode = 3;
+        p.ficc8 = pl->d_ficc8;
+        p.rowcls = pl->d_rowcls;
+        p.colcls = pl->d_colcls;
+        p.nrc = pl->nrc;
+        p.ncc = pl->ncc;
+      } else if (pl->ficw8_ok) {
         // FIC only: rhs = sum x * G computed by the conv kernel's input-checksum
         // warps from their own read of the stored input
         p.rhs_mode = 1;
@@ -346,7 +452,7 @@ int abed_conv_plan_destroy(abed_conv_plan* pl) {
   cudaFree(pl->d_bsum); cudaFree(pl->d_ficw); cudaFree(pl->d_ficw8); cudaFree(pl->d_fc_part); cudaFree(pl->d_tile_sem);
   cudaFree(pl->d_cta_rec); cudaFree(pl->d_kacc); cudaFree(pl->d_outcome);
   cudaFree(pl->d_facc); cudaFree(pl->d_rhs_f); cudaFree(pl->d_ficwf); cudaFree(pl->d_fsum_f); cudaFree(pl->d_dwf);
-  cudaFree(pl->d_af_acc);
+  cudaFree(pl->d_af_acc); cudaFree(pl->d_ficc8);  // row / column classes live inside it
   cudaFree(pl->d_acc); cudaFree(pl->d_zero_bias);
   delete pl;
   return ABED_OK;
@@ -403,6 +509,13 @@ int abed_conv_plan_finalize_many(abed_conv_plan* const* plans, int32_t n, abed_v
                                                                outcomes_dev + 3 * i + 2);
     }
     cuda_check(verdict_launch(jobs.data(), (int)jobs.size(), (cudaStream_t)stream), "verdict");
+  });
+}
+int abed_conv_plan_set_input_checksum_source(abed_conv_plan* pl, int32_t source) {
+  return guarded([&] {
+    if (!pl) throw_invalid("plan is null");
+    if (source != ABED_RHS_STAGED && source != ABED_RHS_REREAD) throw_invalid("input checksum source must be 0 or 1");
+    pl->rhs_src = source;
   });
 }
 int abed_conv_plan_set_reuse_input_checksum(abed_conv_plan* pl, int32_t reuse) {

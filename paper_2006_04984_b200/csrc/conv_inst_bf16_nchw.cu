@@ -1,0 +1,6 @@
+// explicit instantiation: conv kernel variants for (DT_BF16, EPI_NCHW)
+#include "conv_tc_kernel.cuh"
+
+namespace abed_host {
+template cudaError_t launch_epi<abed_dev::DT_BF16, abed_dev::EPI_NCHW>(const ConvTcParams&, int, bool, cudaStream_t);
+}  // namespace abed_host

@@ -108,11 +108,23 @@ struct ConvTcParams {
   int64_t* cta_rec;            // [gridDim][kCtaRec] per-CTA {FC count, first key, lhs, rhs, FIC lhs, FIC rhs}
   unsigned long long* kacc;    // [0] FIC lhs, [1] FIC rhs (in-kernel), [2] CTA done ticket
   unsigned long long* rhs_ext;  // FIC rhs of the pristine input: read (rhs_mode 0) or stored (rhs_mode 1)
-  int rhs_mode;                // 1: input-checksum warps compute the FIC rhs in this kernel,
-                               // 2: AF -- the previous layer's epilogue produced it (af accumulator)
+  int rhs_mode;                // 1: input-checksum warps compute the FIC rhs in this kernel (FR re-read),
+                               // 2: AF -- the previous layer's epilogue produced it (af accumulator),
+                               // 3: SM -- input-checksum warps read the staged A tiles (no re-read)
   int rhs_nsplit;              // image split of the rhs work items
   const int8_t* ficw8;         // FIC weight map G as balanced base-256 digits
                                // [phase][c16][Hl*Wl][3 digits][16 channels] (|G| < 2^23)
+  // rhs_mode 3 (FIC-SM): the input-checksum warps take x from the A stages the
+  // producer already staged (each M tile owns plane pixels [m0, m0 + 128) of
+  // every strip) and G from a class table: G depends on a pixel only through
+  // which filter rows / columns reach it, so G[phase][i][j] =
+  // ficc8[phase][rowcls[a][i]][colcls[b][j]] -- a few KB instead of a map
+  const int8_t* ficc8;         // [c16][3 digits][phase][nrc][ncc][16 channels]
+  const uint8_t* rowcls;       // [nph_h][Hl] row class per phase row
+  const uint8_t* colcls;       // [nph_w][Wl] column class per phase column
+  int nrc, ncc;
+  uint32_t fic_smem;           // bytes of the kernel's smem copy of {ficc8, rowcls, colcls} (0: none)
+  uint32_t fic_tab_bytes;      // ficc8 part of it
   void* outcome;               // abed_verify_outcome[3] {FC, FIC, IC}: FC and FIC written here
   // FIC-AF (fused_conv_epilog's next-layer input checksum tap, checksum.hpp:605-631,
   // cost_model "AF"): the epilogue accumulates the NEXT layer's FIC rhs

@@ -277,6 +277,26 @@ __global__ void fic_weight_digits_kernel(const int32_t* __restrict__ G, int64_t 
   }
 }
 
+// FIC-SM class table, digit-plane major so that pixels of different classes
+// read different shared-memory banks: T8[((grp * 3 + digit) * n_rep + cls) * 16 + e]
+// = digit `digit` of G for channel grp * 16 + e at class cls's representative
+// pixel (cls = (phase * nrc + rc) * ncc + cc); zero for class pairs no pixel has
+__global__ void fic_class_table_kernel(const int8_t* __restrict__ G8, ActGeom g, const int* __restrict__ rep, int n_rep,
+                                       int8_t* __restrict__ T8) {
+  const int64_t HlWl = (int64_t)g.Hl * g.Wl;
+  const int64_t total = (int64_t)n_rep * g.c16 * 48;
+  const int per_phase = (n_rep - 1) / g.n_phase;  // the last cell is the zero cell
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int e = (int)(idx & 15);
+    const int cls = (int)((idx >> 4) % n_rep);
+    const int64_t gd = (idx >> 4) / n_rep;  // grp * 3 + digit
+    const int grp = (int)(gd / 3), digit = (int)(gd % 3);
+    const int pix = rep[cls];
+    const int phase = cls / per_phase;
+    T8[idx] = pix < 0 ? (int8_t)0 : G8[(((int64_t)phase * g.c16 + grp) * HlWl + pix) * 48 + digit * 16 + e];
+  }
+}
+
 // rhs += sum over (plane, image block pixel, image) of x . G ; images split in
 // `nsplit` groups so enough loads are in flight to stream HBM.
 __global__ void fic_rhs_kernel(const int8_t* __restrict__ act, ActGeom g, const int32_t* __restrict__ G, int nsplit,
@@ -485,7 +505,8 @@ static double mma_cycles(int n) {
   return c;
 }
 
-bool choose_tiling(const ActGeom& g, bool fc, int force_block_n, ConvTcParams& p) {
+bool choose_tiling(const ActGeom& g, bool fc, int force_block_n, ConvTcParams& p, uint32_t reserve) {
+  const uint32_t kBudget = kSmemBudget - reserve;  // minus the FIC-SM class table
   // Pick (block_n, channel groups per stage) minimising the modelled kernel time:
   // waves of persistent work units x MMAs per unit x cycles per MMA.
   const int ntaps = g.r * g.s;
@@ -509,8 +530,8 @@ bool choose_tiling(const ActGeom& g, bool fc, int force_block_n, ConvTcParams& p
       // resident B (a CTA keeps its N tile's filters in smem)
       const uint32_t bres = bstage * (g.c16 / gps);
       int stages_res = 0;
-      if (bres + tab < kSmemBudget) stages_res = std::min<int>(abed_dev::kStages, (kSmemBudget - bres - tab) / a_stage(gps));
-      const int stages_ring = std::min<int>(abed_dev::kStages, (kSmemBudget - tab) / (a_stage(gps) + bstage));
+      if (bres + tab < kBudget) stages_res = std::min<int>(abed_dev::kStages, (kBudget - bres - tab) / a_stage(gps));
+      const int stages_ring = std::min<int>(abed_dev::kStages, (kBudget - tab) / (a_stage(gps) + bstage));
       const bool res_ok = stages_res >= 2;
       const bool ring_ok = stages_ring >= 2;
       if (!res_ok && !ring_ok) continue;
