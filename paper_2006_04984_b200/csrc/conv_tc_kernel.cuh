@@ -42,13 +42,14 @@
 namespace abed_dev {
 
 constexpr int kEpiWarps = 8;
+constexpr int kEpiParts = kEpiWarps / 4;  // epilogue warps per TMEM lane quarter
 constexpr int kEpiThreads = kEpiWarps * 32;
 constexpr int kRhsWarps = 2;
 constexpr int kConvThreads = 64 + kEpiThreads + kRhsWarps * 32;
 constexpr int kBiasSmem = 2048;
 constexpr int kBarEpi = 1;       // named barrier: all epilogue warps
-constexpr int kBarHalf0 = 2;     // named barrier: the four half-0 epilogue warps
-constexpr int kBarQuarter0 = 4;  // named barriers 4..7: the two warps of a TMEM lane quarter
+constexpr int kBarHalf0 = 2;     // named barrier: the four part-0 epilogue warps
+constexpr int kBarQuarter0 = 4;  // named barriers 4..7: the epilogue warps of a TMEM lane quarter
 constexpr int64_t kNoKey = 0x7fffffffffffffffll;
 
 // compile-time output flavours
@@ -625,7 +626,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
   __shared__ FcRec s_fc[kEpiWarps];
   __shared__ long long s_lhs[kEpiWarps];
   __shared__ long long s_rhs[kRhsWarps];
-  __shared__ int64_t s_rowsum[kBlockM];
+  __shared__ int64_t s_rowsum[kEpiParts - 1][kBlockM];
   __shared__ int s_tile_last;
 
   // warp index through a shuffle: provably warp-uniform, so ptxas keeps the
@@ -780,10 +781,12 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
     }
   } else if (warp < 2 + kEpiWarps) {
     // ------------------------------------------------------------ epilogue
-    // Two warps per TMEM lane quarter split the tile's 16-column chunks into
-    // contiguous halves; every epilogue warp drains every unit.
-    const int ew = warp - 2;        // 0..7
-    const int half = ew >> 2;       // which half of the chunks
+    // kEpiParts warps per TMEM lane quarter split the tile's 16-column chunks
+    // into contiguous parts; every epilogue warp drains every unit.  Several
+    // warps per SM sub-partition keep tcgen05.ld latency hidden behind the
+    // requantise math of the others.
+    const int ew = warp - 2;        // 0 .. kEpiWarps-1
+    const int part = ew >> 2;       // which part of the chunks
     const int quarter = warp & 3;   // TMEM lane quarter this warp may access
     const int row = quarter * 32 + lane;
     pdl_wait();
@@ -812,8 +815,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
     e.af_gstride = p.af_HlWl * 3;
     long long tr_wait = 0, tr_acc = 0, tr_proc = 0;  // diagnostics (registers)
     const int nch = p.block_n >> 4;  // 16-column chunks of real output channels
-    const int h0 = (nch + 1) >> 1;
-    const int c_lo = half ? h0 : 0, c_hi = half ? nch : h0;
+    const int c_lo = (nch * part) / kEpiParts, c_hi = (nch * (part + 1)) / kEpiParts;
     // per-unit coordinates without integer division: exact float-reciprocal
     // quotients (every operand < 2^24), shifts for the 1/2-strided consumer
     const float rcp_hlwl = 1.0f / static_cast<float>(HlWl), rcp_wl = 1.0f / static_cast<float>(p.Wl);
@@ -884,7 +886,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
       const int k_base = nt * p.block_n;
       // FC checksum digits ride in the 16 columns after the tile's channels
       uint32_t dig[4] = {0u, 0u, 0u, 0u};
-      if (FC && half == 0) tmem_ld4(t_row + p.block_n, dig);
+      if (FC && part == 0) tmem_ld4(t_row + p.block_n, dig);
       // fast path: no fault hook, no filler channels, no IC column sums (warp-uniform)
       const bool slow = p.fault_key >= 0 || (p.check & CHECK_IC) || k_base + c_hi * 16 > p.K;
       Acc row_sum = 0;
@@ -908,10 +910,11 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
       if (FIC) fic_sum += row_sum;
       if (FC) {
         // combine the two column halves of each row
-        if (half == 1) s_rowsum[row] = acc_bits(row_sum);
-        named_bar(kBarQuarter0 + quarter, 64);
-        if (half == 0) {
-          row_sum += bits_acc<Acc>(s_rowsum[row]);
+        if (part > 0) s_rowsum[part - 1][row] = acc_bits(row_sum);
+        named_bar(kBarQuarter0 + quarter, 32 * kEpiParts);
+        if (part == 0) {
+#pragma unroll
+          for (int q = 0; q < kEpiParts - 1; ++q) row_sum += bits_acc<Acc>(s_rowsum[q][row]);
           Acc extra = 0;
           if (valid) {
             if constexpr (DT == DT_I8) {
@@ -956,7 +959,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
           }
         }
         // s_rowsum reuse guard for the next unit
-        named_bar(kBarQuarter0 + quarter, 64);
+        named_bar(kBarQuarter0 + quarter, 32 * kEpiParts);
       }
     }
     if (EPI == EPI_PACKED && DT == DT_I8 && p.af_ficw8) {
