@@ -145,7 +145,8 @@ struct abed_conv_plan {
   // right-hand side of an earlier run (fault campaigns: checksums come from
   // the pristine input, faults.hpp:111-115)
   int reuse_input_checksum = 0;
-  int last_rhs_mode = 0;        // rhs_mode of the last run (its verdict reduction needs it)
+  int last_rhs_mode = 0;
+  int last_grid = 0;            // CTAs of the last conv launch (records the verdict reduces)        // rhs_mode of the last run (its verdict reduction needs it)
   // FIC-AF: this layer's FIC rhs is accumulated by the previous layer's epilogue
   // (which is run with next = this plan); the verdict consumes and resets it
   int af_input = 0;

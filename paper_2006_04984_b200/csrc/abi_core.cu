@@ -98,7 +98,10 @@ void plan_init_common(abed_conv_plan* pl, const abed_layer_shape& shape, int che
     cuda_check(cudaMalloc(&pl->d_tile_sem, (size_t)p.m_tiles * 4), "cudaMalloc(tile_sem)");
     cuda_check(cudaMemset(pl->d_tile_sem, 0, (size_t)p.m_tiles * 4), "memset tile_sem");
   }
-  cuda_check(cudaMalloc(&pl->d_cta_rec, (size_t)conv_tc_grid(p, num_sms()) * abed_dev::kCtaRec * 8), "cudaMalloc(cta_rec)");
+  // one record per CTA of any launch (conv CTAs + input-checksum CTAs <= SMs)
+  cuda_check(cudaMalloc(&pl->d_cta_rec, (size_t)std::max(num_sms(), conv_tc_grid(p, num_sms())) * abed_dev::kCtaRec * 8),
+             "cudaMalloc(cta_rec)");
+  pl->last_grid = conv_tc_grid(p, num_sms());
   cuda_check(cudaMalloc(&pl->d_kacc, 4 * 8), "cudaMalloc(kacc)");
   cuda_check(cudaMemset(pl->d_kacc, 0, 4 * 8), "memset kacc");
   cuda_check(cudaMalloc(&pl->d_outcome, 3 * sizeof(abed_verify_outcome)), "cudaMalloc(outcome)");
@@ -320,15 +323,29 @@ void plan_run(abed_conv_plan* pl, const int8_t* packed, const abed_epilog_params
   if (pl->checks & ABED_CHECK_IC) cuda_check(cudaMemsetAsync(pl->d_acc + 4, 0, pl->shape.k * 8, st), "memset ic");
   if (out_mode == ABED_OUT_I8_COMPARE) cuda_check(cudaMemsetAsync(pl->d_acc + 1, 0, 8, st), "memset cmp");
   p.rhs_mode = 0;
+  p.conv_grid = conv_tc_grid(p, num_sms());
+  p.ic_ctas = 0;
+  // FR input checksum: a conv grid that leaves SMs idle gets extra CTAs there
+  // that do the whole checksum with all their warps; otherwise the conv CTAs'
+  // input-checksum warps do it.  Returns the image split of the work items.
+  auto fr_split = [&](const ActGeom& g) {
+    const int idle = num_sms() - p.conv_grid;
+    int64_t want;
+    if (idle >= 8) {
+      p.ic_ctas = idle;
+      want = 2LL * idle * abed_dev::kConvThreads_host;
+    } else {
+      want = 2LL * p.conv_grid * 64;
+    }
+    const int64_t cells = (int64_t)g.n_phase * g.c16 * g.Hl * g.Wl;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(g.n, (want + cells - 1) / cells));
+  };
   if (!fmode && pl->af_input && (pl->checks & ABED_CHECK_FIC) && !pl->reuse_input_checksum) {
     p.rhs_mode = 2;  // FIC-AF: the producer's epilogue supplies the rhs
   } else if (fmode && (pl->checks & ABED_CHECK_FIC) && !pl->reuse_input_checksum) {
     // float mode: the input-checksum warps compute rhs = sum x * G in-kernel
-    const ActGeom& g = pl->g;
-    const int64_t cells = (int64_t)g.n_phase * g.c16 * g.Hl * g.Wl;
-    const int64_t want = 2LL * conv_tc_grid(p, num_sms()) * 64;
     p.rhs_mode = 1;
-    p.rhs_nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(g.n, (want + cells - 1) / cells));
+    p.rhs_nsplit = fr_split(pl->g);
   } else if (!fmode && (pl->checks & (ABED_CHECK_FIC | ABED_CHECK_IC)) && !pl->reuse_input_checksum) {
     // input checksum of the pristine input (FR option)
     const ActGeom& g = pl->g;
@@ -355,8 +372,7 @@ void plan_run(abed_conv_plan* pl, const int8_t* packed, const abed_epilog_params
         // FIC only: rhs = sum x * G computed by the conv kernel's input-checksum
         // warps from their own read of the stored input
         p.rhs_mode = 1;
-        const int64_t want = 2LL * conv_tc_grid(p, num_sms()) * 64;
-        p.rhs_nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(g.n, (want + cells - 1) / cells));
+        p.rhs_nsplit = fr_split(g);
       } else {
         // |G| too large for the 3-digit map: one separate pass ahead of the conv
         cuda_check(cudaMemsetAsync(pl->d_acc, 0, 8, st), "memset rhs");
@@ -367,13 +383,14 @@ void plan_run(abed_conv_plan* pl, const int8_t* packed, const abed_epilog_params
     }
   }
   pl->last_rhs_mode = p.rhs_mode;
+  pl->last_grid = p.conv_grid + p.ic_ctas;
   cuda_check(conv_tc_launch(p, num_sms(), pl->pdl != 0, st), "conv_i8_tc launch");
 }
 
 abed_dev::VerdictJob plan_verdict_job(const abed_conv_plan* pl, abed_verify_outcome* out_dev) {
   abed_dev::VerdictJob j{};
   j.rec = pl->d_cta_rec;
-  j.grid = pl->dw ? dw_grid() : conv_tc_grid(pl->base, num_sms());
+  j.grid = pl->dw ? dw_grid() : pl->last_grid;
   j.P = pl->g.p;
   j.Q = pl->g.q;
   j.dtype = pl->dtype;

@@ -167,8 +167,13 @@ cudaError_t verdict_launch(const abed_dev::VerdictJob* jobs, int n, cudaStream_t
   return cudaSuccess;
 }
 
-cudaError_t conv_tc_launch(const ConvTcParams& p, int num_sms, bool pdl, cudaStream_t stream) {
-  const int grid = conv_tc_grid(p, num_sms);
+cudaError_t conv_tc_launch(const ConvTcParams& p_in, int num_sms, bool pdl, cudaStream_t stream) {
+  ConvTcParams p = p_in;
+  if (p.conv_grid <= 0) {
+    p.conv_grid = conv_tc_grid(p, num_sms);
+    p.ic_ctas = 0;
+  }
+  const int grid = p.conv_grid + p.ic_ctas;
   switch (p.dtype) {
     case abed_dev::DT_F16: return launch_dt<abed_dev::DT_F16>(p, grid, pdl, stream);
     case abed_dev::DT_BF16: return launch_dt<abed_dev::DT_BF16>(p, grid, pdl, stream);

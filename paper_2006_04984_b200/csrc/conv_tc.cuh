@@ -28,6 +28,9 @@ constexpr int kMaxTaps = 64;
 constexpr int kBlockM = 128;
 constexpr int kStages = 4;       // activation/filter stage ring depth
 constexpr int kStages_host = kStages;
+// conv kernel CTA size: producer + MMA warps, 8 epilogue warps, 2 input-checksum
+// warps (conv_tc_kernel.cuh kConvThreads)
+constexpr int kConvThreads_host = 64 + 8 * 32 + 2 * 32;
 // dynamic smem cap for the conv kernel: 227 KB minus its static smem (bias, reductions)
 constexpr int kConvDynSmemMax = 232448 - 12288;
 
@@ -112,6 +115,10 @@ struct ConvTcParams {
                                // 2: AF -- the previous layer's epilogue produced it (af accumulator),
                                // 3: SM -- input-checksum warps read the staged A tiles (no re-read)
   int rhs_nsplit;              // image split of the rhs work items
+  int conv_grid;               // CTAs running conv work units (blockIdx < conv_grid)
+  int ic_ctas;                 // extra CTAs (blockIdx >= conv_grid) that only compute the FR
+                               // input checksum on SMs the conv grid leaves idle (0: the conv
+                               // CTAs' input-checksum warps do it)
   const int8_t* ficw8;         // FIC weight map G as balanced base-256 digits
                                // [phase][c16][Hl*Wl][3 digits][16 channels] (|G| < 2^23)
   // rhs_mode 3 (FIC-SM): the input-checksum warps take x from the A stages the

@@ -46,6 +46,7 @@ constexpr int kEpiParts = kEpiWarps / 4;  // epilogue warps per TMEM lane quarte
 constexpr int kEpiThreads = kEpiWarps * 32;
 constexpr int kRhsWarps = 2;
 constexpr int kConvThreads = 64 + kEpiThreads + kRhsWarps * 32;
+static_assert(kConvThreads == kConvThreads_host, "host copy of the conv CTA size");
 constexpr int kBiasSmem = 2048;
 constexpr int kBarEpi = 1;       // named barrier: all epilogue warps
 constexpr int kBarHalf0 = 2;     // named barrier: the four part-0 epilogue warps
@@ -83,9 +84,9 @@ __device__ __forceinline__ void decode_tile(const ConvTcParams& p, int tile_seq,
   // b_resident with several N tiles: each CTA owns one N tile (blockIdx % n_tiles)
   if (p.b_resident) {
     nt = blockIdx.x % p.n_tiles;
-    mt = blockIdx.x / p.n_tiles + tile_seq * (gridDim.x / p.n_tiles);
+    mt = blockIdx.x / p.n_tiles + tile_seq * (p.conv_grid / p.n_tiles);
   } else {
-    const int t = blockIdx.x + tile_seq * gridDim.x;
+    const int t = blockIdx.x + tile_seq * p.conv_grid;
     mt = t / p.n_tiles;
     nt = t % p.n_tiles;
   }
@@ -103,6 +104,25 @@ __device__ __forceinline__ int32_t requant_i8(int32_t acc, float scale, float bi
   }
   v = fminf(127.0f, fmaxf(-128.0f, v));
   return __float2int_rz(v);
+}
+
+// requant_i8 with ReLU for two accumulators at once: one FFMA2 (fma.rn.f32x2 =
+// two IEEE fmas, bit-identical to __fmaf_rn), one FADD2.RZ putting trunc(v) in
+// the mantissa of 2^23 + v, and the clamp to [0, 127] done on the float's bit
+// pattern with one DPX add-min-relu per value (positive floats order like their
+// bits; v < 0 gives a pattern below 2^23's, v >= 127 one above 2^23 + 127, and
+// every v in [0, 2^23) lands exactly on 2^23 + trunc(v)).
+__device__ __forceinline__ void requant_relu_pair(int32_t a0, int32_t a1, float scale, float b0, float b1, int32_t& y0,
+                                                  int32_t& y1) {
+  const uint64_t v = (static_cast<uint64_t>(__float_as_uint(static_cast<float>(a1))) << 32) |
+                     __float_as_uint(static_cast<float>(a0));
+  const uint64_t sc = (static_cast<uint64_t>(__float_as_uint(scale)) << 32) | __float_as_uint(scale);
+  const uint64_t bb = (static_cast<uint64_t>(__float_as_uint(b1)) << 32) | __float_as_uint(b0);
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(v), "l"(sc), "l"(bb));
+  asm("add.rz.f32x2 %0, %1, %2;" : "=l"(r) : "l"(r), "l"(0x4B0000004B000000ull));
+  y0 = __viaddmin_s32_relu(static_cast<int>(static_cast<uint32_t>(r)), -0x4B000000, 127);
+  y1 = __viaddmin_s32_relu(static_cast<int>(static_cast<uint32_t>(r >> 32)), -0x4B000000, 127);
 }
 
 __device__ __forceinline__ uint32_t pack4(int32_t a, int32_t b, int32_t c, int32_t d) {
@@ -262,9 +282,12 @@ __device__ __forceinline__ int64_t epi_chunk(const ConvTcParams& p, const EpiCtx
     if (p.dbg & 16) {  // timing experiment: skip the requantise math
 #pragma unroll
       for (int j = 0; j < 16; ++j) y[j] = a[j];
+    } else if (RELU) {
+#pragma unroll
+      for (int j = 0; j < 16; j += 2) requant_relu_pair(a[j], a[j + 1], p.scale, b[j], b[j + 1], y[j], y[j + 1]);
     } else {
 #pragma unroll
-      for (int j = 0; j < 16; ++j) y[j] = requant_i8(a[j], p.scale, b[j], RELU ? 1 : 0);
+      for (int j = 0; j < 16; ++j) y[j] = requant_i8(a[j], p.scale, b[j], 0);
     }
     if (SLOW) {
 #pragma unroll
@@ -601,6 +624,98 @@ __device__ __forceinline__ void mma_warp_run(const ConvTcParams& p, const MmaEnv
   }
 }
 
+// FIC rhs, FR option: sum over the stored input of x * G (checksum.hpp:248-285
+// gen_input_checksum + fic_dot restated as one pass), work items
+// first, first + stride, ... of (plane, pixel, image split).  int8: G as three
+// balanced base-256 digit planes, 12 dp4a per 16-byte chunk, every image load of
+// an item issued before use.  float mode: G in f32, f32 FMAs per item, f64 across
+// items (input_checksum_f64 / fic_dot_f64, checksum.hpp:496-535).  Run by the conv
+// CTAs' input-checksum warps, or by all warps of the extra input-checksum CTAs
+// that fill the SMs a small conv grid leaves idle.
+template <int DT>
+__device__ __forceinline__ void fic_rhs_fr(const ConvTcParams& p, int64_t first, int64_t stride, long long& acc,
+                                           double& facc_rhs) {
+  if constexpr (DT != DT_I8) {
+    const int64_t HlWl = static_cast<int64_t>(p.Hl) * p.Wl;
+    const int nsplit = p.rhs_nsplit;
+    const int64_t total = static_cast<int64_t>(p.n_phase) * p.c16 * HlWl * nsplit;
+    for (int64_t idx = first; idx < total; idx += stride) {
+      const int64_t pix = idx % HlWl;
+      const int64_t rest = idx / HlWl;
+      const int split = static_cast<int>(rest % nsplit);
+      const int64_t plane = rest / nsplit;
+      const float4* gw = reinterpret_cast<const float4*>(p.ficwf) + (plane * HlWl + pix) * 2;
+      const float4 ga = __ldg(gw), gb = __ldg(gw + 1);
+      const uint4* src = reinterpret_cast<const uint4*>(p.act) + plane * p.plane_len + pix;
+      const int n0 = static_cast<int>(static_cast<int64_t>(p.N) * split / nsplit);
+      const int n1 = static_cast<int>(static_cast<int64_t>(p.N) * (split + 1) / nsplit);
+      float item = 0.0f;
+      for (int n = n0; n < n1; n += 4) {
+        uint4 x[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          x[j] = n + j < n1 ? __ldcg(src + static_cast<int64_t>(n + j) * HlWl) : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float2 x0 = unpack_h2<DT>(x[j].x), x1 = unpack_h2<DT>(x[j].y), x2 = unpack_h2<DT>(x[j].z),
+                       x3 = unpack_h2<DT>(x[j].w);
+          item = __fmaf_rn(x0.x, ga.x, item);
+          item = __fmaf_rn(x0.y, ga.y, item);
+          item = __fmaf_rn(x1.x, ga.z, item);
+          item = __fmaf_rn(x1.y, ga.w, item);
+          item = __fmaf_rn(x2.x, gb.x, item);
+          item = __fmaf_rn(x2.y, gb.y, item);
+          item = __fmaf_rn(x3.x, gb.z, item);
+          item = __fmaf_rn(x3.y, gb.w, item);
+        }
+      }
+      facc_rhs += static_cast<double>(item);
+    }
+  } else {
+    const int64_t HlWl = static_cast<int64_t>(p.Hl) * p.Wl;
+    const int nsplit = p.rhs_nsplit;
+    const int64_t total = static_cast<int64_t>(p.n_phase) * p.c16 * HlWl * nsplit;
+    for (int64_t idx = first; idx < total; idx += stride) {
+      const int64_t pix = idx % HlWl;
+      const int64_t rest = idx / HlWl;
+      const int split = static_cast<int>(rest % nsplit);
+      const int64_t plane = rest / nsplit;
+      const uint4* gw = reinterpret_cast<const uint4*>(p.ficw8) + (plane * HlWl + pix) * 3;
+      const uint4 g0 = __ldg(gw), g1 = __ldg(gw + 1), g2 = __ldg(gw + 2);
+      const uint4* src = reinterpret_cast<const uint4*>(p.act) + plane * p.plane_len + pix;
+      const int n0 = static_cast<int>(static_cast<int64_t>(p.N) * split / nsplit);
+      const int n1 = static_cast<int>(static_cast<int64_t>(p.N) * (split + 1) / nsplit);
+      int32_t d0 = 0, d1 = 0, d2 = 0;  // |sum| <= 32 images * 16 * 128 * 128 < 2^31
+      for (int n = n0; n < n1; n += 8) {
+        uint4 x[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          x[j] = n + j < n1 ? __ldcg(src + static_cast<int64_t>(n + j) * HlWl) : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          d0 = __dp4a(static_cast<int>(x[j].x), static_cast<int>(g0.x), d0);
+          d0 = __dp4a(static_cast<int>(x[j].y), static_cast<int>(g0.y), d0);
+          d0 = __dp4a(static_cast<int>(x[j].z), static_cast<int>(g0.z), d0);
+          d0 = __dp4a(static_cast<int>(x[j].w), static_cast<int>(g0.w), d0);
+          d1 = __dp4a(static_cast<int>(x[j].x), static_cast<int>(g1.x), d1);
+          d1 = __dp4a(static_cast<int>(x[j].y), static_cast<int>(g1.y), d1);
+          d1 = __dp4a(static_cast<int>(x[j].z), static_cast<int>(g1.z), d1);
+          d1 = __dp4a(static_cast<int>(x[j].w), static_cast<int>(g1.w), d1);
+          d2 = __dp4a(static_cast<int>(x[j].x), static_cast<int>(g2.x), d2);
+          d2 = __dp4a(static_cast<int>(x[j].y), static_cast<int>(g2.y), d2);
+          d2 = __dp4a(static_cast<int>(x[j].z), static_cast<int>(g2.z), d2);
+          d2 = __dp4a(static_cast<int>(x[j].w), static_cast<int>(g2.w), d2);
+        }
+        if (((n - n0) & 31) == 24) {  // keep the digit sums inside int32
+          acc += static_cast<long long>(d0) + (static_cast<long long>(d1) << 8) + (static_cast<long long>(d2) << 16);
+          d0 = d1 = d2 = 0;
+        }
+      }
+      acc += static_cast<long long>(d0) + (static_cast<long long>(d1) << 8) + (static_cast<long long>(d2) << 16);
+    }
+  }
+}
+
 // pattern ids (host: mma_pattern_of in plan.cu)
 enum MmaPattern : int {
   PAT_GENERIC = 0,
@@ -633,6 +748,39 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
   // role branches convergent and the MMA descriptors in uniform registers
   const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
   const int lane = threadIdx.x & 31;
+
+  if (static_cast<int>(blockIdx.x) >= p.conv_grid) {
+    // ------------------------------------------------ input-checksum CTA
+    // an SM the conv grid leaves idle: every warp works on the FR input checksum
+    pdl_launch_dependents();
+    long long acc = 0;
+    double facc_rhs = 0.0;
+    pdl_wait();
+    if (FIC && p.rhs_mode == 1)
+      fic_rhs_fr<DT>(p, static_cast<int64_t>(blockIdx.x - p.conv_grid) * kConvThreads + threadIdx.x,
+                     static_cast<int64_t>(p.ic_ctas) * kConvThreads, acc, facc_rhs);
+    __shared__ long long s_ic[kConvThreads / 32];
+    if (FIC) {
+      const long long w = DT == DT_I8 ? warp_sum(acc) : __double_as_longlong(warp_sum_d(facc_rhs));
+      if (lane == 0) s_ic[warp] = w;
+    }
+    __syncthreads();
+    if ((FC || FIC) && threadIdx.x == 0) {
+      int64_t* rec = p.cta_rec + static_cast<int64_t>(blockIdx.x) * kCtaRec;
+      rec[0] = 0;       // no FC rows here
+      rec[1] = kNoKey;
+      rec[2] = rec[3] = 0;
+      long long r = 0;
+      double rf = 0.0;
+      for (int w = 0; w < kConvThreads / 32; ++w) {
+        r += s_ic[w];
+        rf += __longlong_as_double(s_ic[w]);
+      }
+      rec[4] = DT == DT_I8 ? 0ll : __double_as_longlong(0.0);
+      rec[5] = DT == DT_I8 ? r : __double_as_longlong(rf);
+    }
+    return;
+  }
   int64_t* const trace = p.trace ? p.trace + static_cast<int64_t>(blockIdx.x) * kTraceSlots : nullptr;
   const long long t_entry = clock64();
   if (trace && threadIdx.x == 0) {
@@ -675,12 +823,12 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
   // number of work units for this CTA
   int n_units;
   if (p.b_resident) {
-    const int per = gridDim.x / p.n_tiles;
+    const int per = p.conv_grid / p.n_tiles;
     const int mt0 = blockIdx.x / p.n_tiles;
     n_units = (static_cast<int>(blockIdx.x) < per * p.n_tiles && mt0 < p.m_tiles) ? (p.m_tiles - mt0 + per - 1) / per : 0;
   } else {
     const int total = p.m_tiles * p.n_tiles;
-    n_units = static_cast<int>(blockIdx.x) < total ? (total - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    n_units = static_cast<int>(blockIdx.x) < total ? (total - blockIdx.x + p.conv_grid - 1) / p.conv_grid : 0;
   }
 
   if (warp == 0) {
@@ -996,48 +1144,10 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
     const int rw = warp - (2 + kEpiWarps);
     long long acc = 0;
     double facc_rhs = 0.0;
-    if (DT != DT_I8 && FIC && p.rhs_mode == 1) {
-      // float mode: G in f32 [plane][pix][8]; 8 fp16/bf16 values per 16-byte
-      // chunk, f32 FMAs per work item, f64 across items (reduce in double like
-      // input_checksum_f64 / fic_dot_f64, checksum.hpp:496-535)
+    if (DT != DT_I8 && FIC && p.rhs_mode == 1 && p.ic_ctas == 0) {
       pdl_wait();
-      const int64_t HlWl = static_cast<int64_t>(p.Hl) * p.Wl;
-      const int nsplit = p.rhs_nsplit;
-      const int64_t total = static_cast<int64_t>(p.n_phase) * p.c16 * HlWl * nsplit;
-      const int64_t stride = static_cast<int64_t>(gridDim.x) * (kRhsWarps * 32);
-      for (int64_t idx = static_cast<int64_t>(blockIdx.x) * (kRhsWarps * 32) + rw * 32 + lane; idx < total;
-           idx += stride) {
-        const int64_t pix = idx % HlWl;
-        const int64_t rest = idx / HlWl;
-        const int split = static_cast<int>(rest % nsplit);
-        const int64_t plane = rest / nsplit;
-        const float4* gw = reinterpret_cast<const float4*>(p.ficwf) + (plane * HlWl + pix) * 2;
-        const float4 ga = __ldg(gw), gb = __ldg(gw + 1);
-        const uint4* src = reinterpret_cast<const uint4*>(p.act) + plane * p.plane_len + pix;
-        const int n0 = static_cast<int>(static_cast<int64_t>(p.N) * split / nsplit);
-        const int n1 = static_cast<int>(static_cast<int64_t>(p.N) * (split + 1) / nsplit);
-        float item = 0.0f;
-        for (int n = n0; n < n1; n += 4) {
-          uint4 x[4];
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            x[j] = n + j < n1 ? __ldcg(src + static_cast<int64_t>(n + j) * HlWl) : make_uint4(0u, 0u, 0u, 0u);
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const float2 x0 = unpack_h2<DT>(x[j].x), x1 = unpack_h2<DT>(x[j].y), x2 = unpack_h2<DT>(x[j].z),
-                         x3 = unpack_h2<DT>(x[j].w);
-            item = __fmaf_rn(x0.x, ga.x, item);
-            item = __fmaf_rn(x0.y, ga.y, item);
-            item = __fmaf_rn(x1.x, ga.z, item);
-            item = __fmaf_rn(x1.y, ga.w, item);
-            item = __fmaf_rn(x2.x, gb.x, item);
-            item = __fmaf_rn(x2.y, gb.y, item);
-            item = __fmaf_rn(x3.x, gb.z, item);
-            item = __fmaf_rn(x3.y, gb.w, item);
-          }
-        }
-        facc_rhs += static_cast<double>(item);
-      }
+      fic_rhs_fr<DT>(p, static_cast<int64_t>(blockIdx.x) * (kRhsWarps * 32) + rw * 32 + lane,
+                     static_cast<int64_t>(p.conv_grid) * (kRhsWarps * 32), acc, facc_rhs);
     } else if (rhs_staged) {
       // FIC-SM: the same sum x * G, with x taken from the A stages the producer
       // staged for the MMAs.  M tile mt owns plane pixels [m0, m0 + 128) of every
@@ -1147,51 +1257,10 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
           }
         }
       }
-    } else if (DT == DT_I8 && FIC && p.rhs_mode == 1) {
+    } else if (DT == DT_I8 && FIC && p.rhs_mode == 1 && p.ic_ctas == 0) {
       pdl_wait();
-      const int64_t HlWl = static_cast<int64_t>(p.Hl) * p.Wl;
-      const int nsplit = p.rhs_nsplit;
-      const int64_t total = static_cast<int64_t>(p.n_phase) * p.c16 * HlWl * nsplit;
-      const int64_t stride = static_cast<int64_t>(gridDim.x) * (kRhsWarps * 32);
-      for (int64_t idx = static_cast<int64_t>(blockIdx.x) * (kRhsWarps * 32) + rw * 32 + lane; idx < total;
-           idx += stride) {
-        const int64_t pix = idx % HlWl;
-        const int64_t rest = idx / HlWl;
-        const int split = static_cast<int>(rest % nsplit);
-        const int64_t plane = rest / nsplit;
-        const uint4* gw = reinterpret_cast<const uint4*>(p.ficw8) + (plane * HlWl + pix) * 3;
-        const uint4 g0 = __ldg(gw), g1 = __ldg(gw + 1), g2 = __ldg(gw + 2);
-        const uint4* src = reinterpret_cast<const uint4*>(p.act) + plane * p.plane_len + pix;
-        const int n0 = static_cast<int>(static_cast<int64_t>(p.N) * split / nsplit);
-        const int n1 = static_cast<int>(static_cast<int64_t>(p.N) * (split + 1) / nsplit);
-        int32_t d0 = 0, d1 = 0, d2 = 0;  // |sum| <= 32 images * 16 * 128 * 128 < 2^31
-        for (int n = n0; n < n1; n += 8) {
-          uint4 x[8];
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-            x[j] = n + j < n1 ? __ldcg(src + static_cast<int64_t>(n + j) * HlWl) : make_uint4(0u, 0u, 0u, 0u);
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            d0 = __dp4a(static_cast<int>(x[j].x), static_cast<int>(g0.x), d0);
-            d0 = __dp4a(static_cast<int>(x[j].y), static_cast<int>(g0.y), d0);
-            d0 = __dp4a(static_cast<int>(x[j].z), static_cast<int>(g0.z), d0);
-            d0 = __dp4a(static_cast<int>(x[j].w), static_cast<int>(g0.w), d0);
-            d1 = __dp4a(static_cast<int>(x[j].x), static_cast<int>(g1.x), d1);
-            d1 = __dp4a(static_cast<int>(x[j].y), static_cast<int>(g1.y), d1);
-            d1 = __dp4a(static_cast<int>(x[j].z), static_cast<int>(g1.z), d1);
-            d1 = __dp4a(static_cast<int>(x[j].w), static_cast<int>(g1.w), d1);
-            d2 = __dp4a(static_cast<int>(x[j].x), static_cast<int>(g2.x), d2);
-            d2 = __dp4a(static_cast<int>(x[j].y), static_cast<int>(g2.y), d2);
-            d2 = __dp4a(static_cast<int>(x[j].z), static_cast<int>(g2.z), d2);
-            d2 = __dp4a(static_cast<int>(x[j].w), static_cast<int>(g2.w), d2);
-          }
-          if (((n - n0) & 31) == 24) {  // keep the digit sums inside int32
-            acc += static_cast<long long>(d0) + (static_cast<long long>(d1) << 8) + (static_cast<long long>(d2) << 16);
-            d0 = d1 = d2 = 0;
-          }
-        }
-        acc += static_cast<long long>(d0) + (static_cast<long long>(d1) << 8) + (static_cast<long long>(d2) << 16);
-      }
+      fic_rhs_fr<DT>(p, static_cast<int64_t>(blockIdx.x) * (kRhsWarps * 32) + rw * 32 + lane,
+                     static_cast<int64_t>(p.conv_grid) * (kRhsWarps * 32), acc, facc_rhs);
     } else {
       pdl_wait();
     }
