@@ -49,7 +49,6 @@ int num_sms();
 __global__ void pack_input_kernel(const int8_t* x, abed_dev::ActGeom g, int8_t* out);
 __global__ void pack_filters_kernel(const int8_t* f, abed_dev::ActGeom g, int block_n, int block_n_tot,
                                     int n_tiles, int gps, int k_stages, int fc, int8_t* out);
-__global__ void filter_sum_kernel(const int8_t* f, int64_t K, int64_t crs, int32_t* sums);
 __global__ void batch_sum_packed_kernel(const int8_t* act, abed_dev::ActGeom g, int32_t* bsum);
 __global__ void box_sum_dot_kernel(const int32_t* bsum, abed_dev::ActGeom g, const int32_t* fsum,
                                    int32_t* ic_out, unsigned long long* fic_rhs);
@@ -105,6 +104,8 @@ void plan_finalize(abed_conv_plan* pl, abed_verify_outcome* out_dev, cudaStream_
 abed_dev::VerdictJob plan_verdict_job(const abed_conv_plan* pl, abed_verify_outcome* out_dev);
 // ref_kernels.cu
 void dev_gen_input_checksum(const int8_t* x, const abed_layer_shape& s, int32_t* sums, cudaStream_t st);
+// column sums of a rows x len int8 matrix (filter checksum, batch checksum image)
+void dev_colsum_i8(const int8_t* x, int64_t rows, int64_t len, int32_t* out, cudaStream_t st);
 void dev_epilog(const int32_t* in, abed_dims4 d, const abed_epilog_params* p, void* out, cudaStream_t st);
 }  // namespace abed_host
 

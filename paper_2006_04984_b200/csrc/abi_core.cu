@@ -226,8 +226,7 @@ abed_conv_plan* plan_create(const abed_layer_shape& shape, const int8_t* filters
     pack_filters_kernel<<<grid_for(rows), 256>>>(filters, g, p.block_n, p.block_n_tot, p.n_tiles, p.gps,
                                                  p.k_stages, (checks & ABED_CHECK_FC) ? 1 : 0, pl->d_wpk);
     cuda_check(cudaGetLastError(), "pack_filters");
-    filter_sum_kernel<<<grid_for(crs), 256>>>(filters, shape.k, crs, pl->d_fsum);
-    cuda_check(cudaGetLastError(), "filter_sum");
+    dev_colsum_i8(filters, shape.k, crs, pl->d_fsum, nullptr);  // gen_filter_checksum (offline)
     if (checks & ABED_CHECK_FIC) {
       const int64_t nw = (int64_t)g.n_phase * g.c16 * 16 * g.Hl * g.Wl;
       cuda_check(cudaMalloc(&pl->d_ficw, nw * 4), "cudaMalloc(ficw)");

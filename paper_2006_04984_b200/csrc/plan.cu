@@ -148,14 +148,6 @@ __global__ void pack_filters_kernel(const int8_t* __restrict__ f, ActGeom g, int
 }
 
 // filter checksum in reference (c,r,s) order, i32 (checksum.hpp:75-90)
-__global__ void filter_sum_kernel(const int8_t* __restrict__ f, int64_t K, int64_t crs, int32_t* __restrict__ sums) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < crs; i += (int64_t)gridDim.x * blockDim.x) {
-    int32_t acc = 0;
-    for (int64_t k = 0; k < K; ++k) acc += f[k * crs + i];
-    sums[i] = acc;
-  }
-}
-
 // ---------------------------------------------------------------------------
 // Input checksum of the packed input.  Stage 1 (HBM-bound, reads the input
 // once): batch sum B[phase][c][i][j] = sum_n plane[(n*Hl+i)*Wl+j] (this is the

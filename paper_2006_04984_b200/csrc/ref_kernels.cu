@@ -114,6 +114,53 @@ __global__ void epilog_kernel(const int32_t* __restrict__ in, abed_dims4 d, floa
   }
 }
 
+// The same epilog on 16 consecutive outputs per thread (P*Q % 16 == 0, aligned
+// buffers): one channel per vector, 64-byte loads, 16-byte (i8) or 64-byte (f32)
+// stores -- HBM-bound, so the vector width is what sets the achieved bandwidth.
+__device__ __forceinline__ float epilog_one(int32_t a, float scale, float b, int relu) {
+  float v = __fmaf_rn(static_cast<float>(a), scale, b);
+  if (relu && v < 0.0f) v = 0.0f;
+  return v;
+}
+__global__ void __launch_bounds__(256) epilog_v16_kernel(const int32_t* __restrict__ in, abed_dims4 d, float scale,
+                                                         const float* __restrict__ bias, int relu, int f32out,
+                                                         void* __restrict__ out) {
+  const int64_t total16 = d.d0 * d.d1 * d.d2 * d.d3 / 16, pq16 = d.d2 * d.d3 / 16;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total16; i += (int64_t)gridDim.x * blockDim.x) {
+    const float b = __ldg(bias + (i / pq16) % d.d1);
+    const int4* src = reinterpret_cast<const int4*>(in) + i * 4;
+    int4 a[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) a[u] = __ldcs(src + u);
+    float v[16];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      v[4 * u] = epilog_one(a[u].x, scale, b, relu);
+      v[4 * u + 1] = epilog_one(a[u].y, scale, b, relu);
+      v[4 * u + 2] = epilog_one(a[u].z, scale, b, relu);
+      v[4 * u + 3] = epilog_one(a[u].w, scale, b, relu);
+    }
+    if (f32out) {
+      float4* dst = reinterpret_cast<float4*>(out) + i * 4;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) dst[u] = make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
+    } else {
+      uint32_t w[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        uint32_t acc = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int32_t q = static_cast<int32_t>(truncf(fminf(127.0f, fmaxf(-128.0f, v[4 * u + j]))));
+          acc |= (static_cast<uint32_t>(q) & 0xFFu) << (8 * j);
+        }
+        w[u] = acc;
+      }
+      reinterpret_cast<uint4*>(out)[i] = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+  }
+}
+
 // ---------------------------------------------------------- checksum kernels
 __global__ void decompose_kernel(const int32_t* __restrict__ sums, int64_t n, int8_t* __restrict__ planes) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -125,14 +172,102 @@ __global__ void recombine_kernel(const int32_t* __restrict__ e, int64_t n, int64
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     out[i] = (int64_t)e[i] + ((int64_t)e[n + i] << 8) + ((int64_t)e[2 * n + i] << 16) + ((int64_t)e[3 * n + i] << 24);
 }
-__global__ void batch_sum_nchw_kernel(const int8_t* __restrict__ x, abed_dims4 d, int32_t* __restrict__ out) {
-  const int64_t chw = d.d1 * d.d2 * d.d3;  // checksum.hpp:350-362
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < chw; i += (int64_t)gridDim.x * blockDim.x) {
-    int32_t acc = 0;
-    for (int64_t n = 0; n < d.d0; ++n) acc += x[n * chw + i];
-    out[i] = acc;
+// Column sums of a rows x len int8 matrix into int32 -- the shape of both
+// gen_filter_checksum (rows = K filters of len = C*R*S, checksum.hpp:75-90) and
+// ic_batch_checksum (rows = N images of len = C*H*W, :350-362).  HBM-bound.  A
+// block owns 512 adjacent columns (32 lanes x one 16-byte vector) of a range of
+// rows; its 8 warps stride the rows (each warp load is 512 contiguous bytes, four
+// rows in flight per thread), reduce through shared memory, and write each column
+// once -- with an integer atomic only when several blocks split the rows (exact
+// and deterministic either way).  `out` must be zeroed when row_splits > 1.
+constexpr int kColsumWarps = 8;
+__global__ void __launch_bounds__(kColsumWarps * 32) colsum_i8_v16_kernel(const int8_t* __restrict__ x, int64_t rows,
+                                                                        int64_t len, int64_t rows_per,
+                                                                        int32_t* __restrict__ out) {
+  __shared__ int32_t red[kColsumWarps][16][32];  // [warp][column in vector][lane]: conflict-free
+  const int64_t cols16 = len >> 4;
+  const int64_t col_tiles = (cols16 + 31) / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t tile = blockIdx.x % col_tiles, split = blockIdx.x / col_tiles;
+  const int64_t c16 = tile * 32 + lane;
+  const int64_t r0 = split * rows_per, r1 = r0 + rows_per < rows ? r0 + rows_per : rows;
+  int32_t acc[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) acc[j] = 0;
+  if (c16 < cols16) {
+    // SIMD byte sums: x ^ 0x80 is x + 128 as an unsigned byte; bytes 0/2 and 1/3
+    // of each word accumulate in the two 16-bit halves of one register (LOP3 +
+    // SHF + LOP3 + 2 IADD per 4 bytes), flushed to int32 every 256 rows (255 x 256
+    // < 2^16) and un-biased by 128 x rows at the end
+    const uint4* base = reinterpret_cast<const uint4*>(x) + c16;
+    int64_t nrows = 0;
+    int64_t r = r0 + warp;
+    while (r < r1) {
+      uint32_t ev[4] = {0u, 0u, 0u, 0u}, od[4] = {0u, 0u, 0u, 0u};
+      for (int it = 0; it < 32 && r < r1; ++it, r += 8 * kColsumWarps) {  // <= 256 rows, eight in flight
+        uint4 v[8];
+        bool ok[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          ok[u] = r + u * kColsumWarps < r1;
+          v[u] = ok[u] ? __ldcs(base + (r + u * kColsumWarps) * cols16) : make_uint4(0x80808080u, 0x80808080u,
+                                                                                      0x80808080u, 0x80808080u);
+          nrows += ok[u] ? 1 : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const uint32_t w[4] = {v[u].x ^ 0x80808080u, v[u].y ^ 0x80808080u, v[u].z ^ 0x80808080u,
+                                 v[u].w ^ 0x80808080u};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            ev[q] += w[q] & 0x00FF00FFu;
+            od[q] += (w[q] >> 8) & 0x00FF00FFu;
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        acc[4 * q] += static_cast<int32_t>(ev[q] & 0xFFFFu);
+        acc[4 * q + 1] += static_cast<int32_t>(od[q] & 0xFFFFu);
+        acc[4 * q + 2] += static_cast<int32_t>(ev[q] >> 16);
+        acc[4 * q + 3] += static_cast<int32_t>(od[q] >> 16);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) acc[j] -= static_cast<int32_t>(128 * nrows);
+  }
+#pragma unroll
+  for (int j = 0; j < 16; ++j) red[warp][j][lane] = acc[j];
+  __syncthreads();
+  const bool split_rows = rows_per < rows;
+  for (int e = threadIdx.x; e < 32 * 16; e += kColsumWarps * 32) {
+    const int j = e >> 5, ln = e & 31;
+    const int64_t col = tile * 512 + ln * 16 + j;
+    if (col >= len) continue;
+    int32_t s = 0;
+#pragma unroll
+    for (int q = 0; q < kColsumWarps; ++q) s += red[q][j][ln];
+    if (split_rows) {
+      if (s != 0) atomicAdd(out + col, s);
+    } else {
+      out[col] = s;
+    }
   }
 }
+// any length / alignment: one column per thread, the same row split
+__global__ void colsum_i8_kernel(const int8_t* __restrict__ x, int64_t rows, int64_t len, int64_t rows_per,
+                                 int32_t* __restrict__ out) {
+  const int64_t chunks = (rows + rows_per - 1) / rows_per;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < len * chunks;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = idx % len, chunk = idx / len;
+    const int64_t r0 = chunk * rows_per, r1 = r0 + rows_per < rows ? r0 + rows_per : rows;
+    int32_t acc = 0;
+    for (int64_t r = r0; r < r1; ++r) acc += x[r * len + c];
+    if (acc != 0) atomicAdd(out + c, acc);
+  }
+}
+
 // gen_input_checksum (checksum.hpp:248-266) from the batch-summed image: one
 // block per (c, r, s), lattice sum over every window position.
 __global__ void input_checksum_kernel(const int32_t* __restrict__ bsum, abed_layer_shape s, int32_t* __restrict__ ic) {
@@ -363,11 +498,36 @@ int guarded2(Fn&& fn) {
   }
 }
 // exported to campaign.cu / abi_core.cu
+void dev_colsum_i8(const int8_t* x, int64_t rows, int64_t len, int32_t* out, cudaStream_t st) {
+  const bool v16 = (len % 16 == 0) && (reinterpret_cast<uintptr_t>(x) % 16 == 0);
+  if (v16) {
+    // split the rows over blocks so the grid is about one full wave (8 resident
+    // blocks per SM) -- a partial second wave would double the latency tail
+    const int64_t col_tiles = (len / 16 + 31) / 32;
+    int64_t splits = ((int64_t)num_sms() * 8) / col_tiles;
+    const int64_t max_splits = (rows + kColsumWarps - 1) / kColsumWarps;  // >= one row per warp
+    if (splits > max_splits) splits = max_splits;
+    if (splits < 1) splits = 1;
+    const int64_t rows_per = (rows + splits - 1) / splits;
+    splits = (rows + rows_per - 1) / rows_per;
+    if (rows_per < rows) cuda_check(cudaMemsetAsync(out, 0, (size_t)len * 4, st), "colsum memset");
+    colsum_i8_v16_kernel<<<(unsigned)(col_tiles * splits), kColsumWarps * 32, 0, st>>>(x, rows, len, rows_per, out);
+  } else {
+    cuda_check(cudaMemsetAsync(out, 0, (size_t)len * 4, st), "colsum memset");
+    const int64_t want = (int64_t)num_sms() * 4 * 256;
+    int64_t rows_per = (rows * len + want - 1) / want;
+    if (rows_per < 16) rows_per = 16;
+    if (rows_per > rows) rows_per = rows;
+    const int64_t work = len * ((rows + rows_per - 1) / rows_per);
+    colsum_i8_kernel<<<grid_for(work, 256), 256, 0, st>>>(x, rows, len, rows_per, out);
+  }
+  launched("colsum_i8");
+}
 void dev_gen_input_checksum(const int8_t* x, const abed_layer_shape& s, int32_t* sums, cudaStream_t st) {
   if (8 + ceil_log2_host(s.n * s.p * s.q) > 32)
     throw_invalid("gen_input_checksum: PQN too large for i32 checksums; a wider plan is required");
   DevBuf<int32_t> b((size_t)(s.c * s.h * s.w));
-  batch_sum_nchw_kernel<<<grid_for(s.c * s.h * s.w, 256), 256, 0, st>>>(x, abed_dims4{s.n, s.c, s.h, s.w}, b.p);
+  dev_colsum_i8(x, s.n, s.c * s.h * s.w, b.p, st);
   input_checksum_kernel<<<(int)std::min<int64_t>(s.c * s.r * s.s, 65535), 256, 0, st>>>(b.p, s, sums);
   launched("gen_input_checksum");
   cuda_check(cudaStreamSynchronize(st), "gen_input_checksum sync");
@@ -383,8 +543,15 @@ void dev_epilog(const int32_t* in, abed_dims4 d, const abed_epilog_params* p, vo
       if (!std::isfinite(b)) throw_invalid("epilog: non-finite bias");
   }
   if (p->output_kind != ABED_I8 && p->output_kind != ABED_F32) throw_invalid("epilog: output kind must be i8 or f32");
-  epilog_kernel<<<grid_for(count4(d), 256), 256, 0, st>>>(in, d, p->scale, p->bias, p->activation == ABED_RELU,
-                                                           p->output_kind == ABED_F32, out);
+  const bool v16 = (d.d2 * d.d3) % 16 == 0 && reinterpret_cast<uintptr_t>(in) % 16 == 0 &&
+                   reinterpret_cast<uintptr_t>(out) % 16 == 0;
+  if (v16)
+    epilog_v16_kernel<<<grid_for(count4(d) / 16, 256), 256, 0, st>>>(in, d, p->scale, p->bias,
+                                                                     p->activation == ABED_RELU,
+                                                                     p->output_kind == ABED_F32, out);
+  else
+    epilog_kernel<<<grid_for(count4(d), 256), 256, 0, st>>>(in, d, p->scale, p->bias, p->activation == ABED_RELU,
+                                                             p->output_kind == ABED_F32, out);
   launched("epilog");
 }
 }  // namespace abed_host
@@ -415,8 +582,7 @@ int abed_gen_filter_checksum(const int8_t* f, abed_dims4 fd, int32_t* sums, void
   GUARD(check_dims(fd);
         if (fd.d0 > (int64_t(1) << 24)) throw_invalid("gen_filter_checksum: K too large for i32 checksums");
         const int64_t crs = fd.d1 * fd.d2 * fd.d3;
-        filter_sum_kernel<<<grid_for(crs, 256), 256, 0, (cudaStream_t)stream>>>(f, fd.d0, crs, sums);
-        launched("gen_filter_checksum"));
+        dev_colsum_i8(f, fd.d0, crs, sums, (cudaStream_t)stream));
 }
 int abed_decompose_checksum_filters(const int32_t* sums, int64_t n, int8_t* planes, void* stream) {
   GUARD(decompose_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(sums, n, planes); launched("decompose"));
@@ -506,8 +672,7 @@ int abed_ic_verify_k(const int32_t* cv, abed_dims4 d, const int8_t* f, abed_dims
 }
 int abed_ic_batch_checksum(const int8_t* x, abed_dims4 d, int32_t* out, void* stream) {
   GUARD(check_dims(d);
-        batch_sum_nchw_kernel<<<grid_for(d.d1 * d.d2 * d.d3, 256), 256, 0, (cudaStream_t)stream>>>(x, d, out);
-        launched("ic_batch_checksum"));
+        dev_colsum_i8(x, d.d0, d.d1 * d.d2 * d.d3, out, (cudaStream_t)stream));
 }
 int abed_ic_batch_verify(const int32_t* cv, abed_dims4 d, const int64_t* extra, abed_verify_outcome* o) {
   GUARD(check_dims(d);
