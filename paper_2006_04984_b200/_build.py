@@ -53,7 +53,33 @@ def build(verbose: bool = False) -> str:
         list(ex.map(_run, cmds))
     if not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
         _run([NVCC, *ARCH, "-shared", "-o", LIB, *objs])
+    build_cli()
     return LIB
+
+
+# nlohmann/json for the CLI's --config files and JSON reports (the reference's own
+# dependency; this image ships a copy inside the cudnn frontend headers)
+JSON_DIRS = [os.environ.get("ABED_JSON_INCLUDE", ""),
+             os.path.join(sys.prefix, "lib", "python3.12", "site-packages", "include", "cudnn_frontend",
+                          "thirdparty", "nlohmann"),
+             "/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann"]
+CLI_SRC = os.path.join(PKG, "cli", "abed_cli.cpp")
+CLI_BIN = os.path.join(PKG, "abed_b200")
+
+
+def build_cli() -> str | None:
+    """g++ the `abed_b200` CLI (verify / inject) against the drop-in headers and libabed_b200.so."""
+    jdir = next((d for d in JSON_DIRS if d and os.path.exists(os.path.join(d, "json.hpp"))), None)
+    if jdir is None:
+        sys.stderr.write("abed_b200 CLI not built: no nlohmann json.hpp found (set ABED_JSON_INCLUDE)\n")
+        return None
+    deps = [CLI_SRC, LIB] + glob.glob(os.path.join(ROOT, "include", "abed", "*.hpp"))
+    if os.path.exists(CLI_BIN) and os.path.getmtime(CLI_BIN) >= max(os.path.getmtime(d) for d in deps):
+        return CLI_BIN
+    _run(["g++", "-std=c++20", "-O2", "-Wall", "-I", os.path.join(ROOT, "include"), "-I", jdir,
+          "-I", "/usr/local/cuda/include", CLI_SRC, "-o", CLI_BIN, "-L", PKG, "-labed_b200",
+          "-Wl,-rpath,$ORIGIN", "-L/usr/local/cuda/lib64", "-lcudart"])
+    return CLI_BIN
 
 
 if __name__ == "__main__":
