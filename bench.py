@@ -423,6 +423,133 @@ def measure_mobilenetv2_int8(args, dev, stream, flush, world, dist):
             "fault_free_verdicts_failed": fails}
 
 
+def resnet50_chains(batch):
+    """Every ResNet-50 conv after the stem (network_config.hpp:245-282 builtin at
+    224x224; conv1 is excluded like the reference's exclude_first_layer): per
+    bottleneck the chain conv1 1x1 -> conv2 3x3 -> conv3 1x1, plus the 1x1
+    projection of each stage's first block as a chain of its own.  The residual
+    adds and pooling are not convolutions and are not part of this library, so
+    each chain starts from fresh packed data."""
+    from paper_2006_04984_b200 import api
+    chains, h, c = [], 56, 64
+    for st, (blocks, width) in enumerate(((3, 64), (4, 128), (6, 256), (3, 512))):
+        out = 4 * width
+        for b in range(blocks):
+            s = 2 if (b == 0 and st > 0) else 1
+            ho = (h + 2 - 3) // s + 1
+            chains.append([api.layer_shape(batch, c, h, h, width, 1, 1, 1, 1, 0, 0),
+                           api.layer_shape(batch, width, h, h, width, 3, 3, s, s, 1, 1),
+                           api.layer_shape(batch, width, ho, ho, out, 1, 1, 1, 1, 0, 0)])
+            if b == 0:
+                chains.append([api.layer_shape(batch, c, h, h, out, 1, 1, s, s, 0, 0)])
+            h, c = ho, out
+    return chains
+
+
+def measure_resnet50_network(args, dev, stream, flush, world, dist):
+    """whole-network protected INT8 inference -- all 52
+    ResNet-50 convs after the stem at batch 32 per GPU, bias + ReLU + requant,
+    chained through the packed layout.  Variants: unprotected, FIC with every
+    layer's input checksum from a second read of its input (FR), FIC-AF (inside a
+    chain the producing epilogue accumulates the consumer's input checksum from the
+    values it stores, cost-model option AF; chain heads stay FR), and full
+    duplication.  Overheads here are the inference-level numbers the paper quotes."""
+    import torch
+
+    from paper_2006_04984_b200 import abi, api
+    layers, ops, seed = [], 0, 5000
+    for chain in resnet50_chains(BATCH):
+        block = []
+        for ls in chain:
+            seed += 1
+            f = api.fill_random_i8(ls.k * ls.c * ls.r * ls.s, api.derive_seed(seed, 2)).view(ls.filter_dims())
+            ops += 2 * ls.n * ls.k * ls.p * ls.q * ls.c * ls.r * ls.s
+            L = {"ls": ls, "plans": {"unprotected": api.ConvPlan(ls, f, 0), "fic": api.ConvPlan(ls, f, abi.CHECK_FIC),
+                                     "fic_sm": api.ConvPlan(ls, f, abi.CHECK_FIC),
+                                     "fic_af": api.ConvPlan(ls, f, abi.CHECK_FIC)}}
+            L["plans"]["fic_sm"].set_input_checksum_source(abi.RHS_STAGED)
+            if block:
+                L["plans"]["fic_af"].set_af_input(True)
+            bias = torch.linspace(-1.0, 1.0, ls.k).tolist()
+            L["ep"] = {v: pl.epilog_params(0.02, bias, True) for v, pl in L["plans"].items()}
+            block.append(L)
+        ls0 = chain[0]
+        x = api.fill_random_i8(ls0.n * ls0.c * ls0.h * ls0.w, api.derive_seed(seed, 1)).view(ls0.input_dims())
+        block[0]["in"] = block[0]["plans"]["unprotected"].pack(x)
+        for a, b in zip(block, block[1:]):
+            a["out"] = b["plans"]["unprotected"].packed_buffer()
+            a["next"] = b
+            b["in"] = a["out"]
+        last = block[-1]["ls"]
+        block[-1]["out"] = torch.zeros(last.n * ((last.k + 15) // 16 * 16) * (last.p + 1) * (last.q + 1) + (1 << 16),
+                                       dtype=torch.int8, device=dev)
+        block[-1]["next"] = None
+        layers += block
+    VARIANTS = ("unprotected", "fic", "fic_sm", "fic_af", "dup")
+    sets = {v: api.PlanSet([L["plans"][v] for L in layers]) for v in ("fic", "fic_sm", "fic_af")}
+
+    def step(variant):
+        for L in layers:
+            nxt = L["next"]["plans"]["fic_af" if variant == "fic_af" else "unprotected"] if L["next"] else None
+            if variant == "dup":
+                pl = L["plans"]["unprotected"]
+                pl.run(L["in"], L["out"], abi.OUT_I8_PACKED, ep=L["ep"]["unprotected"], next_plan=nxt)
+                pl.run(L["in"], L["out"], abi.OUT_I8_COMPARE, ep=L["ep"]["unprotected"], next_plan=nxt)
+            else:
+                pl = L["plans"][variant]
+                pl.run(L["in"], L["out"], abi.OUT_I8_PACKED, ep=L["ep"][variant], next_plan=nxt)
+        if variant in sets:
+            sets[variant].finalize()
+
+    with torch.cuda.stream(stream):
+        for v in VARIANTS:
+            step(v)
+    torch.cuda.synchronize()
+    graphs = {}
+    for v in VARIANTS:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            step(v)
+        graphs[v] = g
+    res = {}
+    cur = torch.cuda.current_stream()
+    for v in VARIANTS:
+        for _ in range(max(3, args.warmup)):
+            flush.zero_()
+            graphs[v].replay()
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        ts = []
+        for _ in range(max(3, args.steps)):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(cur)
+            graphs[v].replay()
+            e1.record(cur)
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        ms = statistics.mean(ts)
+        if dist:
+            tt = torch.tensor([ms], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ms = tt.item()
+        res[v] = {"tops": round(ops * world / (ms * 1e-3) / 1e12, 2), "ms_per_step": round(ms, 4)}
+    fails = sum(oc[1].status for v in ("fic", "fic_sm", "fic_af") for oc in sets[v].outcomes())
+    u = res["unprotected"]["ms_per_step"]
+    return {"workload": f"resnet50-all-convs-int8-b{BATCH} ({len(layers)} convs after the stem: 1x1 + 3x3 + "
+                        "projections, chained per bottleneck; residual adds / pooling not modelled)",
+            "fic_af": "FIC; inside each bottleneck chain the producing epilogue accumulates the consumer's "
+                      "input checksum (chain heads re-read their input)",
+            "global_batch": BATCH * world, "layers": len(layers), "gop_per_step": round(ops * world / 1e9, 2),
+            "variants": res,
+            "overhead_pct": {"fic_vs_unprotected": round(100 * (res["fic"]["ms_per_step"] / u - 1), 2),
+                             "fic_sm_vs_unprotected": round(100 * (res["fic_sm"]["ms_per_step"] / u - 1), 2),
+                             "fic_af_vs_unprotected": round(100 * (res["fic_af"]["ms_per_step"] / u - 1), 2),
+                             "duplication_vs_unprotected": round(100 * (res["dup"]["ms_per_step"] / u - 1), 2)},
+            "fault_free_verdicts_failed": fails}
+
+
 # ---------------------------------------------------------------- GPU arm
 def measure_hbm_kernels(dev, stream, flush, peaks):
     """The HBM-bound checksum kernels and the layout boundary
@@ -614,6 +741,9 @@ def run_ours(args, world, rank, local):
     if not args.skip_vgg:
         vgg = measure_vgg16_fp16(args, dev, stream, flush, world, dist)
     hbm = measure_hbm_kernels(dev, stream, flush, peaks) if rank == 0 else None
+    r50 = None
+    if not args.skip_r50net:
+        r50 = measure_resnet50_network(args, dev, stream, flush, world, dist)
     mbv2 = None
     if not args.skip_mbv2:
         mbv2 = measure_mobilenetv2_int8(args, dev, stream, flush, world, dist)
@@ -786,6 +916,7 @@ def run_ours(args, world, rank, local):
         "cfg3_vgg16_fp16": vgg,
         "cfg4_mobilenetv2_int8": mbv2,
         "hbm_kernels": hbm,
+        "resnet50_network_int8": r50,
     }
     print(json.dumps(line), flush=True)
     if dist:
@@ -804,6 +935,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--skip-vgg", action="store_true", help="skip the VGG-16 FP16 block (BASELINE configs[2])")
     ap.add_argument("--skip-mbv2", action="store_true", help="skip the MobileNetV2 INT8 block (BASELINE configs[3])")
+    ap.add_argument("--skip-r50net", action="store_true", help="skip the whole-network ResNet-50 INT8 block")
     ap.add_argument("--global-batch", type=int, default=0,
                     help="shard this fixed ResNet-50 batch over the GPUs (BASELINE configs[4]: 1024); default 32 per GPU")
     args = ap.parse_args()

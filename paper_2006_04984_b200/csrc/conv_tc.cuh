@@ -159,8 +159,9 @@ struct ConvTcParams {
 // trace slots: 0 globaltimer at entry, 1 clock at entry, 2 setup done, 3 first
 // stage ready (MMA warp), 4 last MMA commit, 5 epilogue done, 6 units, 7 producer
 // done, 8 first copy issued, 9 summed MMA-warp wait cycles on `full`, 10 summed
-// epilogue-warp wait cycles on the accumulator
-constexpr int kTraceSlots = 16;
+// epilogue-warp wait cycles on the accumulator; globaltimer stamps: 16 producer past
+// griddepcontrol.wait, 17 first stage full (MMA warp), 18 last MMA commit, 19 epilogue done
+constexpr int kTraceSlots = 24;
 constexpr int kCtaRec = 6;  // int64 slots per CTA in ConvTcParams::cta_rec
 
 // one plan's verdict reduction (verdict_kernel, conv_tc.cu)

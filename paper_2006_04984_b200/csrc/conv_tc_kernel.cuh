@@ -563,7 +563,12 @@ __device__ __forceinline__ void mma_warp_run(const ConvTcParams& p, const MmaEnv
           const long long w0 = clock64();
           mbar_wait(&v.full[stage], phase);
           const long long w1 = clock64();
-          if (u == 0 && ks == 0) tr_first = w1 - v.t_entry;
+          if (u == 0 && ks == 0) {
+            tr_first = w1 - v.t_entry;
+            uint64_t gt_;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt_));
+            if (v.lane == 0) v.trace[17] = static_cast<int64_t>(gt_);
+          }
           tr_full += w1 - w0;
         } else {
           mbar_wait(&v.full[stage], phase);
@@ -613,7 +618,12 @@ __device__ __forceinline__ void mma_warp_run(const ConvTcParams& p, const MmaEnv
         }
       }
       if (!(p.dbg & 8) || u >= v.n_units - 2) mma_commit_w(&v.tfull[as]);
-      if (v.trace && u == v.n_units - 1) tr_last = clock64() - v.t_entry;
+      if (v.trace && u == v.n_units - 1) {
+        tr_last = clock64() - v.t_entry;
+        uint64_t gt_;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt_));
+        if (v.lane == 0) v.trace[18] = static_cast<int64_t>(gt_);
+      }
     }
   }
   if (v.trace && v.lane == 0) {
@@ -864,7 +874,12 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
       pdl_wait();
       int stage = 0;
       uint32_t phase = 0;
-      if (trace && lane == 0) trace[8] = clock64() - t_entry;
+      if (trace && lane == 0) {
+        trace[8] = clock64() - t_entry;
+        uint64_t gt_;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt_));
+        trace[16] = static_cast<int64_t>(gt_);
+      }
       for (int u = 0; u < n_units; ++u) {
         int mt, nt;
         decode_tile(p, u, mt, nt);
@@ -1273,6 +1288,9 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
   if (trace && warp == 2 && lane == 0) {
     trace[5] = clock64() - t_entry;
     trace[6] = n_units;
+    uint64_t gt_;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt_));
+    trace[19] = static_cast<int64_t>(gt_);
   }
   if (trace && warp == 2 + kEpiWarps && lane == 0) trace[15] = clock64() - t_entry;  // input-checksum warps done
   tc_fence_before();

@@ -30,7 +30,7 @@ def main():
         f = api.fill_random_i8(ls.k * ls.c * ls.r * ls.s, api.derive_seed(li, 2)).view(ls.filter_dims())
         pl = api.ConvPlan(ls, f, checks)
         out = torch.zeros(ls.n * k * (ls.p + 1) * (ls.q + 1) + 65536, dtype=torch.int8, device="cuda")
-        tr = torch.zeros(1024 * 16, dtype=torch.int64, device="cuda")
+        tr = torch.zeros(1024 * 24, dtype=torch.int64, device="cuda")
         layers.append((name, pl, pl.pack(x), out, pl.epilog_params(0.05, torch.linspace(-2, 2, k), True), tr))
     stream = torch.cuda.Stream()
 
@@ -64,7 +64,7 @@ def main():
     prev_end = None
     busy = 0.0
     for name, pl, packed, out, ep, tr in layers:
-        rows = [r for r in tr.view(-1, 16).cpu().tolist() if r[1] != 0]
+        rows = [r for r in tr.view(-1, 24).cpu().tolist() if r[1] != 0]
         start = min(r[0] for r in rows)
         end = max(r[14] for r in rows)
         if t0 is None:
@@ -72,8 +72,18 @@ def main():
         gap = (start - prev_end) / 1e3 if prev_end is not None else 0.0
         span = (end - start) / 1e3
         busy += span
+        rel = [r[16] for r in rows if r[16]]
+        first = [r[17] for r in rows if r[17]]
+        lastmma = [r[18] for r in rows if r[18]]
+        epi = [r[19] for r in rows if r[19]]
+        extra = ""
+        if prev_end is not None and rel:
+            import statistics as st
+            extra = (f"  | release-prevend {(min(rel) - prev_end) / 1e3:5.2f}  first-ready(med) "
+                     f"{(st.median(first) - min(rel)) / 1e3:5.2f}  last-mma(max) {(max(lastmma) - min(rel)) / 1e3:5.2f}"
+                     f"  epi-done(max) {(max(epi) - min(rel)) / 1e3:5.2f}  exit(max) {(end - min(rel)) / 1e3:5.2f}")
         print(f"{name:15s} start {(start - t0) / 1e3:7.2f} us  end {(end - t0) / 1e3:7.2f} us  span {span:6.2f} us  "
-              f"gap-from-prev-end {gap:6.2f} us  ctas {len(rows)}")
+              f"gap-from-prev-end {gap:6.2f} us  ctas {len(rows)}{extra}")
         prev_end = end
     print(f"sum of kernel spans {busy:.1f} us")
 

@@ -32,7 +32,7 @@ def main():
     a = ap.parse_args()
     checks = {"unprotected": 0, "fc": abi.CHECK_FC, "fic": abi.CHECK_FIC}[a.variant]
     only = set(a.only.split(",")) if a.only else None
-    trace = torch.zeros(1024 * 16, dtype=torch.int64, device="cuda")
+    trace = torch.zeros(1024 * 24, dtype=torch.int64, device="cuda")
     for li, (name, c, h, w, k, st) in enumerate(RESNET50_3X3):
         if only and name not in only:
             continue
@@ -61,7 +61,7 @@ def main():
         pl.run(packed, out, abi.OUT_I8_PACKED, ep=ep)
         torch.cuda.synchronize()
         abi.call("abed_debug_set_conv_trace", pl.handle, None, 0)
-        t = trace.view(-1, 16).cpu()
+        t = trace.view(-1, 24).cpu()
         rows = [r for r in t.tolist() if r[1] != 0]
         i = pl.info
         g0 = min(r[0] for r in rows)
