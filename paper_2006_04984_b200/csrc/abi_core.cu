@@ -328,9 +328,18 @@ void plan_run(abed_conv_plan* pl, const int8_t* packed, const abed_epilog_params
   // that do the whole checksum with all their warps; otherwise the conv CTAs'
   // input-checksum warps do it.  Returns the image split of the work items.
   auto fr_split = [&](const ActGeom& g) {
+    if (p.n_tiles == 1 && p.conv_grid > 0) {
+      // wave-quantisation slack: the fewest conv CTAs with the same units per CTA
+      // (same makespan) leave SMs free for the input-checksum CTAs -- used when
+      // it frees enough of them to carry the whole checksum (measured: 12 idle
+      // SMs are too few for ResNet-50 layer1, 42 beat the in-CTA warps on layer2)
+      const int per = (p.m_tiles + p.conv_grid - 1) / p.conv_grid;
+      const int g2 = (p.m_tiles + per - 1) / per;
+      if (num_sms() - g2 >= 24) p.conv_grid = g2;
+    }
     const int idle = num_sms() - p.conv_grid;
     int64_t want;
-    if (idle >= 8) {
+    if (idle >= 16) {
       p.ic_ctas = idle;
       want = 2LL * idle * abed_dev::kConvThreads_host;
     } else {

@@ -642,7 +642,7 @@ __device__ __forceinline__ void mma_warp_run(const ConvTcParams& p, const MmaEnv
 // items (input_checksum_f64 / fic_dot_f64, checksum.hpp:496-535).  Run by the conv
 // CTAs' input-checksum warps, or by all warps of the extra input-checksum CTAs
 // that fill the SMs a small conv grid leaves idle.
-template <int DT>
+template <int DT, int DEPTH = 8>
 __device__ __forceinline__ void fic_rhs_fr(const ConvTcParams& p, int64_t first, int64_t stride, long long& acc,
                                            double& facc_rhs) {
   if constexpr (DT != DT_I8) {
@@ -696,13 +696,13 @@ __device__ __forceinline__ void fic_rhs_fr(const ConvTcParams& p, int64_t first,
       const int n0 = static_cast<int>(static_cast<int64_t>(p.N) * split / nsplit);
       const int n1 = static_cast<int>(static_cast<int64_t>(p.N) * (split + 1) / nsplit);
       int32_t d0 = 0, d1 = 0, d2 = 0;  // |sum| <= 32 images * 16 * 128 * 128 < 2^31
-      for (int n = n0; n < n1; n += 8) {
-        uint4 x[8];
+      for (int n = n0; n < n1; n += DEPTH) {  // DEPTH image loads in flight
+        uint4 x[DEPTH];
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
+        for (int j = 0; j < DEPTH; ++j)
           x[j] = n + j < n1 ? __ldcg(src + static_cast<int64_t>(n + j) * HlWl) : make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
+        for (int j = 0; j < DEPTH; ++j) {
           d0 = __dp4a(static_cast<int>(x[j].x), static_cast<int>(g0.x), d0);
           d0 = __dp4a(static_cast<int>(x[j].y), static_cast<int>(g0.y), d0);
           d0 = __dp4a(static_cast<int>(x[j].z), static_cast<int>(g0.z), d0);
@@ -716,7 +716,7 @@ __device__ __forceinline__ void fic_rhs_fr(const ConvTcParams& p, int64_t first,
           d2 = __dp4a(static_cast<int>(x[j].z), static_cast<int>(g2.z), d2);
           d2 = __dp4a(static_cast<int>(x[j].w), static_cast<int>(g2.w), d2);
         }
-        if (((n - n0) & 31) == 24) {  // keep the digit sums inside int32
+        if (((n - n0) & 31) == 32 - DEPTH) {  // keep the digit sums inside int32
           acc += static_cast<long long>(d0) + (static_cast<long long>(d1) << 8) + (static_cast<long long>(d2) << 16);
           d0 = d1 = d2 = 0;
         }
@@ -767,7 +767,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
     double facc_rhs = 0.0;
     pdl_wait();
     if (FIC && p.rhs_mode == 1)
-      fic_rhs_fr<DT>(p, static_cast<int64_t>(blockIdx.x - p.conv_grid) * kConvThreads + threadIdx.x,
+      fic_rhs_fr<DT, 16>(p, static_cast<int64_t>(blockIdx.x - p.conv_grid) * kConvThreads + threadIdx.x,
                      static_cast<int64_t>(p.ic_ctas) * kConvThreads, acc, facc_rhs);
     __shared__ long long s_ic[kConvThreads / 32];
     if (FIC) {
