@@ -896,7 +896,7 @@ def run_ours(args, world, rank, local):
         "data": "synthetic: SplitMix64 int8 activations/filters generated on device; bias linspace(-2,2), scale 0.05",
         "config": {"workload": WORKLOAD if not args.global_batch else WORKLOAD.replace("-b32", f"-b{rb * world}"),
                    "global_batch": rb * world, "per_gpu_batch": rb, "layers": 16,
-                   "scheme": "FIC-FR in one kernel per layer (input-checksum warps re-read the stored input: x.G with dp4a; epilogue output sums; per-CTA verdict records) + one verdict launch per pass for all 16 VerifyOutcomes",
+                   "scheme": "FIC-FR in one kernel per layer (input checksum x.G with dp4a from a second read of the stored input, by input-checksum warps or, where the conv grid leaves SMs free, input-checksum CTAs; epilogue output sums; per-CTA verdict records) + one verdict launch per pass for all 16 VerifyOutcomes",
                    "parallelism": f"dp{world} (batch shards, NCCL error-count all-reduce)",
                    "l2": "flushed (512 MiB memset) before every timed step", "timing": "CUDA graph replay, CUDA events"},
         "roofline": roofline,
