@@ -614,6 +614,68 @@ def measure_hbm_kernels(dev, stream, flush, peaks):
             "timing": "one-launch CUDA graph after a 512 MiB L2 flush, CUDA events, median of 20", "kernels": res}
 
 
+def measure_abft_gemm(dev, stream, flush):
+    """the classical row/column-checksum ABFT (reference
+    abft_gemm.hpp) on the B200 against the same GEMM unprotected and with the ABED
+    style check fused into the GEMM epilogue (the filter-checksum column = ABFT's
+    row check).  GEMMs = the im2col products of ResNet-50 3x3 layers at batch 32
+    (m = N.P.Q, k = C.R.S, n = K).  All three modes run the same pipeline on the
+    tcgen05 kernel with both operands supplied at run time (pack A, pack B, GEMM,
+    copy-out; "weights_offline" keeps B packed from the warm-up, as ABED's offline
+    filter checksum assumes); ABFT adds its online tasks (checksum row / column as digit rows,
+    the larger GEMM, the dual output-checksum passes over the i64 c_aug).  Each
+    mode: one captured CUDA graph, L2 flushed before every replay, median of 20."""
+    import torch
+
+    from paper_2006_04984_b200 import api
+
+    shapes = {"layer2 (25088x1152x128)": (25088, 1152, 128), "layer3 (6272x2304x256)": (6272, 2304, 256)}
+    out = {}
+    with torch.cuda.stream(stream):
+        for name, (m, k, n) in shapes.items():
+            a = api.fill_random_i8(m * k, api.derive_seed(91, 1)).view(m, k)
+            b = api.fill_random_i8(k * n, api.derive_seed(91, 2)).view(k, n)
+            c = torch.empty((m, n), dtype=torch.int32, device=dev)
+            ca = torch.empty((m + 1, n + 1), dtype=torch.int64, device=dev)
+            plan = api.AbftPlan(m, n, k)
+            res = {}
+            for label, mode in (("plain", api.ABFT_PLAIN), ("abed_fused_row", api.ABFT_FUSED_ROW),
+                                ("abft", api.ABFT_CHECKED)):
+                for _ in range(3):
+                    plan.run(a, b, c, ca, mode)
+                torch.cuda.synchronize()
+                row, col = plan.verdicts()
+                assert row.status == 0 and col.status == 0, (name, label)
+                for setting, bb in (("online", b), ("weights_offline", None)):
+                    g = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(g, stream=stream):
+                        plan.run(a, bb, c, ca, mode)
+                    ts = []
+                    for _ in range(20):
+                        flush.zero_()
+                        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                        e0.record(stream)
+                        g.replay()
+                        e1.record(stream)
+                        e1.synchronize()
+                        ts.append(e0.elapsed_time(e1) * 1e3)
+                    us = statistics.median(ts)
+                    res.setdefault(setting, {})[label] = {"us": round(us, 2),
+                                                          "tops": round(2.0 * m * n * k / (us * 1e-6) / 1e12, 1)}
+            row, col = plan.verdicts()
+            out[name] = res
+            for setting, r in res.items():
+                r["abft_overhead_pct"] = round(100 * (r["abft"]["us"] / r["plain"]["us"] - 1), 1)
+                r["abed_fused_row_overhead_pct"] = round(100 * (r["abed_fused_row"]["us"] / r["plain"]["us"] - 1), 1)
+            out[name]["abft_verdicts"] = [row.status, col.status]
+            del plan
+    torch.cuda.synchronize()
+    return {"what": "int8 GEMM (im2col shapes of ResNet-50 3x3 layers, batch 32): plain / ABED-style fused row check / "
+                    "classical row+column ABFT (abft_gemm.hpp tasks 2-6), all on the tcgen05 GEMM",
+            "timing": "one CUDA graph per mode, L2 flushed before each replay, CUDA events, median of 20",
+            "gemms": out}
+
+
 def run_ours(args, world, rank, local):
     import ctypes as C
 
@@ -741,6 +803,7 @@ def run_ours(args, world, rank, local):
     if not args.skip_vgg:
         vgg = measure_vgg16_fp16(args, dev, stream, flush, world, dist)
     hbm = measure_hbm_kernels(dev, stream, flush, peaks) if rank == 0 else None
+    abft = measure_abft_gemm(dev, stream, flush) if (rank == 0 and not args.skip_abft) else None
     r50 = None
     if not args.skip_r50net:
         r50 = measure_resnet50_network(args, dev, stream, flush, world, dist)
@@ -917,6 +980,7 @@ def run_ours(args, world, rank, local):
         "cfg4_mobilenetv2_int8": mbv2,
         "hbm_kernels": hbm,
         "resnet50_network_int8": r50,
+        "abft_gemm_int8": abft,
     }
     print(json.dumps(line), flush=True)
     if dist:
@@ -936,6 +1000,7 @@ def main():
     ap.add_argument("--skip-vgg", action="store_true", help="skip the VGG-16 FP16 block (BASELINE configs[2])")
     ap.add_argument("--skip-mbv2", action="store_true", help="skip the MobileNetV2 INT8 block (BASELINE configs[3])")
     ap.add_argument("--skip-r50net", action="store_true", help="skip the whole-network ResNet-50 INT8 block")
+    ap.add_argument("--skip-abft", action="store_true", help="skip the ABFT-GEMM comparison block")
     ap.add_argument("--global-batch", type=int, default=0,
                     help="shard this fixed ResNet-50 batch over the GPUs (BASELINE configs[4]: 1024); default 32 per GPU")
     args = ap.parse_args()

@@ -315,6 +315,34 @@ int abed_conv_plan_create_h(const abed_layer_shape* shape, const float* filters,
                             double tau_fc, double tau_fic, int32_t force_block_n, abed_conv_plan** plan);
 int abed_pack_input_h(const abed_conv_plan* plan, const float* input, void* packed, void* stream);
 int abed_conv_plan_set_tau(abed_conv_plan* plan, double tau_fc, double tau_fic);
+/* ------------------------------------------------------------ ABFT GEMM comparison
+ * Row/column-checksum ABFT for an int8 GEMM (abft_gemm.hpp:98-152), the classical
+ * scheme the paper contrasts with ABED, on the tcgen05 GEMM: A (m x k) and B (k x n)
+ * row-major int8 device matrices, c (m x n i32, may be NULL), c_aug ((m+1) x (n+1)
+ * i64: the augmented product with the checksum row and column, abft_gemm.hpp:139),
+ * row / column VerifyOutcomes of abft_check (:70-96; locus (index, -1, -1)).
+ * Guards as the reference: inner-dimension mismatch, 16 + ceil_log2(m n k) > 63,
+ * 16 + ceil_log2(k) > 31 are invalid_argument (:106-111). */
+enum { ABED_ABFT_CHECKED = 0, ABED_ABFT_PLAIN = 1, ABED_ABFT_FUSED_ROW = 2 };
+/* abft_gemm (synchronous; outcomes in host memory) */
+int abed_abft_gemm_i8(const int8_t* a, int64_t m, int64_t k, const int8_t* b, int64_t kb, int64_t n, int32_t* c,
+                      int64_t* c_aug, abed_verify_outcome* row_check, abed_verify_outcome* col_check);
+/* abft_check (:70-96) on a device (rows x cols) i64 c_aug; rows, cols >= 2 */
+int abed_abft_check(const int64_t* c_aug, int64_t rows, int64_t cols, abed_verify_outcome* row_check,
+                    abed_verify_outcome* col_check);
+/* Plan form for timing (allocation-free, stream-ordered runs).  mode:
+ * ABED_ABFT_CHECKED = abft_gemm's online tasks (2)-(6) (outcomes_dev[2] = {row, col});
+ * ABED_ABFT_PLAIN = the same GEMM pipeline without checksums (unprotected baseline);
+ * ABED_ABFT_FUSED_ROW = ABED-style: the row check as a filter-checksum column
+ * verified inside the GEMM epilogue (outcomes_dev[0]; [1] is a pass).
+ * b == NULL reuses B (and its checksum column) packed by an earlier run in the
+ * same mode: the weights-offline setting. */
+typedef struct abed_abft_plan abed_abft_plan;
+int abed_abft_plan_create(int64_t m, int64_t n, int64_t k, abed_abft_plan** plan);
+int abed_abft_plan_destroy(abed_abft_plan* plan);
+int abed_abft_plan_run(abed_abft_plan* plan, const int8_t* a, const int8_t* b, int32_t* c, int64_t* c_aug,
+                       abed_verify_outcome* outcomes_dev, int32_t mode, void* stream);
+
 /* diagnostics (no reference counterpart): record a per-CTA clock timeline of the
  * conv kernel into trace_dev (16 int64 per CTA, caller-zeroed); NULL disables.
  * flags bit 0 makes the epilogue skip its work (timing experiments only). */

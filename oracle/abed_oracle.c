@@ -699,3 +699,63 @@ int ora_run_campaign(const abed_campaign_config* cfg, int64_t t_begin, int64_t t
   free(f);
   return st;
 }
+
+/* ------------------------------------------------------------------ ABFT GEMM */
+int ora_abft_check(const int64_t* ca, int64_t rows, int64_t cols, abed_verify_outcome* row,
+                   abed_verify_outcome* col) { /* abft_gemm.hpp:70-96 */
+  const int64_t m = rows - 1, n = cols - 1;
+  if (m < 1 || n < 1) return ORA_INVALID;
+  int64_t bad = 0;
+  outcome_ok(row);
+  for (int64_t i = 0; i <= m; ++i) { /* row sums vs the appended column */
+    uint64_t sum = 0; /* int64 wraparound, as the reference's two's-complement sums */
+    for (int64_t j = 0; j < n; ++j) sum += (uint64_t)ca[i * cols + j];
+    if ((int64_t)sum != ca[i * cols + n]) {
+      if (!bad) outcome_fail(row, (int64_t)sum, ca[i * cols + n], 1, i, -1, -1);
+      ++bad;
+    }
+  }
+  row->error_count = bad;
+  bad = 0;
+  outcome_ok(col);
+  for (int64_t j = 0; j <= n; ++j) { /* column sums vs the appended row */
+    uint64_t sum = 0;
+    for (int64_t i = 0; i < m; ++i) sum += (uint64_t)ca[i * cols + j];
+    if ((int64_t)sum != ca[m * cols + j]) {
+      if (!bad) outcome_fail(col, (int64_t)sum, ca[m * cols + j], 1, j, -1, -1);
+      ++bad;
+    }
+  }
+  col->error_count = bad;
+  return ORA_OK;
+}
+int ora_abft_gemm(const int8_t* a, int64_t m, int64_t k, const int8_t* b, int64_t kb, int64_t n, int32_t* c,
+                  int64_t* ca, abed_verify_outcome* row, abed_verify_outcome* col) { /* abft_gemm.hpp:102-152 */
+  if (m < 1 || n < 1 || k < 1 || k != kb) return ORA_INVALID;
+  if (16 + ora_ceil_log2(m * n * k) > 63 || 16 + ora_ceil_log2(k) > 31) return ORA_INVALID;
+  int32_t* colsum = (int32_t*)calloc((size_t)k, 4); /* task (3): A column sums, B row sums (i32) */
+  int32_t* rowsum = (int32_t*)calloc((size_t)k, 4);
+  if (!colsum || !rowsum) { free(colsum); free(rowsum); return ORA_INVALID; }
+  for (int64_t t = 0; t < k; ++t) {
+    for (int64_t i = 0; i < m; ++i) colsum[t] += a[i * k + t];
+    for (int64_t j = 0; j < n; ++j) rowsum[t] += b[t * n + j];
+  }
+  const int64_t cols = n + 1; /* task (4): (m+1) x (n+1) product of the augmented operands in i64 */
+  for (int64_t i = 0; i <= m; ++i)
+    for (int64_t j = 0; j <= n; ++j) {
+      int64_t acc = 0;
+      for (int64_t t = 0; t < k; ++t) {
+        const int64_t x = i < m ? a[i * k + t] : colsum[t];
+        const int64_t y = j < n ? b[t * n + j] : rowsum[t];
+        acc += x * y;
+      }
+      ca[i * cols + j] = acc;
+    }
+  free(colsum);
+  free(rowsum);
+  ora_abft_check(ca, m + 1, n + 1, row, col); /* task (5) */
+  if (c)                                      /* task (6): trimmed copy-out */
+    for (int64_t i = 0; i < m; ++i)
+      for (int64_t j = 0; j < n; ++j) c[i * n + j] = (int32_t)ca[i * cols + j];
+  return ORA_OK;
+}

@@ -108,6 +108,12 @@ int ora_run_trial(const abed_layer_shape* ls, const int8_t* x, const int8_t* f, 
 int ora_run_campaign(const abed_campaign_config* cfg, int64_t t_begin, int64_t t_end,
                      abed_campaign_report* rep);                                    /* :276 */
 
+/* abft_gemm.hpp:70-96 abft_check / :102-152 abft_gemm (row-major i8 A m x k, B k x n) */
+int ora_abft_check(const int64_t* c_aug, int64_t rows, int64_t cols, abed_verify_outcome* row,
+                   abed_verify_outcome* col);
+int ora_abft_gemm(const int8_t* a, int64_t m, int64_t k, const int8_t* b, int64_t kb, int64_t n, int32_t* c,
+                  int64_t* c_aug, abed_verify_outcome* row, abed_verify_outcome* col);
+
 #ifdef __cplusplus
 }
 #endif

@@ -267,6 +267,39 @@ class Oracle:
             fn(ptr(convout), convout.size, expected, C.byref(o))
         return o
 
+    # ------------------------------------------------------------ ABFT GEMM
+    def abft_gemm(self, a, b):
+        """abft_gemm (abft_gemm.hpp:102-152): (c i32 m x n, c_aug i64 (m+1) x (n+1), row, col)."""
+        a = np.ascontiguousarray(a, np.int8)
+        b = np.ascontiguousarray(b, np.int8)
+        m, k = a.shape
+        kb, n = b.shape
+        c = np.empty((m, n), np.int32)
+        ca = np.empty((m + 1, n + 1), np.int64)
+        row, col = VerifyOutcome(), VerifyOutcome()
+        fn = self._f("abft_gemm")
+        fn.argtypes = [P, C.c_int64, C.c_int64, P, C.c_int64, C.c_int64, P, P, C.POINTER(VerifyOutcome),
+                       C.POINTER(VerifyOutcome)]
+        self._chk(fn(ptr(a), m, k, ptr(b), kb, n, ptr(c), ptr(ca), C.byref(row), C.byref(col)))
+        return c, ca, row, col
+
+    def abft_check(self, c_aug):
+        """abft_check (abft_gemm.hpp:70-96) -> (row, col)."""
+        ca = np.ascontiguousarray(c_aug, np.int64)
+        row, col = VerifyOutcome(), VerifyOutcome()
+        fn = self._f("abft_check")
+        fn.argtypes = [P, C.c_int64, C.c_int64, C.POINTER(VerifyOutcome), C.POINTER(VerifyOutcome)]
+        self._chk(fn(ptr(ca), ca.shape[0], ca.shape[1], C.byref(row), C.byref(col)))
+        return row, col
+
+    def abft_costs(self, m, n, k, single_pass=False):
+        """abft_costs (abft_gemm.hpp:41-55), reference build only: 5 x [ops, read, write, moved]."""
+        out = np.zeros(20, np.int64)
+        fn = self._f("abft_costs", None)
+        fn.argtypes = [C.c_int64, C.c_int64, C.c_int64, C.c_int, P]
+        fn(m, n, k, 1 if single_pass else 0, ptr(out))
+        return out.reshape(5, 4)
+
     def ic_verify_k(self, convout, f, ic):
         convout = np.ascontiguousarray(convout, np.int32)
         f = np.ascontiguousarray(f, np.int8)

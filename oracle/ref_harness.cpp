@@ -6,6 +6,7 @@
 // (abed_oracle.c) against the reference itself, (2) generate tests/golden/, and
 // (3) time the reference's own CPU path for bench.py (cpu_baseline / --impl
 // reference).  No reference source is copied into this repository.
+#include <abed/abft_gemm.hpp>
 #include <abed/checksum.hpp>
 #include <abed/convolution.hpp>
 #include <abed/faults.hpp>
@@ -345,6 +346,40 @@ double ref_time_layer(const abed_layer_shape* s, int scheme, int threads, const 
   for (auto& th : pool) th.join();
   const auto t1 = std::chrono::steady_clock::now();
   return std::chrono::duration<double>(t1 - t0).count();
+}
+
+// abft_gemm.hpp:102-152 / :70-96 (row-major i8 operands; c_aug (m+1) x (n+1) i64)
+int ref_abft_gemm(const int8_t* a, int64_t m, int64_t k, const int8_t* b, int64_t kb, int64_t n, int32_t* c,
+                  int64_t* ca, abed_verify_outcome* row, abed_verify_outcome* col) {
+  return guard([&] {
+    Matrix am(m, k, ElemKind::I8), bm(kb, n, ElemKind::I8);
+    std::memcpy(am.view<std::int8_t>().data(), a, (size_t)(m * k));
+    std::memcpy(bm.view<std::int8_t>().data(), b, (size_t)(kb * n));
+    const AbftResult r = abft_gemm(am, bm);
+    if (c) std::memcpy(c, r.c.view<const std::int32_t>().data(), (size_t)(m * n) * 4);
+    std::memcpy(ca, r.c_aug.view<const std::int64_t>().data(), (size_t)((m + 1) * (n + 1)) * 8);
+    put_outcome(r.row_check, row);
+    put_outcome(r.col_check, col);
+  });
+}
+int ref_abft_check(const int64_t* ca, int64_t rows, int64_t cols, abed_verify_outcome* row, abed_verify_outcome* col) {
+  return guard([&] {
+    Matrix cm(rows, cols, ElemKind::I64);
+    std::memcpy(cm.view<std::int64_t>().data(), ca, (size_t)(rows * cols) * 8);
+    const auto [r, c] = abft_check(cm);
+    put_outcome(r, row);
+    put_outcome(c, col);
+  });
+}
+// abft_gemm.hpp:41-55 abft_costs: 5 tasks x {ops, read, write, moved}
+void ref_abft_costs(int64_t m, int64_t n, int64_t k, int single_pass, int64_t* out) {
+  const AbftCosts cs = abft_costs(m, n, k, single_pass != 0);
+  for (int t = 0; t < 5; ++t) {
+    out[4 * t + 0] = cs.tasks[t].ops;
+    out[4 * t + 1] = cs.tasks[t].read_bytes;
+    out[4 * t + 2] = cs.tasks[t].write_bytes;
+    out[4 * t + 3] = cs.tasks[t].elements_moved;
+  }
 }
 
 }  // extern "C"

@@ -133,6 +133,11 @@ SIGNATURES = {
     "abed_fill_random_i8": (C.c_int, [P, i64, u64, u64, P]),
     "abed_fill_random_extreme": (C.c_int, [P, i64, u64, u64, P]),
     "abed_derive_seed": (u64, [u64, u64]),
+    "abed_abft_gemm_i8": (C.c_int, [P, i64, i64, P, i64, i64, P, P, OUTC, OUTC]),
+    "abed_abft_check": (C.c_int, [P, i64, i64, OUTC, OUTC]),
+    "abed_abft_plan_create": (C.c_int, [i64, i64, i64, C.POINTER(P)]),
+    "abed_abft_plan_destroy": (C.c_int, [P]),
+    "abed_abft_plan_run": (C.c_int, [P, P, P, P, P, P, i32, P]),
     "abed_conv_i8": (C.c_int, [P, P, SHP, P, P]),
     "abed_conv_f32": (C.c_int, [P, P, SHP, P, P]),
     "abed_epilog": (C.c_int, [P, Dims4, C.POINTER(EpilogParams), P, P]),

@@ -302,6 +302,62 @@ def run_campaign(ls, scheme, target, trials=1000, root_seed=1, mode=abi.DATA_ONE
 
 
 # ------------------------------------------------------------------ protected conv plan (hot path)
+# ---------------------------------------------------------------- ABFT GEMM
+ABFT_CHECKED, ABFT_PLAIN, ABFT_FUSED_ROW = 0, 1, 2
+
+
+def abft_gemm(a, b):
+    """abft_gemm (abft_gemm.hpp:102-152): row/column-checksum ABFT for an int8 GEMM
+    on the tcgen05 GEMM.  a: m x k, b: k x n int8 CUDA tensors (row-major).
+    Returns (c int32 m x n, c_aug int64 (m+1) x (n+1), row_check, col_check)."""
+    if a.dtype != torch.int8 or b.dtype != torch.int8:
+        raise abi.InvalidArgument(abi.ERR_INVALID_ARGUMENT, "abft_gemm: operands must be i8")
+    m, k = a.shape
+    kb, n = b.shape
+    c = torch.empty((m, n), dtype=torch.int32, device=a.device)
+    ca = torch.empty((m + 1, n + 1), dtype=torch.int64, device=a.device)
+    row, col = VerifyOutcome(), VerifyOutcome()
+    _sync()
+    call("abed_abft_gemm_i8", _p(a), m, k, _p(b), kb, n, _p(c), _p(ca), C.byref(row), C.byref(col))
+    return c, ca, row, col
+
+
+def abft_check(c_aug):
+    """abft_check (abft_gemm.hpp:70-96) on an int64 (m+1) x (n+1) CUDA tensor -> (row, col)."""
+    row, col = VerifyOutcome(), VerifyOutcome()
+    _sync()
+    call("abed_abft_check", _p(c_aug), c_aug.shape[0], c_aug.shape[1], C.byref(row), C.byref(col))
+    return row, col
+
+
+class AbftPlan:
+    """Allocation-free ABFT GEMM runs on the current stream (timing, graphs).
+    mode ABFT_CHECKED: the reference's online tasks (2)-(6); ABFT_PLAIN: the same
+    GEMM without checksums; ABFT_FUSED_ROW: row check fused into the GEMM epilogue."""
+
+    def __init__(self, m, n, k):
+        self.m, self.n, self.k = m, n, k
+        h = C.c_void_p()
+        call("abed_abft_plan_create", m, n, k, C.byref(h))
+        self.h = h
+        self.outcomes = torch.zeros(2 * C.sizeof(VerifyOutcome), dtype=torch.uint8, device="cuda")
+
+    def run(self, a, b, c=None, c_aug=None, mode=ABFT_CHECKED):
+        call("abed_abft_plan_run", self.h, _p(a), _p(b) if b is not None else None, _p(c) if c is not None else None,
+             _p(c_aug) if c_aug is not None else None, _p(self.outcomes), mode, _stream())
+
+    def verdicts(self):
+        raw = self.outcomes.cpu().numpy().tobytes()
+        sz = C.sizeof(VerifyOutcome)
+        return VerifyOutcome.from_buffer_copy(raw[:sz]), VerifyOutcome.from_buffer_copy(raw[sz:])
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h is not None and h.value and abi is not None and abi._lib is not None:
+            abi._lib.abed_abft_plan_destroy(h)
+            self.h = None
+
+
 class ConvPlan:
     """One protected layer: packed filters (+ FC checksum-digit rows), the offline
     filter checksum and the per-tile verification workspace."""

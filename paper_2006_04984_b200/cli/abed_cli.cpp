@@ -3,8 +3,10 @@
 // convolution, checksum, verdict and fault-injection trial runs through
 // libabed_b200.so.  Same flags, the same CSV / JSON report schemas and the same
 // exit codes (0 success, 1 usage / config / IO error, 2 verification mismatch,
-// abed_main.cpp:29-31).  `cost` and `abft` (the analytic cost model and the
-// ABFT-GEMM study) are not part of the protected-conv path and are not provided.
+// abed_main.cpp:29-31), plus `abft` (abed_main.cpp:425-487), the row/column
+// checksum ABFT-GEMM comparison, whose GEMMs and checks run on the B200 too.
+// `cost` (the analytic cost model) is not part of the protected-conv path and is
+// not provided.
 //
 // Flags are parsed by hand (the reference uses CLI11, which this image lacks);
 // the JSON reports use nlohmann/json like the reference.
@@ -340,6 +342,53 @@ int run_inject(const Args& a) {
   return kExitOk;
 }
 
+// abed_main.cpp:436-487 run_abft: per trial a fresh SplitMix64(derive_seed(seed, t))
+// draws A, B, then (i, j, bit) of a single c_aug corruption; same CSV / JSON schema
+int run_abft(const Args& a) {
+  const std::int64_t m = to_i64(a.get("--m", "64"), "--m"), n = to_i64(a.get("--n", "64"), "--n");
+  const std::int64_t k = to_i64(a.get("--k", "64"), "--k"), trials = to_i64(a.get("--trials", "1000"), "--trials");
+  if (m < 1 || n < 1 || k < 1 || trials < 1) throw UsageError("--m/--n/--k/--trials must be positive");
+  const std::uint64_t seed = static_cast<std::uint64_t>(to_i64(a.get("--seed", "1"), "--seed"));
+  const bool single_pass = a.flags.count("--single-pass") != 0;
+  std::int64_t faultfree_pass = 0, detected = 0;
+  for (std::int64_t t = 0; t < trials; ++t) {
+    SplitMix64 rng(derive_seed(seed, static_cast<std::uint64_t>(t)));
+    Matrix am(m, k, ElemKind::I8), bm(k, n, ElemKind::I8);
+    for (auto& v : am.view<std::int8_t>()) v = rng.next_i8();
+    for (auto& v : bm.view<std::int8_t>()) v = rng.next_i8();
+    AbftResult result = abft_gemm(am, bm, single_pass);
+    if (result.pass()) ++faultfree_pass;
+    const auto i = static_cast<std::int64_t>(rng.below(static_cast<std::uint64_t>(m)));
+    const auto j = static_cast<std::int64_t>(rng.below(static_cast<std::uint64_t>(n)));
+    const int bit = static_cast<int>(rng.below(63));
+    result.c_aug.at<std::int64_t>(i, j) ^= std::int64_t{1} << bit;
+    const auto [row_check, col_check] = abft_check(result.c_aug);
+    if (!row_check.pass() || !col_check.pass()) ++detected;
+  }
+  const AbftCosts costs = abft_costs(m, n, k, single_pass);
+  const double rate = static_cast<double>(detected) / static_cast<double>(trials);
+  std::ostringstream csv;
+  csv << "m,n,k,trials,faultfree_pass,detected,detection_rate,copy_elements,seed\n";
+  csv << m << "," << n << "," << k << "," << trials << "," << faultfree_pass << "," << detected << "," << rate << ","
+      << costs.copy_elements() << "," << seed << "\n";
+  csv << "task,ops,read_bytes,write_bytes,elements_moved\n";
+  nlohmann::json tasks = nlohmann::json::array();
+  for (const auto& task : costs.tasks) {
+    csv << task.name << "," << task.ops << "," << task.read_bytes << "," << task.write_bytes << ","
+        << task.elements_moved << "\n";
+    tasks.push_back({{"task", std::string(task.name)},
+                     {"ops", task.ops},
+                     {"read_bytes", task.read_bytes},
+                     {"write_bytes", task.write_bytes},
+                     {"elements_moved", task.elements_moved}});
+  }
+  const nlohmann::json doc{{"m", m}, {"n", n}, {"k", k}, {"trials", trials}, {"faultfree_pass", faultfree_pass},
+                           {"detected", detected}, {"detection_rate", rate}, {"copy_elements", costs.copy_elements()},
+                           {"tasks", tasks}, {"seed", seed}};
+  emit(a, csv.str(), doc);
+  return kExitOk;
+}
+
 const std::set<std::string> kLayerOpts = {"--config", "--network", "--image", "--layer", "--cap-hw", "--out"};
 
 std::set<std::string> with(std::set<std::string> base, std::initializer_list<const char*> more) {
@@ -357,6 +406,7 @@ void usage(std::ostream& os) {
         "  abed_b200 inject (--network NAME [--image ..] | --config FILE) --layer ID --scheme fc|ic|fic\n"
         "            --target input|filter|convout [--trials N] [--seed S] [--mode ones|random] [--jobs J]\n"
         "            [--scale X] [--cap-hw N] [--json] [--out FILE]\n"
+        "  abed_b200 abft [--m M] [--n N] [--k K] [--trials T] [--seed S] [--single-pass] [--json] [--out FILE]\n"
         "exit codes: 0 success, 1 usage/config/IO error, 2 verification mismatch\n";
 }
 
@@ -386,6 +436,10 @@ int main(int argc, char** argv) {
                                              "--scale"}),
                            {"--json"});
       return run_inject(a);
+    }
+    if (cmd == "abft") {
+      const Args a = parse(argc, argv, {"--m", "--n", "--k", "--trials", "--seed", "--out"}, {"--single-pass", "--json"});
+      return run_abft(a);
     }
     std::cerr << "error: unknown subcommand '" << cmd << "'\n";
     usage(std::cerr);

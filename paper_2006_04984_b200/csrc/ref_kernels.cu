@@ -507,6 +507,10 @@ void dev_colsum_i8(const int8_t* x, int64_t rows, int64_t len, int32_t* out, cud
     int64_t splits = ((int64_t)num_sms() * 8) / col_tiles;
     const int64_t max_splits = (rows + kColsumWarps - 1) / kColsumWarps;  // >= one row per warp
     if (splits > max_splits) splits = max_splits;
+    // every split adds one integer atomic per column: same-address atomics
+    // serialise in L2 (394 splits over 1152 columns measured 38 us for 29 MB),
+    // so cap the contention per column
+    if (splits > 64) splits = 64;
     if (splits < 1) splits = 1;
     const int64_t rows_per = (rows + splits - 1) / splits;
     splits = (rows + rows_per - 1) / rows_per;

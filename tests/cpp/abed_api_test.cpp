@@ -1,5 +1,5 @@
 // Drop-in API tests: the assertions of the reference's own suites
-// (/root/reference/proj/tests/{tensor,convolution,checksum,faults}_test.cpp),
+// (/root/reference/proj/tests/{tensor,convolution,checksum,faults,abft_gemm}_test.cpp),
 // restated against include/abed/*.hpp, whose compute runs on the B200.
 // "Host*" suites touch no device (run on CPU); the rest need a GPU.
 #include <abed/abed.hpp>
@@ -304,6 +304,97 @@ TEST(Campaign, AcceptanceCountsAndDeterminism) {
   EXPECT_EQ(a.detected + b.detected, r.detected);
   c.trials = 0;
   EXPECT_THROW(run_campaign(c), std::invalid_argument);
+}
+
+// ------------------------------------------------------------------ abft_gemm_test.cpp
+namespace {
+Matrix random_matrix(std::int64_t rows, std::int64_t cols, SplitMix64& rng) {
+  Matrix m(rows, cols, ElemKind::I8);
+  for (auto& v : m.view<std::int8_t>()) v = rng.next_i8();
+  return m;
+}
+}  // namespace
+
+TEST(HostAbftCosts, CostAccounting) {  // abft_gemm_test.cpp:87-98 + the reference's numbers (tests/golden/abft.json)
+  const std::int64_t m = 7, n = 5, k = 9;
+  const AbftCosts costs = abft_costs(m, n, k);
+  EXPECT_EQ(costs.tasks[2].ops, (m + 1) * (n + 1) * k);
+  EXPECT_EQ(costs.copy_elements(), m * k + k * n + 2 * m * n);
+  EXPECT_EQ(costs.tasks[0].elements_moved, m * k + k * n);
+  EXPECT_EQ(costs.tasks[4].elements_moved, 2 * m * n);
+  const AbftCosts one_pass = abft_costs(m, n, k, true);
+  EXPECT_LT(one_pass.tasks[3].read_bytes, costs.tasks[3].read_bytes);
+  EXPECT_EQ(one_pass.tasks[2].ops, costs.tasks[2].ops);
+  const std::int64_t want[5][4] = {{0, 108, 432, 108}, {90, 108, 72, 0}, {432, 504, 384, 0}, {82, 768, 8, 0},
+                                   {0, 280, 140, 70}};
+  for (int t = 0; t < 5; ++t) {
+    EXPECT_EQ(costs.tasks[t].ops, want[t][0]);
+    EXPECT_EQ(costs.tasks[t].read_bytes, want[t][1]);
+    EXPECT_EQ(costs.tasks[t].write_bytes, want[t][2]);
+    EXPECT_EQ(costs.tasks[t].elements_moved, want[t][3]);
+  }
+  EXPECT_EQ(abft_costs(16, 12, 20).copy_elements(), 944);  // cli_test.cpp:143
+}
+
+TEST(AbftGemm, IdentityPasses) {
+  Matrix eye(2, 2, ElemKind::I8);
+  eye.at<std::int8_t>(0, 0) = 1;
+  eye.at<std::int8_t>(1, 1) = 1;
+  const AbftResult result = abft_gemm(eye, eye);
+  EXPECT_TRUE(result.pass());
+  EXPECT_EQ(result.c.at<std::int32_t>(0, 0), 1);
+  EXPECT_EQ(result.c.at<std::int32_t>(0, 1), 0);
+  EXPECT_EQ(result.c.at<std::int32_t>(1, 1), 1);
+  EXPECT_EQ(result.c_aug.at<std::int64_t>(2, 2), 2);
+}
+
+TEST(AbftGemm, SingleCorruptionFlagsRowAndColumn) {
+  SplitMix64 rng(7);
+  const Matrix a = random_matrix(6, 5, rng);
+  const Matrix b = random_matrix(5, 4, rng);
+  AbftResult result = abft_gemm(a, b);
+  EXPECT_TRUE(result.pass());
+  result.c_aug.at<std::int64_t>(2, 3) ^= std::int64_t{1} << 17;
+  const auto [row_check, col_check] = abft_check(result.c_aug);
+  EXPECT_FALSE(row_check.pass());
+  EXPECT_FALSE(col_check.pass());
+  EXPECT_TRUE(row_check.locus.has_value() && (*row_check.locus)[0] == 2);
+  EXPECT_TRUE(col_check.locus.has_value() && (*col_check.locus)[0] == 3);
+}
+
+TEST(AbftGemm, ChecksumRowMatchesColumnSumOracleAndRandomInstances) {
+  SplitMix64 rng(8);
+  const Matrix a = random_matrix(8, 8, rng);
+  const Matrix b = random_matrix(8, 8, rng);
+  const AbftResult result = abft_gemm(a, b);
+  EXPECT_TRUE(result.pass());
+  for (std::int64_t j = 0; j < 8; ++j) {
+    std::int64_t col_sum = 0;
+    for (std::int64_t i = 0; i < 8; ++i) {
+      std::int64_t c = 0;
+      for (std::int64_t t = 0; t < 8; ++t) c += a.at<std::int8_t>(i, t) * b.at<std::int8_t>(t, j);
+      EXPECT_EQ(result.c.at<std::int32_t>(i, j), c);
+      col_sum += c;
+    }
+    EXPECT_EQ(result.c_aug.at<std::int64_t>(8, j), col_sum);
+  }
+  SplitMix64 r9(9);
+  for (int iter = 0; iter < 50; ++iter) {
+    const std::int64_t m = 1 + static_cast<std::int64_t>(r9.below(16));
+    const std::int64_t k = 1 + static_cast<std::int64_t>(r9.below(16));
+    const std::int64_t n = 1 + static_cast<std::int64_t>(r9.below(16));
+    const Matrix x = random_matrix(m, k, r9), y = random_matrix(k, n, r9);
+    EXPECT_TRUE(abft_gemm(x, y).pass());
+  }
+}
+
+TEST(AbftGemm, Guards) {
+  Matrix a(2, 3, ElemKind::I8);
+  Matrix b(4, 2, ElemKind::I8);
+  EXPECT_THROW(abft_gemm(a, b), std::invalid_argument);
+  Matrix a32(2, 2, ElemKind::I32);
+  Matrix b32(2, 2, ElemKind::I32);
+  EXPECT_THROW(abft_gemm(a32, b32), std::invalid_argument);
 }
 
 int main(int argc, char** argv) { return mini_gtest::run_all(argc, argv); }

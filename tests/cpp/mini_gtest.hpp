@@ -77,6 +77,7 @@ void cmp(const A& a, const B& b, Op op, const char* text, const char* file, int 
 #define EXPECT_GT(a, b) MG_CMP(a, b, >, false)
 #define EXPECT_GE(a, b) MG_CMP(a, b, >=, false)
 #define EXPECT_LE(a, b) MG_CMP(a, b, <=, false)
+#define EXPECT_LT(a, b) MG_CMP(a, b, <, false)
 #define EXPECT_TRUE(c) \
   do { if (!(c)) mini_gtest::fail(__FILE__, __LINE__, "expected true: " #c, false); } while (0)
 #define ASSERT_TRUE(c) \

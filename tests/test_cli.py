@@ -156,3 +156,21 @@ def test_inject_reproduces_reference_campaign(cli):
         assert [int(v) for v in row[3:7]] == c["counts"], (c, row)
         done += 1
     assert done == 6
+
+
+@pytest.mark.parametrize("args", ["abft --m 0", "abft --k x", "abft --trials 5 --bogus"])
+def test_abft_usage_errors_exit_1(cli, args):
+    code, out = run(cli, args)
+    assert code == 1 and "error" in out, out
+
+
+@pytest.mark.gpu
+def test_abft_report_and_copy_accounting(cli):  # cli_test.cpp:138-147
+    code, out = run(cli, "abft --m 16 --n 12 --k 20 --trials 25 --seed 9")
+    assert code == 0, out
+    assert "m,n,k,trials,faultfree_pass,detected,detection_rate,copy_elements,seed" in out
+    assert "16,12,20,25,25,25,1,944,9" in out
+    assert "copy_in," in out and "gemm," in out
+    code, out = run(cli, "abft --m 16 --n 12 --k 20 --trials 3 --seed 9 --single-pass --json")
+    doc = json.loads(out)
+    assert code == 0 and doc["copy_elements"] == 944 and doc["detected"] == 3 and len(doc["tasks"]) == 5
