@@ -47,6 +47,8 @@ bool choose_tiling(const abed_dev::ActGeom& g, bool fc, int force_block_n, abed_
 int num_sms();
 
 __global__ void pack_input_kernel(const int8_t* x, abed_dev::ActGeom g, int8_t* out);
+// NCHW -> strip planes (vectorised 4-pixel quads; plan.cu)
+void launch_pack_input(const int8_t* x, const abed_dev::ActGeom& g, int8_t* packed, cudaStream_t st);
 __global__ void pack_filters_kernel(const int8_t* f, abed_dev::ActGeom g, int block_n, int block_n_tot,
                                     int n_tiles, int gps, int k_stages, int fc, int8_t* out);
 __global__ void batch_sum_packed_kernel(const int8_t* act, abed_dev::ActGeom g, int32_t* bsum);

@@ -498,8 +498,7 @@ int abed_conv_plan_info(const abed_conv_plan* pl, abed_plan_info* info) {
 }
 int abed_pack_input(const abed_conv_plan* pl, const int8_t* input, int8_t* packed, void* stream) {
   return guarded([&] {
-    const int64_t n16 = geom_packed_bytes(pl->g) / 16;
-    pack_input_kernel<<<grid_for(n16), 256, 0, (cudaStream_t)stream>>>(input, pl->g, packed);
+    launch_pack_input(input, pl->g, packed, (cudaStream_t)stream);
     cuda_check(cudaGetLastError(), "pack_input");
   });
 }
@@ -566,8 +565,7 @@ int abed_conv_i8(const int8_t* input, const int8_t* filters, const abed_layer_sh
     int8_t* packed = nullptr;
     try {
       cuda_check(cudaMalloc(&packed, geom_packed_bytes(pl->g)), "cudaMalloc(packed)");
-      const int64_t n16 = geom_packed_bytes(pl->g) / 16;
-      pack_input_kernel<<<grid_for(n16), 256, 0, st>>>(input, pl->g, packed);
+      launch_pack_input(input, pl->g, packed, st);
       plan_run(pl, packed, nullptr, ABED_OUT_I32_NCHW, convout, nullptr, -1, 0, st);
       cuda_check(cudaStreamSynchronize(st), "conv_i8 sync");
     } catch (...) {

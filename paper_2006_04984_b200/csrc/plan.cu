@@ -95,6 +95,121 @@ __global__ void pack_input_kernel(const int8_t* __restrict__ x, ActGeom g, int8_
 }
 
 // ---------------------------------------------------------------------------
+// pack_input, vectorised: one thread per four consecutive pixels of ONE M-space
+// row of one plane (quads are aligned to row starts, so no quad crosses a row).
+// For a unit-stride phase each channel's four source bytes are contiguous in the
+// NCHW row: two aligned 32-bit loads + a funnel shift fetch them, halo / edge
+// pixels are masked arithmetically (no divergent per-pixel path), and a 4x4 byte
+// transpose (__byte_perm) turns the 16 channel words into four 16-byte pixels:
+// 32 loads per 64 output bytes instead of 64 byte loads.  Strided phases gather
+// bytes.  Pixels past the last image (plane tail) are zero-filled.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void transpose_store4(const uint32_t (&cw)[16], uint4* dst, int n_pix) {
+  uint32_t o[4][4];  // [pixel][channel word q]
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint32_t a0 = __byte_perm(cw[4 * q], cw[4 * q + 1], 0x5140);      // c0p0 c1p0 c0p1 c1p1
+    const uint32_t a1 = __byte_perm(cw[4 * q], cw[4 * q + 1], 0x7362);      // c0p2 c1p2 c0p3 c1p3
+    const uint32_t b0 = __byte_perm(cw[4 * q + 2], cw[4 * q + 3], 0x5140);  // c2p0 c3p0 c2p1 c3p1
+    const uint32_t b1 = __byte_perm(cw[4 * q + 2], cw[4 * q + 3], 0x7362);  // c2p2 c3p2 c2p3 c3p3
+    o[0][q] = __byte_perm(a0, b0, 0x5410);
+    o[1][q] = __byte_perm(a0, b0, 0x7632);
+    o[2][q] = __byte_perm(a1, b1, 0x5410);
+    o[3][q] = __byte_perm(a1, b1, 0x7632);
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+    if (u < n_pix) dst[u] = make_uint4(o[u][0], o[u][1], o[u][2], o[u][3]);
+}
+
+__global__ void pack_input_v4_kernel(const int8_t* __restrict__ x, ActGeom g, int64_t x_bytes, int vec_ok,
+                                     int8_t* __restrict__ out) {
+  const int qpr = (g.Wl + 3) >> 2;                       // quads per M-space row
+  const int64_t rows = (int64_t)g.n * g.Hl;
+  const int64_t planes = (int64_t)g.n_phase * g.c16;
+  const int64_t body = planes * rows * qpr;
+  const int64_t tail_pix = g.plane_len - g.m_total;       // zero pixels after the last image
+  const int64_t tail_q = (tail_pix + 3) >> 2;
+  const int64_t total = body + planes * tail_q;
+  const int64_t HW = (int64_t)g.h * g.w;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    if (idx >= body) {
+      const int64_t k = idx - body;
+      const int64_t plane = k / tail_q, t0 = g.m_total + (k % tail_q) * 4;
+      uint4* dst = reinterpret_cast<uint4*>(out) + plane * g.plane_len + t0;
+      const int np = (int)(g.plane_len - t0 < 4 ? g.plane_len - t0 : 4);
+      for (int u = 0; u < np; ++u) dst[u] = make_uint4(0, 0, 0, 0);
+      continue;
+    }
+    const int qi = (int)(idx % qpr);
+    const int64_t rest = idx / qpr;
+    const int64_t row = rest % rows;  // n * Hl + i
+    const int64_t plane = rest / rows;
+    const int grp = (int)(plane % g.c16);
+    const int phase = (int)(plane / g.c16);
+    const int n = (int)(row / g.Hl), i = (int)(row % g.Hl);
+    const int j0 = qi * 4;
+    const int n_pix = min(4, g.Wl - j0);
+    uint4* dst = reinterpret_cast<uint4*>(out) + plane * g.plane_len + row * g.Wl + j0;
+    const int a = phase / g.nph_w, b = phase % g.nph_w;
+    const int hh = i * g.sh + a - g.ph;
+    const int ww0 = j0 * g.sw + b - g.pw;
+    uint32_t cw[16];
+    if (hh < 0 || hh >= g.h || grp * 16 >= g.c) {
+#pragma unroll
+      for (int e = 0; e < 16; ++e) cw[e] = 0;
+    } else {
+      // byte mask of the pixels whose source column lies inside the image
+      uint32_t keep = 0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int ww = ww0 + u * g.sw;
+        if (u < n_pix && ww >= 0 && ww < g.w) keep |= 0xFFu << (8 * u);
+      }
+      const int64_t row0 = ((int64_t)n * g.c + grp * 16) * HW + (int64_t)hh * g.w;
+      if (g.sw == 1 && vec_ok) {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          uint32_t v = 0;
+          if (grp * 16 + e < g.c && keep) {
+            const int64_t off = row0 + (int64_t)e * HW + ww0;
+            const int64_t al = off & ~int64_t(3);
+            const uint32_t lo = al >= 0 ? __ldg(reinterpret_cast<const uint32_t*>(x + al)) : 0u;
+            const uint32_t hi = al + 4 < x_bytes ? __ldg(reinterpret_cast<const uint32_t*>(x + al + 4)) : 0u;
+            v = __funnelshift_r(lo, hi, (uint32_t)(off & 3) * 8) & keep;
+          }
+          cw[e] = v;
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          uint32_t v = 0;
+          if (grp * 16 + e < g.c) {
+            const int8_t* src = x + row0 + (int64_t)e * HW;
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if ((keep >> (8 * u)) & 1u) v |= (uint32_t)(uint8_t)__ldg(src + ww0 + u * g.sw) << (8 * u);
+          }
+          cw[e] = v;
+        }
+      }
+    }
+    transpose_store4(cw, dst, n_pix);
+  }
+}
+
+void launch_pack_input(const int8_t* x, const ActGeom& g, int8_t* packed, cudaStream_t st) {
+  const int64_t quads = (int64_t)g.n_phase * g.c16 * ((int64_t)g.n * g.Hl * ((g.Wl + 3) / 4) + g.plane_len / 4);
+  const int64_t x_bytes = (int64_t)g.n * g.c * g.h * g.w;
+  int64_t blocks = (quads + 255) / 256;
+  const int64_t cap = (int64_t)num_sms() * 16;
+  if (blocks > cap) blocks = cap;
+  const int vec_ok = (reinterpret_cast<uintptr_t>(x) & 3) == 0;  // aligned 32-bit source loads
+  pack_input_v4_kernel<<<(unsigned)blocks, 256, 0, st>>>(x, g, x_bytes, vec_ok, packed);
+}
+
+// ---------------------------------------------------------------------------
 // pack_filters: B blocks [nt][ks][tap][gl][row][16B]; rows >= block_n hold the
 // balanced base-256 digits of the per-N-tile filter checksum
 // fsum_nt[c,r,s] = sum_{k in tile} f[k,c,r,s]  (checksum.hpp:75-90 restricted to

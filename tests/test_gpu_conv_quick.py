@@ -41,3 +41,27 @@ def test_conv_i8_matches_exact(dims):
     got = out.cpu().to(torch.int64)
     bad = (got != want).nonzero()
     assert bad.numel() == 0, f"{bad.shape[0]} mismatches, first {bad[:4].tolist()} got {got.flatten()[:8]} want {want.flatten()[:8]}"
+
+
+@pytest.mark.parametrize("dims", SHAPES + [(2, 20, 13, 17, 16, 3, 3, 1, 1, 1, 1), (1, 16, 9, 6, 16, 1, 1, 1, 1, 0, 0)])
+def test_pack_input_vector_path_equals_byte_path(dims):
+    """abed_pack_input's 4-pixel vector path (aligned source) and its per-pixel
+    gather (the same tensor at an odd address) give identical strip planes, and the
+    conv on them is exact."""
+    from paper_2006_04984_b200 import api
+    ls = abi.layer_shape(*dims)
+    g = torch.Generator().manual_seed(7 + sum(dims))
+    x = torch.randint(-128, 128, ls.input_dims(), dtype=torch.int8, generator=g).cuda()
+    f = torch.randint(-128, 128, ls.filter_dims(), dtype=torch.int8, generator=g).cuda()
+    plan = api.ConvPlan(ls, f, 0)
+    a = plan.pack(x, plan.packed_buffer())
+    raw = torch.empty(x.numel() + 1, dtype=torch.int8, device="cuda")
+    raw[1:].copy_(x.flatten())
+    b = plan.packed_buffer()
+    abi.call("abed_pack_input", plan.handle, raw.data_ptr() + 1, b.data_ptr(), None)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    out = torch.empty(ls.output_dims(), dtype=torch.int32, device="cuda")
+    plan.run(a, out, abi.OUT_I32_NCHW)
+    torch.cuda.synchronize()
+    assert torch.equal(out.cpu().to(torch.int64), ref_conv(x.cpu(), f.cpu(), ls))
