@@ -24,6 +24,10 @@ namespace abed_dev {
 // checksum.hpp:211-236; fc_verify_f32 :541-565); FIC: lhs = sum of the outputs,
 // rhs = fic_dot (fic_verify :287-294; fic_verify_f32 / float_verify :474-539).
 __global__ void __launch_bounds__(256) verdict_kernel(const __grid_constant__ VerdictBatch b) {
+  // launched as a programmatic dependent of the last conv kernel (which triggers
+  // its dependents early): the launch overlaps that kernel's tail, and this wait
+  // returns once it has completed and its records are visible
+  pdl_wait();
   const VerdictJob& j = b.job[blockIdx.x];
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   __shared__ FcRec s_fc[8];
@@ -160,8 +164,16 @@ cudaError_t verdict_launch(const abed_dev::VerdictJob* jobs, int n, cudaStream_t
     abed_dev::VerdictBatch b{};
     b.n = n - i < abed_dev::kMaxVerdictJobs ? n - i : abed_dev::kMaxVerdictJobs;
     for (int k = 0; k < b.n; ++k) b.job[k] = jobs[i + k];
-    abed_dev::verdict_kernel<<<b.n, 256, 0, stream>>>(b);
-    const cudaError_t e = cudaGetLastError();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(b.n);
+    cfg.blockDim = dim3(256);
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, abed_dev::verdict_kernel, b);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;

@@ -242,7 +242,7 @@ struct EpiCtx {
 // One 16-channel chunk of one row: (slow path only: fault hook, filler trim,
 // IC sums), row sum, requantise + store (or compare).  Returns the chunk's
 // contribution to the row sum.  b = the chunk's 16 biases.
-template <int EPI, bool RELU, bool SUMS, bool SLOW>
+template <int EPI, bool RELU, bool SUMS, bool SLOW, bool C32 = false>
 __device__ __forceinline__ int64_t epi_chunk(const ConvTcParams& p, const EpiCtx& e, int32_t (&a)[16],
                                              const float (&b)[16], int k0, long long& af_out) {
   if (SLOW) {
@@ -257,7 +257,10 @@ __device__ __forceinline__ int64_t epi_chunk(const ConvTcParams& p, const EpiCtx
   }
   int64_t sum = 0;
   if (SUMS) {
-    if (e.chunk32) {
+    // C32 (compile time, chosen per layer from e.chunk32): the 16-value chunk sum
+    // in int32 (exact when CRS < 8192) -- a runtime flag here made the compiler
+    // evaluate both the int32 and the sign-extended int64 chains (~2.7 instr/value)
+    if constexpr (C32) {
       int32_t s = 0;
 #pragma unroll
       for (int j = 0; j < 16; ++j) s += a[j];
@@ -435,7 +438,7 @@ __device__ __forceinline__ void load_bias16(const ConvTcParams& p, const EpiCtx&
 // processed) and the biases are read before the wait.  The loop body is not
 // unrolled across steps, so the epilogue stays resident in the instruction cache.
 // An odd trailing chunk is loaded as a 16-column step.
-template <int DT, int EPI, bool RELU, bool SUMS, bool SLOW>
+template <int DT, int EPI, bool RELU, bool SUMS, bool SLOW, bool C32 = false>
 __device__ __forceinline__ std::conditional_t<DT == DT_I8, int64_t, double> epi_columns(
     const ConvTcParams& p, const EpiCtx& e, uint32_t t_row, int k_base, int c_lo, int c_hi, long long& af_out) {
   std::conditional_t<DT == DT_I8, int64_t, double> row_sum = 0;
@@ -444,7 +447,7 @@ __device__ __forceinline__ std::conditional_t<DT == DT_I8, int64_t, double> epi_
       int32_t a[16];
 #pragma unroll
       for (int j = 0; j < 16; ++j) a[j] = static_cast<int32_t>(v[j]);
-      row_sum += epi_chunk<EPI, RELU, SUMS, SLOW>(p, e, a, b, k0, af_out);
+      row_sum += epi_chunk<EPI, RELU, SUMS, SLOW, C32>(p, e, a, b, k0, af_out);
     } else {
       row_sum += epi_chunk_h<DT, EPI, RELU, SUMS, SLOW>(p, e, v, b, k0);
     }
@@ -1057,6 +1060,10 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
       } else if (!slow) {
         if (p.dbg & 64)
           row_sum = epi_columns<DT, EPI, true, false, false>(p, e, t_row, k_base, c_lo, c_hi, af_sum);
+        else if (DT == DT_I8 && (FC || FIC) && e.chunk32)
+          row_sum = p.relu
+                        ? epi_columns<DT, EPI, true, FC || FIC, false, true>(p, e, t_row, k_base, c_lo, c_hi, af_sum)
+                        : epi_columns<DT, EPI, false, FC || FIC, false, true>(p, e, t_row, k_base, c_lo, c_hi, af_sum);
         else
           row_sum = p.relu ? epi_columns<DT, EPI, true, FC || FIC, false>(p, e, t_row, k_base, c_lo, c_hi, af_sum)
                            : epi_columns<DT, EPI, false, FC || FIC, false>(p, e, t_row, k_base, c_lo, c_hi, af_sum);

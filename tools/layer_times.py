@@ -28,7 +28,7 @@ def main():
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     variants = [("unprotected", 0, 0, 0), ("fic", abi.CHECK_FIC, 0, 0), ("fic-reuse-rhs", abi.CHECK_FIC, 1, 0),
                 ("fic-reuse-novd", abi.CHECK_FIC, 1, 32), ("fic-reuse-nosum", abi.CHECK_FIC, 1, 64),
-                ("fic-reuse-none", abi.CHECK_FIC, 1, 96), ("fc", abi.CHECK_FC, 0, 0)]
+                ("fic-reuse-none", abi.CHECK_FIC, 1, 96), ("fc", abi.CHECK_FC, 0, 0), ("fic-staged", abi.CHECK_FIC, 0, -1)]
     print(f"{'layer':15s} " + " ".join(f"{v[0]:>15s}" for v in variants) + "   (us per launch)")
     for li, (name, c, h, w, k, st) in enumerate(RESNET50_3X3):
         if only and name not in only:
@@ -39,6 +39,9 @@ def main():
         row = []
         for vname, checks, reuse, dbg in variants:
             pl = api.ConvPlan(ls, f, checks)
+            if dbg < 0:
+                pl.set_input_checksum_source(abi.RHS_STAGED)
+                dbg = 0
             packed = pl.pack(x)
             out = torch.zeros(ls.n * k * (ls.p + 1) * (ls.q + 1) + 65536, dtype=torch.int8, device="cuda")
             ep = pl.epilog_params(0.05, torch.linspace(-2, 2, k), True)
