@@ -373,8 +373,16 @@ __device__ __forceinline__ double epi_chunk_h(const ConvTcParams& p, const EpiCt
   for (int j = 0; j < 16; ++j) a[j] = __uint_as_float(v[j]);
   double sum = 0.0;
   if (SUMS) {
+    // f32 pairwise tree over the chunk, one conversion, f64 across chunks: 16
+    // F2F.F64 + 16 DADD per chunk cost VGG-16 conv1_2 ~75 us.  The tree adds at
+    // most 4 * 2^-24 * sum|out| to the lhs error, inside the thresholds' slack
+    // ((CRS + 32) * 2^-22 per output, bench.py / DESIGN.md)
+    float t8[8];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) sum += static_cast<double>(a[j]);
+    for (int j = 0; j < 8; ++j) t8[j] = a[2 * j] + a[2 * j + 1];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) t8[j] = t8[2 * j] + t8[2 * j + 1];
+    sum = static_cast<double>((t8[0] + t8[1]) + (t8[2] + t8[3]));
   }
   if (EPI == EPI_PACKED || EPI == EPI_COMPARE) {
     float y[16];
@@ -662,26 +670,32 @@ __device__ __forceinline__ void fic_rhs_fr(const ConvTcParams& p, int64_t first,
       const uint4* src = reinterpret_cast<const uint4*>(p.act) + plane * p.plane_len + pix;
       const int n0 = static_cast<int>(static_cast<int64_t>(p.N) * split / nsplit);
       const int n1 = static_cast<int>(static_cast<int64_t>(p.N) * (split + 1) / nsplit);
-      float item = 0.0f;
-      for (int n = n0; n < n1; n += 4) {
-        uint4 x[4];
+      // DEPTH image loads in flight and four independent FMA chains: with one
+      // chain and four loads the two input-checksum warps of a busy SM moved
+      // ~1.6 TB/s machine-wide (VGG-16 conv1_2: the re-read took longer than the conv)
+      constexpr int kD = DEPTH < 8 ? 8 : DEPTH;
+      float acc4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+      for (int n = n0; n < n1; n += kD) {
+        uint4 x[kD];
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < kD; ++j)
           x[j] = n + j < n1 ? __ldcg(src + static_cast<int64_t>(n + j) * HlWl) : make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < kD; ++j) {
           const float2 x0 = unpack_h2<DT>(x[j].x), x1 = unpack_h2<DT>(x[j].y), x2 = unpack_h2<DT>(x[j].z),
                        x3 = unpack_h2<DT>(x[j].w);
-          item = __fmaf_rn(x0.x, ga.x, item);
-          item = __fmaf_rn(x0.y, ga.y, item);
-          item = __fmaf_rn(x1.x, ga.z, item);
-          item = __fmaf_rn(x1.y, ga.w, item);
-          item = __fmaf_rn(x2.x, gb.x, item);
-          item = __fmaf_rn(x2.y, gb.y, item);
-          item = __fmaf_rn(x3.x, gb.z, item);
-          item = __fmaf_rn(x3.y, gb.w, item);
+          float& a = acc4[j & 3];
+          a = __fmaf_rn(x0.x, ga.x, a);
+          a = __fmaf_rn(x0.y, ga.y, a);
+          a = __fmaf_rn(x1.x, ga.z, a);
+          a = __fmaf_rn(x1.y, ga.w, a);
+          a = __fmaf_rn(x2.x, gb.x, a);
+          a = __fmaf_rn(x2.y, gb.y, a);
+          a = __fmaf_rn(x3.x, gb.z, a);
+          a = __fmaf_rn(x3.y, gb.w, a);
         }
       }
+      const float item = (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
       facc_rhs += static_cast<double>(item);
     }
   } else {
@@ -1168,7 +1182,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
     double facc_rhs = 0.0;
     if (DT != DT_I8 && FIC && p.rhs_mode == 1 && p.ic_ctas == 0) {
       pdl_wait();
-      fic_rhs_fr<DT>(p, static_cast<int64_t>(blockIdx.x) * (kRhsWarps * 32) + rw * 32 + lane,
+      fic_rhs_fr<DT, DT == DT_I8 ? 8 : 16>(p, static_cast<int64_t>(blockIdx.x) * (kRhsWarps * 32) + rw * 32 + lane,
                      static_cast<int64_t>(p.conv_grid) * (kRhsWarps * 32), acc, facc_rhs);
     } else if (rhs_staged) {
       // FIC-SM: the same sum x * G, with x taken from the A stages the producer
@@ -1281,7 +1295,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
       }
     } else if (DT == DT_I8 && FIC && p.rhs_mode == 1 && p.ic_ctas == 0) {
       pdl_wait();
-      fic_rhs_fr<DT>(p, static_cast<int64_t>(blockIdx.x) * (kRhsWarps * 32) + rw * 32 + lane,
+      fic_rhs_fr<DT, DT == DT_I8 ? 8 : 16>(p, static_cast<int64_t>(blockIdx.x) * (kRhsWarps * 32) + rw * 32 + lane,
                      static_cast<int64_t>(p.conv_grid) * (kRhsWarps * 32), acc, facc_rhs);
     } else {
       pdl_wait();
