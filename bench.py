@@ -899,30 +899,46 @@ def run_ours(args, world, rank, local):
                 with torch.cuda.stream(s_out):
                     host_out[i].copy_(dev_out[i], non_blocking=True)
                     oc_host[i * 216:(i + 1) * 216].copy_(pl._outcomes, non_blocking=True)
-            cur.wait_stream(s_out)
+            for st_ in (s_in, s_cmp, s_out):
+                cur.wait_stream(st_)
 
         for _ in range(args.warmup):
             e2e_step()
         torch.cuda.synchronize()
-        ts = []
-        for _ in range(args.steps):
-            flush.zero_()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
+
+        def time_e2e(run):
+            ts = []
+            for _ in range(args.steps):
+                flush.zero_()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                run()
+                e1.record()
+                torch.cuda.synchronize()
+                ts.append(e0.elapsed_time(e1))
+            return statistics.mean(ts)
+
+        # eager: ~100 host calls per step (ctypes + torch copies) -- host-launch
+        # bound on a slow host; graph: the same C-ABI calls and the same pinned
+        # H2D / D2H copies captured once and replayed (every byte still crosses
+        # PCIe inside the timed region)
+        eager_ms = time_e2e(e2e_step)
+        g_e2e = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g_e2e):
             e2e_step()
-            e1.record()
-            torch.cuda.synchronize()
-            ts.append(e0.elapsed_time(e1))
-        e_ms = statistics.mean(ts)
+        g_e2e.replay()
+        torch.cuda.synchronize()
+        e_ms = time_e2e(g_e2e.replay)
         if dist:
             t = torch.tensor([e_ms], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = t.item()
         e2e = {"value": round(ops_step / (e_ms * 1e-3) / 1e12, 3), "unit": "TOPS", "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h), "ms_per_step": round(e_ms, 3),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": round(e_ms, 3), "eager_ms_per_step": round(eager_ms, 3),
                "path": "per layer: pinned H2D NCHW -> abed_pack_input -> abed_conv_plan_run(FIC, OUT_I8_NCHW) -> "
                        "abed_conv_plan_finalize -> D2H output + verdicts; H2D / compute / D2H on three streams, "
-                       "pipelined across the 16 layers"}
+                       "pipelined across the 16 layers; the step's calls captured once as a CUDA graph and replayed "
+                       "(eager_ms_per_step: the same calls issued from Python every step)"}
 
     # ------------------------------------------------ detection coverage (GPU fault campaigns)
     cfg1 = api.layer_shape(1, 64, 56, 56, 64, 3, 3, 1, 1, 1, 1)
