@@ -50,7 +50,7 @@ def main():
             if m not in hdr:
                 continue
             i = hdr.index(m)
-            v = float(r[i].replace(",", "")) if r[i] else None
+            v = float(r[i].replace(",", "")) if r[i] and r[i] != "no data" else None
             if v is not None and units[i] in SCALE:
                 v *= SCALE[units[i]]
             e[key] = v
