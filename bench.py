@@ -855,6 +855,8 @@ def run_ours(args, world, rank, local):
         pass
     roofline = {"bound": "tensor", "achieved": round(conv_tops, 2), "peak": round(peak, 1), "unit": "TFLOP/s",
                 "frac": round(conv_tops / peak, 4), "traffic": ncu.get("traffic_bytes_per_launch"),
+                "traffic_source": "profiles/ncu_summary.json: dram__bytes_read.sum + dram__bytes_write.sum of one "
+                                  "launch of " + str(ncu.get("traffic_layer")) + " (ncu --set full)",
                 "kernel": "conv_i8_tc_kernel<int8, packed out, FIC> (conv + input-checksum warps + output sums + verdict)",
                 "peak_source": ("2 x MEASURED_PEAKS.json bf16_tflops (burst): tcgen05 kind::i8 issues K=32 at the "
                                 "kind::f16 K=16 rate (tools/mma_microbench.cu)" if bf16 else "2 x fallback bf16 1590"),
