@@ -57,6 +57,8 @@ __global__ void box_sum_dot_kernel(const int32_t* bsum, abed_dev::ActGeom g, con
 __global__ void fic_weight_kernel(const int32_t* fsum, abed_dev::ActGeom g, int32_t* G);
 __global__ void fic_weight_digits_kernel(const int32_t* G, int64_t cells, int8_t* G8, int* too_big);
 __global__ void fic_class_table_kernel(const int8_t* G8, abed_dev::ActGeom g, const int* rep, int n_rep, int8_t* T8);
+__global__ void fic_rhs_dp4a_kernel(const int8_t* act, abed_dev::ActGeom g, const int8_t* G8, int nsplit,
+                                    unsigned long long* rhs);
 __global__ void fic_rhs_kernel(const int8_t* act, abed_dev::ActGeom g, const int32_t* G, int nsplit,
                                unsigned long long* rhs);
 __global__ void fc_finalize_rec_kernel(const int64_t* rec, int m_tiles, int P, int Q, abed_verify_outcome* out);

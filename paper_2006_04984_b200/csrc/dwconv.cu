@@ -19,6 +19,7 @@
 // outputs x 9 MACs.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -364,7 +365,15 @@ void plan_run_dw(abed_conv_plan* pl, const int8_t* packed, const abed_epilog_par
     cuda_check(cudaMemsetAsync(pl->d_acc, 0, 8, st), "memset rhs");
     const int64_t cells = (int64_t)g.n_phase * g.c16 * g.Hl * g.Wl;
     const int nsplit = g.n >= 8 ? 8 : g.n;
-    fic_rhs_kernel<<<grid_for(cells * nsplit, 256), 256, 0, st>>>(packed, g, pl->d_ficw, nsplit, pl->d_acc);
+    if (pl->ficw8_ok) {
+      // one item per (plane, pixel, image split); every item walks >= 8 images so
+      // its G digits (48 B) are amortised and its 8 loads in flight are all used
+      const int64_t want = (int64_t)num_sms() * 2048;
+      const int ns = (int)std::max<int64_t>(1, std::min<int64_t>(g.n / 8, (want + cells - 1) / cells));
+      fic_rhs_dp4a_kernel<<<grid_for(cells * ns, 256), 256, 0, st>>>(packed, g, pl->d_ficw8, ns, pl->d_acc);
+    } else {
+      fic_rhs_kernel<<<grid_for(cells * nsplit, 256), 256, 0, st>>>(packed, g, pl->d_ficw, nsplit, pl->d_acc);
+    }
     cuda_check(cudaGetLastError(), "fic_rhs");
   }
   pl->last_rhs_mode = af_in ? 2 : 0;  // AF accumulator, or the FR rhs in d_acc[0]
