@@ -54,7 +54,63 @@ struct DwParams {
   const int8_t* af_ficw8;
   unsigned long long* af_acc;
   int64_t af_HlWl;
+  // FIC rhs in-kernel (FR): this plan's G digit planes [phase][c16][Hl*Wl][3][16 B]
+  // and the image split of the (plane, pixel) items; nullptr = off
+  const int8_t* ficw8;
+  int rhs_nsplit;
 };
+
+// FIC rhs (FR option) over the stored input, x . G with G as three balanced
+// base-256 digit planes: item = (plane, pixel position, image split), its G
+// digits loaded once, 8 image loads in flight, 12 dp4a per 16-byte chunk; the
+// digit partials are flushed every 32 images (exact in int32).  Same sum as
+// checksum.hpp:248-285 (gen_input_checksum + fic_dot) regrouped by input pixel.
+__device__ __forceinline__ long long dw_fic_rhs(const DwParams& p, int64_t first, int64_t stride) {
+  constexpr int DEPTH = 8;
+  const int64_t HlWl = static_cast<int64_t>(p.Hl) * p.Wl;
+  const int nsplit = p.rhs_nsplit;
+  const int64_t total = static_cast<int64_t>(p.n_phase) * p.c16 * HlWl * nsplit;
+  long long acc = 0;
+  for (int64_t idx = first; idx < total; idx += stride) {
+    const int64_t pix = idx % HlWl;
+    const int64_t rest = idx / HlWl;
+    const int split = static_cast<int>(rest % nsplit);
+    const int64_t plane = rest / nsplit;
+    const uint4* gw = reinterpret_cast<const uint4*>(p.ficw8) + (plane * HlWl + pix) * 3;
+    const uint4 g0 = __ldg(gw), g1 = __ldg(gw + 1), g2 = __ldg(gw + 2);
+    const uint4* src = reinterpret_cast<const uint4*>(p.act) + plane * p.plane_len + pix;
+    const int n0 = static_cast<int>(static_cast<int64_t>(p.N) * split / nsplit);
+    const int n1 = static_cast<int>(static_cast<int64_t>(p.N) * (split + 1) / nsplit);
+    int32_t d0 = 0, d1 = 0, d2 = 0;
+    for (int n = n0; n < n1; n += DEPTH) {
+      uint4 x[DEPTH];
+#pragma unroll
+      for (int j = 0; j < DEPTH; ++j)
+        x[j] = n + j < n1 ? __ldcs(src + static_cast<int64_t>(n + j) * HlWl) : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+      for (int j = 0; j < DEPTH; ++j) {
+        d0 = __dp4a(static_cast<int>(x[j].x), static_cast<int>(g0.x), d0);
+        d0 = __dp4a(static_cast<int>(x[j].y), static_cast<int>(g0.y), d0);
+        d0 = __dp4a(static_cast<int>(x[j].z), static_cast<int>(g0.z), d0);
+        d0 = __dp4a(static_cast<int>(x[j].w), static_cast<int>(g0.w), d0);
+        d1 = __dp4a(static_cast<int>(x[j].x), static_cast<int>(g1.x), d1);
+        d1 = __dp4a(static_cast<int>(x[j].y), static_cast<int>(g1.y), d1);
+        d1 = __dp4a(static_cast<int>(x[j].z), static_cast<int>(g1.z), d1);
+        d1 = __dp4a(static_cast<int>(x[j].w), static_cast<int>(g1.w), d1);
+        d2 = __dp4a(static_cast<int>(x[j].x), static_cast<int>(g2.x), d2);
+        d2 = __dp4a(static_cast<int>(x[j].y), static_cast<int>(g2.y), d2);
+        d2 = __dp4a(static_cast<int>(x[j].z), static_cast<int>(g2.z), d2);
+        d2 = __dp4a(static_cast<int>(x[j].w), static_cast<int>(g2.w), d2);
+      }
+      if (((n - n0) & 31) == 32 - DEPTH) {
+        acc += static_cast<long long>(d0) + (static_cast<long long>(d1) << 8) + (static_cast<long long>(d2) << 16);
+        d0 = d1 = d2 = 0;
+      }
+    }
+    acc += static_cast<long long>(d0) + (static_cast<long long>(d1) << 8) + (static_cast<long long>(d2) << 16);
+  }
+  return acc;
+}
 
 // 4x4 byte transpose of four taps (a, b, c, d: one byte per channel) so that
 // y[i] = {a.i, b.i, c.i, d.i} holds four taps of channel i for one dp4a
@@ -197,16 +253,30 @@ __global__ void __launch_bounds__(256) dwconv_i8_kernel(const __grid_constant__ 
     if ((threadIdx.x & 31) == 0 && af != 0) atomicAdd(p.af_acc, static_cast<unsigned long long>(af));
   }
   if (p.fic) {
+    // this block's share of the FIC rhs (FR), after its conv work
+    long long rhs = p.ficw8 ? dw_fic_rhs(p, static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x,
+                                         static_cast<int64_t>(gridDim.x) * blockDim.x)
+                            : 0;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) fic += __shfl_xor_sync(0xffffffffu, fic, o);
-    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = fic;
+    for (int o = 16; o > 0; o >>= 1) {
+      fic += __shfl_xor_sync(0xffffffffu, fic, o);
+      rhs += __shfl_xor_sync(0xffffffffu, rhs, o);
+    }
+    __shared__ long long s_rhs[8];
+    if ((threadIdx.x & 31) == 0) {
+      s_red[threadIdx.x >> 5] = fic;
+      s_rhs[threadIdx.x >> 5] = rhs;
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
-      long long t = 0;
-      for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += s_red[w];
+      long long t = 0, r = 0;
+      for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) {
+        t += s_red[w];
+        r += s_rhs[w];
+      }
       int64_t* rec = p.cta_rec + static_cast<int64_t>(blockIdx.x) * kCtaRec;
       rec[4] = t;
-      rec[5] = 0;
+      rec[5] = r;
     }
   }
 }
@@ -360,23 +430,26 @@ void plan_run_dw(abed_conv_plan* pl, const int8_t* packed, const abed_epilog_par
   p.fault_key = fault_key;
   p.fault_bit = fault_bit;
   const bool af_in = p.fic && pl->af_input && !pl->reuse_input_checksum;
+  bool fr_in_kernel = false;
   if (p.fic && !pl->reuse_input_checksum && !af_in) {
-    // FR: input checksum dot of the stored input, one pass ahead of the conv
-    cuda_check(cudaMemsetAsync(pl->d_acc, 0, 8, st), "memset rhs");
     const int64_t cells = (int64_t)g.n_phase * g.c16 * g.Hl * g.Wl;
-    const int nsplit = g.n >= 8 ? 8 : g.n;
     if (pl->ficw8_ok) {
-      // one item per (plane, pixel, image split); every item walks >= 8 images so
-      // its G digits (48 B) are amortised and its 8 loads in flight are all used
-      const int64_t want = (int64_t)num_sms() * 2048;
-      const int ns = (int)std::max<int64_t>(1, std::min<int64_t>(g.n / 8, (want + cells - 1) / cells));
-      fic_rhs_dp4a_kernel<<<grid_for(cells * ns, 256), 256, 0, st>>>(packed, g, pl->d_ficw8, ns, pl->d_acc);
+      // FR inside the depthwise kernel: every block dots its share of the stored
+      // input after its conv work; the rhs rides in the per-block records (slot 5)
+      const int64_t threads = (int64_t)dw_grid() * 256;
+      p.ficw8 = pl->d_ficw8;
+      p.rhs_nsplit = (int)std::max<int64_t>(1, std::min<int64_t>(std::max(1, g.n / 8), (threads + cells - 1) / cells));
+      fr_in_kernel = true;
     } else {
+      // |G| too large for the 3-digit map: one separate pass ahead of the conv
+      cuda_check(cudaMemsetAsync(pl->d_acc, 0, 8, st), "memset rhs");
+      const int nsplit = g.n >= 8 ? 8 : g.n;
       fic_rhs_kernel<<<grid_for(cells * nsplit, 256), 256, 0, st>>>(packed, g, pl->d_ficw, nsplit, pl->d_acc);
+      cuda_check(cudaGetLastError(), "fic_rhs");
     }
-    cuda_check(cudaGetLastError(), "fic_rhs");
   }
-  pl->last_rhs_mode = af_in ? 2 : 0;  // AF accumulator, or the FR rhs in d_acc[0]
+  // AF accumulator, FR rhs from the block records, or the rhs kept in d_acc[0]
+  pl->last_rhs_mode = af_in ? 2 : fr_in_kernel ? 1 : 0;
   const int grid = dw_grid();
   switch (out_mode) {
     case ABED_OUT_NONE: abed_dev::dwconv_i8_kernel<0><<<grid, 256, 0, st>>>(p); break;
