@@ -118,6 +118,104 @@ __global__ void abft_pack_a_kernel(const int8_t* __restrict__ a, int64_t m, int6
   }
 }
 
+// Checked mode, tasks (2) + (3) for A in ONE read of A: a block owns one 16-column
+// group g and kRowsPerBlock rows; each thread copies its rows' 16-byte chunks into
+// the strip planes and accumulates the 16 column sums as SIMD byte sums (x ^ 0x80
+// split into two 16-bit lanes per word: 4 instr per 4 bytes, flushed to int32
+// every 128 rows), then one shared-memory reduction and 16 integer atomics per
+// block.  The digit pixels (m .. m+3) follow in abft_a_digits_kernel once the
+// column sums are complete.
+constexpr int kPackSumThreads = 256;
+constexpr int kRowsPerBlock = 4096;
+__global__ void __launch_bounds__(kPackSumThreads) abft_pack_a_sum_kernel(const int8_t* __restrict__ a, int64_t m,
+                                                                           int64_t k, int c16, int64_t plane_len,
+                                                                           int8_t* __restrict__ out,
+                                                                           int32_t* __restrict__ colsum) {
+  __shared__ int32_t red[16][kPackSumThreads / 32];
+  const int g = blockIdx.y;
+  const int64_t c0 = (int64_t)g * 16;
+  const int64_t r0 = (int64_t)blockIdx.x * kRowsPerBlock;
+  const int64_t r1 = min(m, r0 + kRowsPerBlock);
+  const bool vec = (k % 16 == 0) && ((reinterpret_cast<uintptr_t>(a) & 15) == 0);
+  int32_t acc[16];
+#pragma unroll
+  for (int e = 0; e < 16; ++e) acc[e] = 0;
+  uint32_t ev[4] = {0, 0, 0, 0}, od[4] = {0, 0, 0, 0};
+  int cnt = 0;
+  int64_t rows_done = 0;
+  uint4* dst = reinterpret_cast<uint4*>(out) + (int64_t)g * plane_len;
+  for (int64_t i = r0 + threadIdx.x; i < r1; i += kPackSumThreads) {
+    uint4 v;
+    if (vec) {
+      v = __ldcs(reinterpret_cast<const uint4*>(a + i * k + c0));
+    } else {
+      uint32_t w4[4] = {0, 0, 0, 0};
+      for (int e = 0; e < 16 && c0 + e < k; ++e) w4[e >> 2] |= (uint32_t)(uint8_t)a[i * k + c0 + e] << (8 * (e & 3));
+      v = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+    }
+    dst[i] = v;
+    const uint32_t w[4] = {v.x ^ 0x80808080u, v.y ^ 0x80808080u, v.z ^ 0x80808080u, v.w ^ 0x80808080u};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      ev[q] += w[q] & 0x00FF00FFu;
+      od[q] += (w[q] >> 8) & 0x00FF00FFu;
+    }
+    ++rows_done;
+    if (++cnt == 128) {  // 128 * 255 < 2^16
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        acc[4 * q] += (int32_t)(ev[q] & 0xFFFFu);
+        acc[4 * q + 1] += (int32_t)(od[q] & 0xFFFFu);
+        acc[4 * q + 2] += (int32_t)(ev[q] >> 16);
+        acc[4 * q + 3] += (int32_t)(od[q] >> 16);
+        ev[q] = od[q] = 0;
+      }
+      cnt = 0;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    acc[4 * q] += (int32_t)(ev[q] & 0xFFFFu);
+    acc[4 * q + 1] += (int32_t)(od[q] & 0xFFFFu);
+    acc[4 * q + 2] += (int32_t)(ev[q] >> 16);
+    acc[4 * q + 3] += (int32_t)(od[q] >> 16);
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
+    int32_t v = acc[e] - 128 * (int32_t)rows_done;  // un-bias x ^ 0x80 = x + 128
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[e][warp] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < 16 && c0 + threadIdx.x < k) {
+    int32_t t = 0;
+    for (int w = 0; w < kPackSumThreads / 32; ++w) t += red[threadIdx.x][w];
+    atomicAdd(colsum + c0 + threadIdx.x, t);
+  }
+}
+
+// digit pixels m .. m+3 of every channel group, and zero pixels m+4 .. plane_len
+__global__ void abft_a_digits_kernel(int64_t m, int64_t k, const int32_t* __restrict__ colsum, int digits, int c16,
+                                     int64_t plane_len, int8_t* __restrict__ out) {
+  const int64_t tail = plane_len - m;
+  const int64_t total = (int64_t)c16 * tail;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int g = (int)(idx / tail);
+    const int64_t i = m + idx % tail;
+    const int64_t c0 = (int64_t)g * 16;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (i < m + digits && c0 < k) {
+      uint32_t w4[4] = {0, 0, 0, 0};
+      for (int e = 0; e < 16 && c0 + e < k; ++e)
+        w4[e >> 2] |= (uint32_t)(uint8_t)digit_of(colsum[c0 + e], (int)(i - m)) << (8 * (e & 3));
+      v = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+    }
+    reinterpret_cast<uint4*>(out)[(int64_t)g * plane_len + i] = v;
+  }
+}
+
 // GEMM output o[j][i] (K-major: (n + dn) x (m + dm) int32) -> c_aug (m+1) x (n+1)
 // int64 with the digit rows / columns recombined, and/or the trimmed c (m x n
 // int32, task 6).  32x32 tiles over (i, j) of c_aug through shared memory.
@@ -371,7 +469,6 @@ void run(abed_abft_plan* p, const int8_t* a, const int8_t* b, int32_t* c, int64_
     pl = gemm_plan(p, 0, mode == ABED_ABFT_FUSED_ROW ? ABED_CHECK_FC : 0);
     (mode == ABED_ABFT_PLAIN ? p->plain : p->fused) = pl;
   }
-  if (digits) dev_colsum_i8(a, m, k, p->colsum, st);  // task 3: column sums of A
   const ActGeom& g = pl->g;
   if (b) {
     // B side (skipped when b == NULL: B stays packed from an earlier run, i.e. the
@@ -388,9 +485,19 @@ void run(abed_abft_plan* p, const int8_t* a, const int8_t* b, int32_t* c, int64_
   } else if (!p->b_packed[mode]) {
     throw_invalid("abft plan: b == NULL before B was packed by a run in this mode");
   }
-  // task 2: A into the strip planes with the checksum row's digits
-  const int64_t n16 = (int64_t)g.c16 * g.plane_len;
-  abft_pack_a_kernel<<<grid_for(n16, 256), 256, 0, st>>>(a, m, k, p->colsum, digits, g.c16, g.plane_len, p->packed);
+  if (digits) {
+    // tasks 2 + 3 for A in one read: strip-plane copy + column sums, then the
+    // checksum row's digit pixels
+    cuda_check(cudaMemsetAsync(p->colsum, 0, (size_t)k * 4, st), "abft colsum");
+    const dim3 grid((unsigned)((m + kRowsPerBlock - 1) / kRowsPerBlock), (unsigned)g.c16);
+    abft_pack_a_sum_kernel<<<grid, kPackSumThreads, 0, st>>>(a, m, k, g.c16, g.plane_len, p->packed, p->colsum);
+    const int64_t nt = (int64_t)g.c16 * (g.plane_len - m);
+    abft_a_digits_kernel<<<grid_for(nt, 256), 256, 0, st>>>(m, k, p->colsum, digits, g.c16, g.plane_len, p->packed);
+  } else {
+    // task 2: A into the strip planes
+    const int64_t n16 = (int64_t)g.c16 * g.plane_len;
+    abft_pack_a_kernel<<<grid_for(n16, 256), 256, 0, st>>>(a, m, k, p->colsum, 0, g.c16, g.plane_len, p->packed);
+  }
   cuda_check(cudaGetLastError(), "abft operands");
   // task 4: the (larger) GEMM on tcgen05
   plan_run(pl, p->packed, nullptr, ABED_OUT_I32_NCHW, p->out, nullptr, -1, 0, st);
