@@ -346,6 +346,9 @@ void plan_run(abed_conv_plan* pl, const int8_t* packed, const abed_epilog_params
       want = 2LL * p.conv_grid * 64;
     }
     const int64_t cells = (int64_t)g.n_phase * g.c16 * g.Hl * g.Wl;
+    // ResNet-50 b32: the 256->64/128 1x1 layers at 56x56 (26 MB inputs) gain ~2 us
+    // with 16 loads in flight; the <= 7 MB inputs lose ~0.4 us (tools/r50net_layer_times.py)
+    p.rhs_deep = geom_packed_bytes(g) >= (int64_t(16) << 20) ? 1 : 0;
     return (int)std::max<int64_t>(1, std::min<int64_t>(g.n, (want + cells - 1) / cells));
   };
   if (!fmode && pl->af_input && (pl->checks & ABED_CHECK_FIC) && !pl->reuse_input_checksum) {

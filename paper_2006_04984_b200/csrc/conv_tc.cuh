@@ -115,6 +115,7 @@ struct ConvTcParams {
                                // 2: AF -- the previous layer's epilogue produced it (af accumulator),
                                // 3: SM -- input-checksum warps read the staged A tiles (no re-read)
   int rhs_nsplit;              // image split of the rhs work items
+  int rhs_deep;                // int8 FR: 16 image loads in flight per item (large inputs) instead of 8
   int conv_grid;               // CTAs running conv work units (blockIdx < conv_grid)
   int ic_ctas;                 // extra CTAs (blockIdx >= conv_grid) that only compute the FR
                                // input checksum on SMs the conv grid leaves idle (0: the conv

@@ -1182,8 +1182,14 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
     double facc_rhs = 0.0;
     if (DT != DT_I8 && FIC && p.rhs_mode == 1 && p.ic_ctas == 0) {
       pdl_wait();
-      fic_rhs_fr<DT, DT == DT_I8 ? 8 : 16>(p, static_cast<int64_t>(blockIdx.x) * (kRhsWarps * 32) + rw * 32 + lane,
-                     static_cast<int64_t>(p.conv_grid) * (kRhsWarps * 32), acc, facc_rhs);
+      const int64_t first = static_cast<int64_t>(blockIdx.x) * (kRhsWarps * 32) + rw * 32 + lane;
+      const int64_t stride = static_cast<int64_t>(p.conv_grid) * (kRhsWarps * 32);
+      // large inputs (HBM-bound 1x1 layers with C >> K): more image loads in flight;
+      // measured slower on the small 3x3 inputs, so chosen per plan
+      if (DT != DT_I8 || p.rhs_deep)
+        fic_rhs_fr<DT, 16>(p, first, stride, acc, facc_rhs);
+      else
+        fic_rhs_fr<DT, 8>(p, first, stride, acc, facc_rhs);
     } else if (rhs_staged) {
       // FIC-SM: the same sum x * G, with x taken from the A stages the producer
       // staged for the MMAs.  M tile mt owns plane pixels [m0, m0 + 128) of every
@@ -1295,8 +1301,14 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
       }
     } else if (DT == DT_I8 && FIC && p.rhs_mode == 1 && p.ic_ctas == 0) {
       pdl_wait();
-      fic_rhs_fr<DT, DT == DT_I8 ? 8 : 16>(p, static_cast<int64_t>(blockIdx.x) * (kRhsWarps * 32) + rw * 32 + lane,
-                     static_cast<int64_t>(p.conv_grid) * (kRhsWarps * 32), acc, facc_rhs);
+      const int64_t first = static_cast<int64_t>(blockIdx.x) * (kRhsWarps * 32) + rw * 32 + lane;
+      const int64_t stride = static_cast<int64_t>(p.conv_grid) * (kRhsWarps * 32);
+      // large inputs (HBM-bound 1x1 layers with C >> K): more image loads in flight;
+      // measured slower on the small 3x3 inputs, so chosen per plan
+      if (DT != DT_I8 || p.rhs_deep)
+        fic_rhs_fr<DT, 16>(p, first, stride, acc, facc_rhs);
+      else
+        fic_rhs_fr<DT, 8>(p, first, stride, acc, facc_rhs);
     } else {
       pdl_wait();
     }
