@@ -140,7 +140,8 @@ struct abed_conv_plan {
   // compete with the SS-mode MMA operand reads and it holds stages), so FR is default.
   int rhs_src = ABED_RHS_REREAD;
   int64_t* d_fc_part = nullptr;     // FC row partials per N tile (n_tiles > 1)
-  unsigned int* d_tile_sem = nullptr;  // FC tiles-done counters per M tile
+  unsigned int* d_tile_sem = nullptr;  // FC per-M-tile flags (several N tiles), epoch-tagged
+  unsigned fc_epoch = 0;               // incremented per run; never 0 (the flags' initial value)
   int64_t* d_cta_rec = nullptr;     // FC per-CTA records
   unsigned long long* d_kacc = nullptr;  // kernel accumulators {FIC lhs, FIC rhs, done ticket, -}
   abed_verify_outcome* d_outcome = nullptr;  // {FC, FIC, IC} verdicts written by the conv kernel

@@ -310,6 +310,8 @@ void plan_run(abed_conv_plan* pl, const int8_t* packed, const abed_epilog_params
   }
   p.fc_part = pl->d_fc_part;
   p.tile_sem = pl->d_tile_sem;
+  if (++pl->fc_epoch == 0u) pl->fc_epoch = 1u;
+  p.fc_epoch = pl->fc_epoch;
   p.cta_rec = pl->d_cta_rec;
   p.kacc = pl->d_kacc;
   p.outcome = pl->d_outcome;
@@ -412,6 +414,15 @@ abed_dev::VerdictJob plan_verdict_job(const abed_conv_plan* pl, abed_verify_outc
   j.rhs_ext_f = pl->d_rhs_f;
   j.tau_fic = pl->tau_fic;
   j.out = out_dev;
+  j.fc_part = pl->d_fc_part;
+  j.tile_flag = pl->d_tile_sem;
+  j.fc_epoch = pl->fc_epoch;
+  j.n_tiles = pl->dw ? 1 : pl->base.n_tiles;
+  j.m_tiles = pl->g.m_tiles;
+  j.Hl = pl->g.Hl;
+  j.Wl = pl->g.Wl;
+  j.m_total = pl->g.m_total;
+  j.tau_fc = pl->tau_fc;
   return j;
 }
 

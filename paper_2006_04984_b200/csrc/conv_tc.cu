@@ -35,6 +35,38 @@ __global__ void __launch_bounds__(256) verdict_kernel(const __grid_constant__ Ve
   FcRec fc{0, kNoKey, 0, 0};
   long long li = 0, ri = 0;
   double lf = 0.0, rf = 0.0;
+  if ((j.checks & CHECK_FC) && j.n_tiles > 1) {
+    // full-channel row sums of the flagged M tiles (fc_verify, checksum.hpp:211-236)
+    const int64_t HlWl = static_cast<int64_t>(j.Hl) * j.Wl;
+    const int64_t PQ = static_cast<int64_t>(j.P) * j.Q;
+    const int64_t stride = static_cast<int64_t>(j.m_tiles) * kBlockM * 2;
+    for (int mt = 0; mt < j.m_tiles; ++mt) {
+      if (j.tile_flag[mt] != j.fc_epoch) continue;  // not raised by the last run
+      for (int r = t; r < kBlockM; r += blockDim.x) {
+        const int64_t m = static_cast<int64_t>(mt) * kBlockM + r;
+        if (m >= j.m_total) continue;
+        const int64_t n = m / HlWl, rem = m % HlWl, pp = rem / j.Wl, qq = rem % j.Wl;
+        if (pp >= j.P || qq >= j.Q) continue;
+        const int64_t key = n * PQ + pp * j.Q + qq;
+        const int64_t* q = j.fc_part + m * 2;
+        if (j.dtype == DT_I8) {
+          long long l = 0, rr = 0;
+          for (int nt = 0; nt < j.n_tiles; ++nt) {
+            l += __ldcg(q + nt * stride);
+            rr += __ldcg(q + nt * stride + 1);
+          }
+          if (l != rr) fc_note(fc, key, l, rr);
+        } else {
+          double l = 0.0, rr = 0.0;
+          for (int nt = 0; nt < j.n_tiles; ++nt) {
+            l += __longlong_as_double(__ldcg(q + nt * stride));
+            rr += __longlong_as_double(__ldcg(q + nt * stride + 1));
+          }
+          if (!(fabs(l - rr) <= j.tau_fc)) fc_note(fc, key, __double_as_longlong(l), __double_as_longlong(rr));
+        }
+      }
+    }
+  }
   for (int c = t; c < j.grid; c += blockDim.x) {
     const int64_t* rec = j.rec + static_cast<int64_t>(c) * kCtaRec;
     if (j.checks & CHECK_FC) {

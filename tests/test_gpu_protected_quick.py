@@ -84,3 +84,38 @@ def test_convout_fault_detected(dims):
     assert oc[0].lhs == int(conv[ni, :, pi, qi].sum()) and oc[0].rhs == int(want[ni, :, pi, qi].sum())
     assert oc[1].status == 1 and oc[1].lhs == int(conv.sum()) and oc[1].rhs == int(want.sum())
     assert oc[2].status == 1 and oc[2].locus[0] == ki
+
+
+@pytest.mark.parametrize("dims", [(2, 128, 14, 14, 256, 3, 3, 1, 1, 1, 1), (2, 256, 7, 7, 512, 3, 3, 1, 1, 1, 1)])
+def test_fc_several_n_tiles_fault_then_clean_run(dims):
+    """FC across N tiles (per-tile flags, full-channel recheck in the verdict): a
+    ConvOut fault is reported with the reference's full-row lhs / rhs, finalize is
+    idempotent, and a later fault-free run on the same plan passes."""
+    from paper_2006_04984_b200 import api
+    ls = abi.layer_shape(*dims)
+    g = torch.Generator().manual_seed(3 + sum(dims))
+    x = torch.randint(-128, 128, ls.input_dims(), dtype=torch.int8, generator=g)
+    f = torch.randint(-128, 128, ls.filter_dims(), dtype=torch.int8, generator=g)
+    want = ref_conv(x, f, ls)
+    plan = api.ConvPlan(ls, f.cuda(), abi.CHECK_FC)
+    assert plan.info.n_tiles > 1
+    packed = plan.pack(x.cuda())
+    key, bit = (want.numel() * 3) // 5, 12
+    n, k, p, q = ls.output_dims()
+    ni, rem = divmod(key, k * p * q)
+    pi, qi = divmod(rem % (p * q), q)
+    out = torch.empty(ls.output_dims(), dtype=torch.int32, device="cuda")
+    plan.run(packed, out, abi.OUT_I32_NCHW, fault_key=key, fault_bit=bit)
+    plan.finalize()
+    fc = plan.outcomes()[0]
+    got = out.cpu().to(torch.int64)
+    assert fc.status == 1 and tuple(fc.locus) == (ni, pi, qi) and fc.error_count == 1
+    assert fc.lhs == int(got[ni, :, pi, qi].sum()) and fc.rhs == int(want[ni, :, pi, qi].sum())
+    plan.finalize()
+    again = plan.outcomes()[0]
+    assert (again.status, tuple(again.locus), again.lhs, again.rhs) == (1, (ni, pi, qi), fc.lhs, fc.rhs)
+    plan.run(packed, out, abi.OUT_I32_NCHW)
+    plan.finalize()
+    clean = plan.outcomes()[0]
+    assert clean.status == 0 and clean.error_count == 0
+    assert torch.equal(out.cpu().to(torch.int64), want)
