@@ -417,7 +417,9 @@ abed_dev::VerdictJob plan_verdict_job(const abed_conv_plan* pl, abed_verify_outc
   j.fc_part = pl->d_fc_part;
   j.tile_flag = pl->d_tile_sem;
   j.fc_epoch = pl->fc_epoch;
-  j.n_tiles = pl->dw ? 1 : pl->base.n_tiles;
+  // int8 plans with several N tiles: the verdict rechecks flagged M tiles; float
+  // plans keep the full-channel FC check in-kernel
+  j.n_tiles = (pl->dw || pl->dtype != abed_dev::DT_I8) ? 1 : pl->base.n_tiles;
   j.m_tiles = pl->g.m_tiles;
   j.Hl = pl->g.Hl;
   j.Wl = pl->g.Wl;

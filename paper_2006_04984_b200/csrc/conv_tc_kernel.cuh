@@ -1121,13 +1121,39 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
             // full-channel check (fc_verify, :211-236), so the CTA only raises the
             // M tile's flag, and the verdict kernel -- after the whole grid --
             // recomputes the full-channel sums of flagged tiles from these
-            // partials, with the reference's semantics and loop order.  (Float
-            // mode flags at tau / n_tiles: unflagged rows pass the full check.)
+            // partials, with the reference's semantics and loop order.
             int64_t* part = p.fc_part + (static_cast<int64_t>(nt) * p.m_tiles * kBlockM + m) * 2;
             part[0] = acc_bits(row_sum);
             part[1] = acc_bits(extra);
-            const bool bad = valid && fc_mismatch<DT>(row_sum, extra, p.tau_fc / p.n_tiles);
-            if (__any_sync(0xffffffffu, bad) && lane == 0) p.tile_sem[mt] = p.fc_epoch;
+            if constexpr (DT == DT_I8) {
+              const bool bad = valid && row_sum != extra;
+              if (__any_sync(0xffffffffu, bad) && lane == 0) p.tile_sem[mt] = p.fc_epoch;
+            } else {
+              // float mode: per-tile differences may add up across tiles, so the
+              // full-channel check stays in-kernel -- the CTA completing the M
+              // tile's last N tile sums every tile's partials (fc_verify_f32,
+              // :541-565); tile_sem counts tiles here
+              __threadfence();
+              named_bar(kBarHalf0, 128);
+              if (row == 0) {
+                const unsigned prev = atomicAdd(&p.tile_sem[mt], 1u);
+                s_tile_last = prev == static_cast<unsigned>(p.n_tiles - 1);
+              }
+              named_bar(kBarHalf0, 128);
+              if (s_tile_last) {
+                __threadfence();
+                if (valid) {
+                  Acc l = 0, r = 0;
+                  for (int t = 0; t < p.n_tiles; ++t) {
+                    const int64_t* q = p.fc_part + (static_cast<int64_t>(t) * p.m_tiles * kBlockM + m) * 2;
+                    l += bits_acc<Acc>(__ldcg(q));
+                    r += bits_acc<Acc>(__ldcg(q + 1));
+                  }
+                  if (fc_mismatch<DT>(l, r, p.tau_fc)) fc_note(fc, key, acc_bits(l), acc_bits(r));
+                }
+                if (row == 0) p.tile_sem[mt] = 0u;  // ready for the next run
+              }
+            }
           }
         }
         // s_rowsum reuse guard for the next unit
