@@ -743,6 +743,30 @@ __device__ __forceinline__ void fic_rhs_fr(const ConvTcParams& p, int64_t first,
   }
 }
 
+// FR input-checksum items of this CTA (the same set fic_rhs_fr's static stride
+// gives its two input-checksum warps), claimed 32 at a time from a shared-memory
+// counter, so warps that have finished their own role -- producer, MMA issuer,
+// epilogue after its last unit -- take over part of the input-checksum tail.
+template <int DT>
+__device__ __forceinline__ void fr_claim_loop(const ConvTcParams& p, int* s_claim, int lane, long long& acc,
+                                              double& facc) {
+  const int64_t HlWl = static_cast<int64_t>(p.Hl) * p.Wl;
+  const int64_t total = static_cast<int64_t>(p.n_phase) * p.c16 * HlWl * p.rhs_nsplit;
+  const int64_t stride = static_cast<int64_t>(p.conv_grid) * (kRhsWarps * 32);
+  const int64_t base0 = static_cast<int64_t>(blockIdx.x) * (kRhsWarps * 32);
+  for (;;) {
+    int c = 0;
+    if (lane == 0) c = atomicAdd(s_claim, 1);
+    c = __shfl_sync(0xffffffffu, c, 0);
+    const int64_t idx0 = base0 + (c & 1) * 32 + static_cast<int64_t>(c >> 1) * stride;
+    if (idx0 >= total) break;
+    if (DT != DT_I8 || p.rhs_deep)
+      fic_rhs_fr<DT, 16>(p, idx0 + lane, int64_t(1) << 62, acc, facc);
+    else
+      fic_rhs_fr<DT, 8>(p, idx0 + lane, int64_t(1) << 62, acc, facc);
+  }
+}
+
 // pattern ids (host: mma_pattern_of in plan.cu)
 enum MmaPattern : int {
   PAT_GENERIC = 0,
@@ -767,7 +791,6 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
   __shared__ __align__(16) float s_bias[kBiasSmem];
   __shared__ FcRec s_fc[kEpiWarps];
   __shared__ long long s_lhs[kEpiWarps];
-  __shared__ long long s_rhs[kRhsWarps];
   __shared__ int64_t s_rowsum[kEpiParts - 1][kBlockM];
   __shared__ int s_tile_last;
 
@@ -839,11 +862,21 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
     if (rhs_staged) mbar_init(reinterpret_cast<uint64_t*>(smem + L.fic_off + p.fic_smem), 1);
     fence_mbar_init();
   }
+  __shared__ int s_fr_claim;
+  __shared__ long long s_rhs_all[kConvThreads / 32];
+  if (threadIdx.x == 0) s_fr_claim = 0;
+  if (threadIdx.x < kConvThreads / 32) s_rhs_all[threadIdx.x] = 0;
   if (warp == 1) tmem_alloc(tmem_slot, tmem_cols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // FR input checksum shared by every warp that has finished its role (dbg 256: off)
+  // float mode only: on int8 layers the claims of the producer / MMA warps slowed the
+  // epilogue-bound CTAs (ResNet-50 layer1 FIC 12.3 -> 13.4 us); VGG-16 FP16 FIC 18% -> 11%
+  const bool fr_share = DT != DT_I8 && FIC && p.rhs_mode == 1 && p.ic_ctas == 0 && !(p.dbg & 256);
+  long long fr_acc = 0;
+  double fr_facc = 0.0;
   if (trace && threadIdx.x == 0) trace[2] = clock64() - t_entry;
   pdl_launch_dependents();
 
@@ -929,6 +962,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
     } else {
       pdl_wait();
     }
+    if (fr_share) fr_claim_loop<DT>(p, &s_fr_claim, lane, fr_acc, fr_facc);
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     pdl_wait();
@@ -959,6 +993,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
       case PAT_1x1_S2_G2: mma_warp_run<DT, 1, 1, 2, 2, 2>(p, v); break;
       default: mma_warp_run<DT, 0, 0, 1, 1, 2>(p, v); break;
     }
+    if (fr_share) fr_claim_loop<DT>(p, &s_fr_claim, lane, fr_acc, fr_facc);
   } else if (warp < 2 + kEpiWarps) {
     // ------------------------------------------------------------ epilogue
     // kEpiParts warps per TMEM lane quarter split the tile's 16-column chunks
@@ -1171,6 +1206,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
       trace[11] = tr_acc;
       trace[12] = tr_proc;
     }
+    if (fr_share) fr_claim_loop<DT>(p, &s_fr_claim, lane, fr_acc, fr_facc);
     // CTA-level partials of the epilogue warps
     if (FC) {
       const FcRec w = fc_warp_reduce(fc);
@@ -1196,14 +1232,13 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
     double facc_rhs = 0.0;
     if (DT != DT_I8 && FIC && p.rhs_mode == 1 && p.ic_ctas == 0) {
       pdl_wait();
-      const int64_t first = static_cast<int64_t>(blockIdx.x) * (kRhsWarps * 32) + rw * 32 + lane;
-      const int64_t stride = static_cast<int64_t>(p.conv_grid) * (kRhsWarps * 32);
-      // large inputs (HBM-bound 1x1 layers with C >> K): more image loads in flight;
-      // measured slower on the small 3x3 inputs, so chosen per plan
-      if (DT != DT_I8 || p.rhs_deep)
+      if (fr_share) {
+        fr_claim_loop<DT>(p, &s_fr_claim, lane, acc, facc_rhs);
+      } else {
+        const int64_t first = static_cast<int64_t>(blockIdx.x) * (kRhsWarps * 32) + rw * 32 + lane;
+        const int64_t stride = static_cast<int64_t>(p.conv_grid) * (kRhsWarps * 32);
         fic_rhs_fr<DT, 16>(p, first, stride, acc, facc_rhs);
-      else
-        fic_rhs_fr<DT, 8>(p, first, stride, acc, facc_rhs);
+      }
     } else if (rhs_staged) {
       // FIC-SM: the same sum x * G, with x taken from the A stages the producer
       // staged for the MMAs.  M tile mt owns plane pixels [m0, m0 + 128) of every
@@ -1315,21 +1350,29 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
       }
     } else if (DT == DT_I8 && FIC && p.rhs_mode == 1 && p.ic_ctas == 0) {
       pdl_wait();
-      const int64_t first = static_cast<int64_t>(blockIdx.x) * (kRhsWarps * 32) + rw * 32 + lane;
-      const int64_t stride = static_cast<int64_t>(p.conv_grid) * (kRhsWarps * 32);
-      // large inputs (HBM-bound 1x1 layers with C >> K): more image loads in flight;
-      // measured slower on the small 3x3 inputs, so chosen per plan
-      if (DT != DT_I8 || p.rhs_deep)
-        fic_rhs_fr<DT, 16>(p, first, stride, acc, facc_rhs);
-      else
-        fic_rhs_fr<DT, 8>(p, first, stride, acc, facc_rhs);
+      if (fr_share) {
+        fr_claim_loop<DT>(p, &s_fr_claim, lane, acc, facc_rhs);
+      } else {
+        const int64_t first = static_cast<int64_t>(blockIdx.x) * (kRhsWarps * 32) + rw * 32 + lane;
+        const int64_t stride = static_cast<int64_t>(p.conv_grid) * (kRhsWarps * 32);
+        // large inputs (HBM-bound 1x1 layers with C >> K): more image loads in
+        // flight; measured slower on the small 3x3 inputs, so chosen per plan
+        if (p.rhs_deep)
+          fic_rhs_fr<DT, 16>(p, first, stride, acc, facc_rhs);
+        else
+          fic_rhs_fr<DT, 8>(p, first, stride, acc, facc_rhs);
+      }
     } else {
       pdl_wait();
     }
-    if (FIC) {
-      const long long w = DT == DT_I8 ? warp_sum(acc) : __double_as_longlong(warp_sum_d(facc_rhs));
-      if (lane == 0) s_rhs[rw] = w;
-    }
+    fr_acc += acc;
+    fr_facc += facc_rhs;
+  }
+  // every warp's share of the FIC rhs (input-checksum warps, and the others when
+  // they took part through fr_claim_loop)
+  if (FIC && (DT != DT_I8 || warp >= 2 + kEpiWarps)) {  // int8: only the input-checksum warps hold a share
+    const long long w = DT == DT_I8 ? warp_sum(fr_acc) : __double_as_longlong(warp_sum_d(fr_facc));
+    if (lane == 0) s_rhs_all[warp] = w;
   }
 
   if (trace && warp == 2 && lane == 0) {
@@ -1375,14 +1418,14 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
         for (int w = 0; w < kEpiWarps; ++w) l += s_lhs[w];
         rec[4] = l;
         long long r = 0;
-        for (int w = 0; w < kRhsWarps; ++w) r += s_rhs[w];
+        for (int w = 0; w < kConvThreads / 32; ++w) r += s_rhs_all[w];
         rec[5] = r;
       } else {
         double l = 0.0;
         for (int w = 0; w < kEpiWarps; ++w) l += __longlong_as_double(s_lhs[w]);
         rec[4] = __double_as_longlong(l);
         double r = 0.0;
-        for (int w = 0; w < kRhsWarps; ++w) r += __longlong_as_double(s_rhs[w]);
+        for (int w = 0; w < kConvThreads / 32; ++w) r += __longlong_as_double(s_rhs_all[w]);
         rec[5] = __double_as_longlong(r);
       }
     }
