@@ -10,6 +10,7 @@
 // ships), so the rest of the drop-in stays dependency-free.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <filesystem>
 #include <fstream>
@@ -178,6 +179,29 @@ inline NetworkConfig load_network(const std::filesystem::path& path) {
   nlohmann::json j;
   f >> j;
   return network_from_json(j);
+}
+
+/// network_config.hpp apply_pruned_k / load_pruned: per-layer output-channel
+/// overrides {"layers": [{"id", "k"}], "name"?}; 1 <= k <= the layer's K
+inline NetworkConfig apply_pruned_k(const NetworkConfig& cfg, const nlohmann::json& pruned) {
+  NetworkConfig out = cfg;
+  for (const auto& e : pruned.at("layers")) {
+    const std::string id = e.at("id").get<std::string>();
+    const std::int64_t k = e.at("k").get<std::int64_t>();
+    auto it = std::find_if(out.layers.begin(), out.layers.end(), [&](const LayerConfig& l) { return l.id == id; });
+    if (it == out.layers.end()) throw std::invalid_argument("pruned config: unknown layer id '" + id + "'");
+    if (k < 1 || k > it->shape.k) throw std::invalid_argument("pruned config: bad k for layer '" + id + "'");
+    it->shape.k = k;
+  }
+  if (pruned.contains("name")) out.name = pruned.at("name").get<std::string>();
+  return out;
+}
+inline NetworkConfig load_pruned(const NetworkConfig& cfg, const std::filesystem::path& path) {
+  std::ifstream f(path);
+  if (!f) throw std::runtime_error("load_pruned: cannot open " + path.string());
+  nlohmann::json j;
+  f >> j;
+  return apply_pruned_k(cfg, j);
 }
 #endif
 

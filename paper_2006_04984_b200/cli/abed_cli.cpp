@@ -4,9 +4,8 @@
 // libabed_b200.so.  Same flags, the same CSV / JSON report schemas and the same
 // exit codes (0 success, 1 usage / config / IO error, 2 verification mismatch,
 // abed_main.cpp:29-31), plus `abft` (abed_main.cpp:425-487), the row/column
-// checksum ABFT-GEMM comparison, whose GEMMs and checks run on the B200 too.
-// `cost` (the analytic cost model) is not part of the protected-conv path and is
-// not provided.
+// checksum ABFT-GEMM comparison, whose GEMMs and checks run on the B200 too,
+// and `cost` (abed_main.cpp:350-417), the analytic op / byte model (host only).
 //
 // Flags are parsed by hand (the reference uses CLI11, which this image lacks);
 // the JSON reports use nlohmann/json like the reference.
@@ -102,16 +101,16 @@ void emit(const Args& a, const std::string& csv, const nlohmann::json& doc) {
 }
 
 // abed_main.cpp:68-92 resolve_network / resolve_layer
-LayerConfig resolve_layer(const Args& a) {
-  NetworkConfig cfg;
+NetworkConfig resolve_network(const Args& a) {
   if (a.has("--config") && a.has("--network")) throw UsageError("--config excludes --network");
   if (a.has("--image") && !a.has("--network")) throw UsageError("--image needs --network");
-  if (a.has("--config"))
-    cfg = load_network(a.get("--config", ""));
-  else if (a.has("--network"))
-    cfg = builtin_network(a.get("--network", ""), a.get("--image", "224"));
-  else
-    throw std::invalid_argument("one of --config or --network is required");
+  if (a.has("--config")) return load_network(a.get("--config", ""));
+  if (a.has("--network")) return builtin_network(a.get("--network", ""), a.get("--image", "224"));
+  throw std::invalid_argument("one of --config or --network is required");
+}
+
+LayerConfig resolve_layer(const Args& a) {
+  const NetworkConfig cfg = resolve_network(a);
   const std::string id = a.get("--layer", "");
   LayerConfig layer;
   if (cfg.has_layer(id)) {
@@ -389,6 +388,50 @@ int run_abft(const Args& a) {
   return kExitOk;
 }
 
+// abed_main.cpp:360-417 run_cost: per-layer and total op / byte counts of a
+// scheme and implementation option over a network, same CSV / JSON schema
+int run_cost(const Args& a) {
+  if (!a.has("--scheme")) throw UsageError("--scheme is required");
+  NetworkConfig cfg = resolve_network(a);
+  const Scheme scheme = parse_scheme(a.get("--scheme", "fic"));
+  const std::string opt = a.get("--option", "fr");
+  if (opt != "uf" && opt != "fr" && opt != "af") throw std::invalid_argument("unknown option '" + opt + "' (uf|fr|af)");
+  const ImplOption option = opt == "uf" ? ImplOption::UF : opt == "fr" ? ImplOption::FR : ImplOption::AF;
+  CostOptions opts;
+  opts.fc_planes = static_cast<int>(to_i64(a.get("--fc-planes", "4"), "--fc-planes"));
+  opts.fc_pad_to_8 = a.flags.count("--fc-pad8") != 0;
+  const NetworkConfig unpruned = cfg;
+  const bool pruned = a.has("--pruned");
+  if (pruned) cfg = load_pruned(cfg, a.get("--pruned", ""));
+  const CostReport rep = aggregate_network(cfg, scheme, option, opts, pruned ? &unpruned : nullptr);
+
+  std::ostringstream csv;
+  csv << "network,layer,scheme,option,fma,add,mul,act,cast,read_bytes,write_bytes,op_overhead_pct,byte_overhead_pct\n";
+  auto line = [&](const std::string& id, const OpCounts& o, const ByteCounts& b, double op_pct, double byte_pct) {
+    csv << rep.network << "," << id << "," << to_string(scheme) << "," << to_string(option) << "," << o.fma << ","
+        << o.add << "," << o.mul << "," << o.activation_eval << "," << o.cast << "," << b.read_bytes << ","
+        << b.write_bytes << "," << op_pct << "," << byte_pct << "\n";
+  };
+  auto fields = [](const OpCounts& o, const ByteCounts& b, double op_pct, double byte_pct) {
+    return nlohmann::json{{"fma", o.fma}, {"add", o.add}, {"mul", o.mul}, {"act", o.activation_eval},
+                          {"cast", o.cast}, {"read_bytes", b.read_bytes}, {"write_bytes", b.write_bytes},
+                          {"op_overhead_pct", op_pct}, {"byte_overhead_pct", byte_pct}};
+  };
+  nlohmann::json rows = nlohmann::json::array();
+  for (const auto& r : rep.rows) {
+    line(r.layer + (r.excluded ? " (excluded)" : ""), r.ops, r.bytes, r.op_overhead_pct(), r.byte_overhead_pct());
+    nlohmann::json j = {{"layer", r.layer}, {"excluded", r.excluded}};
+    j.update(fields(r.ops, r.bytes, r.op_overhead_pct(), r.byte_overhead_pct()));
+    rows.push_back(j);
+  }
+  line("TOTAL", rep.total_ops, rep.total_bytes, rep.op_overhead_pct(), rep.byte_overhead_pct());
+  const nlohmann::json doc{{"network", rep.network}, {"scheme", to_string(scheme)}, {"option", to_string(option)},
+                           {"layers", rows},
+                           {"total", fields(rep.total_ops, rep.total_bytes, rep.op_overhead_pct(), rep.byte_overhead_pct())}};
+  emit(a, csv.str(), doc);
+  return kExitOk;
+}
+
 const std::set<std::string> kLayerOpts = {"--config", "--network", "--image", "--layer", "--cap-hw", "--out"};
 
 std::set<std::string> with(std::set<std::string> base, std::initializer_list<const char*> more) {
@@ -406,6 +449,8 @@ void usage(std::ostream& os) {
         "  abed_b200 inject (--network NAME [--image ..] | --config FILE) --layer ID --scheme fc|ic|fic\n"
         "            --target input|filter|convout [--trials N] [--seed S] [--mode ones|random] [--jobs J]\n"
         "            [--scale X] [--cap-hw N] [--json] [--out FILE]\n"
+        "  abed_b200 cost (--network NAME [--image ..] | --config FILE) --scheme fc|ic|icbatch|fic [--option uf|fr|af]\n"
+        "            [--pruned FILE] [--fc-pad8] [--fc-planes 1..4] [--json] [--out FILE]\n"
         "  abed_b200 abft [--m M] [--n N] [--k K] [--trials T] [--seed S] [--single-pass] [--json] [--out FILE]\n"
         "exit codes: 0 success, 1 usage/config/IO error, 2 verification mismatch\n";
 }
@@ -436,6 +481,12 @@ int main(int argc, char** argv) {
                                              "--scale"}),
                            {"--json"});
       return run_inject(a);
+    }
+    if (cmd == "cost") {
+      const Args a = parse(argc, argv, {"--config", "--network", "--image", "--scheme", "--option", "--pruned",
+                                        "--fc-planes", "--out"},
+                           {"--fc-pad8", "--json"});
+      return run_cost(a);
     }
     if (cmd == "abft") {
       const Args a = parse(argc, argv, {"--m", "--n", "--k", "--trials", "--seed", "--out"}, {"--single-pass", "--json"});

@@ -174,3 +174,31 @@ def test_abft_report_and_copy_accounting(cli):  # cli_test.cpp:138-147
     code, out = run(cli, "abft --m 16 --n 12 --k 20 --trials 3 --seed 9 --single-pass --json")
     doc = json.loads(out)
     assert code == 0 and doc["copy_elements"] == 944 and doc["detected"] == 3 and len(doc["tasks"]) == 5
+
+
+def test_cost_report_columns_and_pruned_override(cli):  # cli_test.cpp:86, 107-129
+    code, out = run(cli, "cost --network vgg16 --image 224 --scheme fc --option uf")
+    assert code == 0, out
+    assert "network,layer,scheme,option,fma,add,mul,act,cast,read_bytes,write_bytes,op_overhead_pct,byte_overhead_pct" in out
+    assert "TOTAL" in out and "conv1_1 (excluded)" in out
+    code, pruned = run(cli, "cost --network vgg16 --image 224 --scheme fc --option uf --pruned "
+                       + os.path.join(GOLDEN, "vgg16_pruned.json"))
+    assert code == 0, pruned
+
+    def total_op_pct(text):
+        line = next(ln for ln in text.splitlines() if ",TOTAL," in ln)
+        return float(line.split(",")[-2])
+    assert total_op_pct(pruned) < total_op_pct(out)
+    assert run(cli, "cost --network resnet18 --image 1080p --scheme fic --option xx")[0] == 1
+
+
+def test_cost_json_matches_reference_model(cli):  # cli_test.cpp:130-136 + tests/golden/cost.json
+    code, out = run(cli, "cost --network resnet50 --image 1080p --scheme fic --option fr --json")
+    assert code == 0, out
+    doc = json.loads(out)
+    assert doc["network"] == "resnet50-1080p" and "op_overhead_pct" in doc["total"]
+    gold = next(r for r in json.load(open(os.path.join(GOLDEN, "cost.json")))["networks"]
+                if r["net"] == "resnet50-1080p" and r["scheme"] == "fic" and r["option"] == "fr")
+    t = doc["total"]
+    assert [t["fma"], t["add"], t["mul"], t["act"], t["cast"]] == gold["ops"]
+    assert [t["read_bytes"], t["write_bytes"]] == gold["bytes"]
