@@ -202,3 +202,16 @@ def test_cost_json_matches_reference_model(cli):  # cli_test.cpp:130-136 + tests
     t = doc["total"]
     assert [t["fma"], t["add"], t["mul"], t["act"], t["cast"]] == gold["ops"]
     assert [t["read_bytes"], t["write_bytes"]] == gold["bytes"]
+
+
+def test_cost_fc_plane_options(cli):  # cost --fc-pad8 / --fc-planes (abed_main.cpp:531-532)
+    def total_bytes(args):
+        code, out = run(cli, "cost --network resnet18 --image 224 --scheme fc --option fr --json " + args)
+        assert code == 0, out
+        t = json.loads(out)["total"]
+        return t["read_bytes"] + t["write_bytes"], t["fma"]
+    base, fma4 = total_bytes("")
+    pad, _ = total_bytes("--fc-pad8")
+    _, fma2 = total_bytes("--fc-planes 2")
+    assert pad > base and fma2 < fma4
+    assert run(cli, "cost --network resnet18 --image 224 --scheme fc --fc-planes 5")[0] == 1
