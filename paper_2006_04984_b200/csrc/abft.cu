@@ -416,8 +416,8 @@ int ceil_log2_i64(int64_t v) {  // checksum.hpp:53-62
 struct abed_abft_plan {
   int64_t m = 0, n = 0, k = 0;
   abed_conv_plan* aug = nullptr;    // (m+4)-pixel x (n+4)-filter GEMM, no checks
-  abed_conv_plan* plain = nullptr;  // m x n GEMM, no checks (lazy)
-  abed_conv_plan* fused = nullptr;  // m x n GEMM, FC row check in the epilogue (lazy)
+  abed_conv_plan* plain = nullptr;  // m x n GEMM, no checks
+  abed_conv_plan* fused = nullptr;  // m x n GEMM, FC row check in the epilogue
   int8_t* f = nullptr;              // transposed (n+4) x k filters
   int8_t* packed = nullptr;         // packed A (sized for the augmented plan)
   int32_t* colsum = nullptr;        // k
@@ -465,10 +465,6 @@ void run(abed_abft_plan* p, const int8_t* a, const int8_t* b, int32_t* c, int64_
   const int64_t m = p->m, n = p->n, k = p->k;
   const int digits = mode == ABED_ABFT_CHECKED ? kDigits : 0;
   abed_conv_plan* pl = mode == ABED_ABFT_CHECKED ? p->aug : mode == ABED_ABFT_PLAIN ? p->plain : p->fused;
-  if (!pl) {
-    pl = gemm_plan(p, 0, mode == ABED_ABFT_FUSED_ROW ? ABED_CHECK_FC : 0);
-    (mode == ABED_ABFT_PLAIN ? p->plain : p->fused) = pl;
-  }
   const ActGeom& g = pl->g;
   if (b) {
     // B side (skipped when b == NULL: B stays packed from an earlier run, i.e. the
@@ -528,6 +524,9 @@ abed_abft_plan* create(int64_t m, int64_t n, int64_t k) {
       cuda_check(cudaMalloc(&p->fc_out, 3 * sizeof(abed_verify_outcome)), "cudaMalloc(abft fc)");
       check_ws_alloc(p->ws, m, n);
       p->aug = gemm_plan(p, kDigits, 0);
+    // all three GEMM plans up front: runs stay allocation- and sync-free (graph capture)
+    p->plain = gemm_plan(p, 0, 0);
+    p->fused = gemm_plan(p, 0, ABED_CHECK_FC);
       cuda_check(cudaMalloc(&p->packed, (size_t)geom_packed_bytes(p->aug->g)), "cudaMalloc(abft packed)");
   } catch (...) {
     destroy(p);
