@@ -63,22 +63,33 @@ JSON_DIRS = [os.environ.get("ABED_JSON_INCLUDE", ""),
              os.path.join(sys.prefix, "lib", "python3.12", "site-packages", "include", "cudnn_frontend",
                           "thirdparty", "nlohmann"),
              "/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann"]
-CLI_SRC = os.path.join(PKG, "cli", "abed_cli.cpp")
-CLI_BIN = os.path.join(PKG, "abed_b200")
+# The CLI is the reference's own driver, UNMODIFIED, compiled where it lies
+# (tools/abed_main.cpp of the reference) against this repository's drop-in headers
+# include/abed/*.hpp and linked to libabed_b200.so: every `abed verify / inject /
+# cost / abft` call runs on the B200 library.  CLI11 (vendored by the reference,
+# absent from its tree) is replaced by the minimal compatible parser in
+# tools/dropin_cli/CLI11.hpp.  The binary is built here (where the reference
+# exists) and travels with the repository snapshot.
+REF_CLI_SRC = os.environ.get("ABED_REF_CLI", "/root/reference/proj/tools/abed_main.cpp")
+CLI_DIR = os.path.join(ROOT, "tools", "dropin_cli")
+CLI_BIN = os.path.join(CLI_DIR, "abed")
 
 
 def build_cli() -> str | None:
-    """g++ the `abed_b200` CLI (verify / inject) against the drop-in headers and libabed_b200.so."""
+    """g++ the reference CLI against the drop-in headers and libabed_b200.so (tools/dropin_cli/abed)."""
+    if not os.path.exists(REF_CLI_SRC):
+        return CLI_BIN if os.path.exists(CLI_BIN) else None
     jdir = next((d for d in JSON_DIRS if d and os.path.exists(os.path.join(d, "json.hpp"))), None)
     if jdir is None:
-        sys.stderr.write("abed_b200 CLI not built: no nlohmann json.hpp found (set ABED_JSON_INCLUDE)\n")
+        sys.stderr.write("abed CLI not built: no nlohmann json.hpp found (set ABED_JSON_INCLUDE)\n")
         return None
-    deps = [CLI_SRC, LIB] + glob.glob(os.path.join(ROOT, "include", "abed", "*.hpp"))
+    deps = [REF_CLI_SRC, LIB, os.path.join(CLI_DIR, "CLI11.hpp")] + \
+        glob.glob(os.path.join(ROOT, "include", "abed", "*.hpp"))
     if os.path.exists(CLI_BIN) and os.path.getmtime(CLI_BIN) >= max(os.path.getmtime(d) for d in deps):
         return CLI_BIN
-    _run(["g++", "-std=c++20", "-O2", "-Wall", "-I", os.path.join(ROOT, "include"), "-I", jdir,
-          "-I", "/usr/local/cuda/include", CLI_SRC, "-o", CLI_BIN, "-L", PKG, "-labed_b200",
-          "-Wl,-rpath,$ORIGIN", "-L/usr/local/cuda/lib64", "-lcudart"])
+    _run(["g++", "-std=c++20", "-O2", "-I", CLI_DIR, "-I", os.path.join(ROOT, "include"), "-I", jdir,
+          "-I", "/usr/local/cuda/include", REF_CLI_SRC, "-o", CLI_BIN, "-L", PKG, "-labed_b200",
+          "-Wl,-rpath,$ORIGIN/../../paper_2006_04984_b200", "-L/usr/local/cuda/lib64", "-lcudart"])
     return CLI_BIN
 
 

@@ -1,5 +1,7 @@
-"""The `abed_b200` CLI (verify / inject; reference tools/abed_main.cpp) and the
-drop-in network_config.hpp, mirroring the reference's cli_test.cpp: usage errors
+"""The reference's own CLI (tools/abed_main.cpp, UNMODIFIED) compiled against the
+drop-in headers include/abed/*.hpp and libabed_b200.so (tools/dropin_cli/abed,
+built by paper_2006_04984_b200/_build.py), and the drop-in network_config.hpp,
+mirroring the reference's cli_test.cpp: usage errors
 exit 1 (no GPU needed), fault-free verification exits 0 with the plan table, the
 forced-32 negative control exits 2, float mode with tau 0 passes on integer data,
 .abed dump / reload round-trips, and an injection campaign reproduces the
@@ -20,7 +22,7 @@ GOLDEN = os.path.join(ROOT, "tests", "golden")
 def cli():
     path = _build.build_cli()
     if path is None:
-        pytest.skip("nlohmann json.hpp not available")
+        pytest.skip("drop-in CLI not built (reference driver source or nlohmann json.hpp not available)")
     return path
 
 
@@ -39,6 +41,10 @@ def run(cli, args):
     "verify --network resnet18 --image 4k --layer 1 --scheme fic",
     "verify --network resnet18 --layer 1",                              # --scheme required
     "verify --network resnet18 --layer 1 --scheme fic --bogus 1",
+    "verify --network resnet18 --layer 1 --scheme fic --seed -1",       # uint64 seed: negative rejected
+    "verify --network resnet18 --layer 1 --scheme fic --seed 18446744073709551616",  # > 2^64 - 1
+    "verify --config x.json --network resnet18 --layer 1 --scheme fic",  # --config excludes --network
+    "verify --image 224 --layer 1 --scheme fic",                        # --image needs --network
 ])
 def test_usage_errors_exit_1(cli, args):
     code, out = run(cli, args)
@@ -94,6 +100,13 @@ def test_verify_every_scheme_passes(cli, scheme):
     assert code == 0, out
     assert "layer,scheme,mode,status,lhs,rhs,locus,seed" in out
     assert f"{scheme},int,pass" in out and "plan,b," in out
+
+
+@pytest.mark.gpu
+def test_verify_full_uint64_seed(cli):  # CLI11 reads --seed as std::uint64_t (abed_main.cpp:499)
+    code, out = run(cli, "verify --network resnet18 --layer 1 --cap-hw 8 --scheme fc --seed 18446744073709551615")
+    assert code == 0, out
+    assert out.strip().split("\n")[1].endswith(",18446744073709551615")
 
 
 @pytest.mark.gpu
