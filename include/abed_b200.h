@@ -238,8 +238,17 @@ int abed_run_campaign(const abed_campaign_config* config, int64_t trial_begin, i
  * and the per-tile verification workspace of one layer.  The activations live in
  * the packed strip-plane layout; abed_pack_input converts a
  * reference NCHW tensor, and a previous layer can write it directly
- * (ABED_OUT_I8_PACKED).  Scheme bits: ABED_CHECK_FC | ABED_CHECK_FIC | ABED_CHECK_IC. */
-enum { ABED_CHECK_FC = 1, ABED_CHECK_FIC = 2, ABED_CHECK_IC = 4 };
+ * (ABED_OUT_I8_PACKED).  Scheme bits: ABED_CHECK_FC | ABED_CHECK_FIC | ABED_CHECK_IC |
+ * ABED_CHECK_ICBATCH.
+ * ABED_CHECK_ICBATCH (int8, not with ABED_CHECK_IC) fuses ic_batch_checksum +
+ * conv_batch_checksum + ic_batch_verify (checksum.hpp:350-421): the packed input
+ * carries the batch-sum image as 2 (N <= 256) or 3 extra balanced base-256 digit
+ * images after the N real ones (written inside the conv kernel; the buffer size is
+ * abed_plan_info.packed_input_bytes), the tensor-core conv of those rows is the
+ * checksum row of the GEMM, and each run ends with a scan comparing the per-(k,p,q)
+ * batch sums of the outputs against it; its VerifyOutcome (locus (k, p, q)) is
+ * written into outcome slot 2 by finalize. */
+enum { ABED_CHECK_FC = 1, ABED_CHECK_FIC = 2, ABED_CHECK_IC = 4, ABED_CHECK_ICBATCH = 8 };
 enum {
   ABED_OUT_NONE = 0, ABED_OUT_I32_NCHW = 1, ABED_OUT_I8_NCHW = 2, ABED_OUT_F32_NCHW = 3,
   ABED_OUT_I8_PACKED = 4, ABED_OUT_I8_COMPARE = 5,
@@ -267,7 +276,7 @@ int abed_conv_plan_run(abed_conv_plan* plan, const int8_t* packed_input, const a
                        int32_t fault_bit, void* stream);
 /* Reduces the last run's per-CTA records into reference VerifyOutcomes (device
  * side, one small launch), asynchronously; outcome_dev points to 3 device
- * abed_verify_outcome {FC, FIC, IC}. */
+ * abed_verify_outcome {FC, FIC, IC or ICBatch}. */
 int abed_conv_plan_finalize(abed_conv_plan* plan, abed_verify_outcome* outcome_dev, void* stream);
 /* FIC-AF (fused_conv_epilog's next-layer input-checksum tap, checksum.hpp:605-631):
  * on = 1 marks that this int8 FIC plan's right-hand side is produced by the

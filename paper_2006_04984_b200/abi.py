@@ -20,7 +20,7 @@ FC, IC, ICBATCH, FIC = 0, 1, 2, 3
 TARGET_INPUT, TARGET_FILTER, TARGET_CONVOUT = 0, 1, 2
 DETECTED, SDC, MASKED, DETECTED_BENIGN = 0, 1, 2, 3
 DATA_ONES, DATA_RANDOM_I8 = 0, 1
-CHECK_FC, CHECK_FIC, CHECK_IC = 1, 2, 4
+CHECK_FC, CHECK_FIC, CHECK_IC, CHECK_ICBATCH = 1, 2, 4, 8
 # FIC input-checksum source (abed_conv_plan_set_input_checksum_source)
 RHS_STAGED, RHS_REREAD = 0, 1
 OUT_NONE, OUT_I32_NCHW, OUT_I8_NCHW, OUT_F32_NCHW, OUT_I8_PACKED, OUT_I8_COMPARE, OUT_H_PACKED, OUT_H_COMPARE = range(8)

@@ -39,7 +39,8 @@ int guarded(Fn&& fn) {
 
 // plan.cu
 // cpg: channels per 16-byte pixel group (16 for int8, 8 for fp16/bf16)
-abed_dev::ActGeom make_geom(const abed_layer_shape& s, int cpg = 16);
+// n_extra: ICBatch digit images appended after the n images (M-space and planes only)
+abed_dev::ActGeom make_geom(const abed_layer_shape& s, int cpg = 16, int n_extra = 0);
 int geom_strip_pix(const abed_dev::ActGeom& g);
 int64_t geom_packed_bytes(const abed_dev::ActGeom& g);
 bool choose_tiling(const abed_dev::ActGeom& g, bool fc, int force_block_n, abed_dev::ConvTcParams& p,
@@ -77,6 +78,9 @@ int conv_tc_grid(const abed_dev::ConvTcParams& p, int num_sms);
 int mma_pattern_of(const abed_dev::ActGeom& g, int gps);
 // pdl: launch with programmatic stream serialization (griddepcontrol in the kernel)
 cudaError_t conv_tc_launch(const abed_dev::ConvTcParams& p, int num_sms, bool pdl, cudaStream_t stream);
+// ICBatch: compare and reset after a fused run (p.icb_ready = {writer counter, ticket})
+cudaError_t icb_scan_launch(const abed_dev::ConvTcParams& p, int64_t* rec, abed_verify_outcome* out,
+                            cudaStream_t stream);
 // reduces the per-CTA verdict records of n plans (one block each)
 cudaError_t verdict_launch(const abed_dev::VerdictJob* jobs, int n, cudaStream_t stream);
 
@@ -157,6 +161,14 @@ struct abed_conv_plan {
   // (which is run with next = this plan); the verdict consumes and resets it
   int af_input = 0;
   unsigned long long* d_af_acc = nullptr;
+  // ICBatch fused (CHECK_ICB): batch sums of the outputs [K*P*Q], conv of the
+  // digit images [n_extra][K*P*Q], {writer counter, scan ticket}, scan records,
+  // the last run's outcome (copied into slot 2 by finalize)
+  unsigned long long* d_icb_lhs = nullptr;
+  int32_t* d_icb_dig = nullptr;
+  unsigned int* d_icb_ctl = nullptr;
+  int64_t* d_icb_rec = nullptr;
+  abed_verify_outcome* d_icb_out = nullptr;
   // float mode (fp16 / bf16 operands, f32 accumulators; abi_f16.cu)
   int dtype = 0;                 // abed_dev::DT_I8 / DT_F16 / DT_BF16
   double tau_fc = 0.0, tau_fic = 0.0;

@@ -60,7 +60,17 @@ void validate_shape(const abed_layer_shape& s) {
 void plan_init_common(abed_conv_plan* pl, const abed_layer_shape& shape, int checks, int force_bn, int cpg) {
   pl->shape = shape;
   pl->checks = checks;
-  pl->g = make_geom(shape, cpg);
+  if (checks & ~(ABED_CHECK_FC | ABED_CHECK_FIC | ABED_CHECK_IC | ABED_CHECK_ICBATCH))
+    throw_invalid("conv plan: unknown check bits");
+  int n_extra = 0;
+  if (checks & ABED_CHECK_ICBATCH) {
+    // ic_batch_checksum / conv_batch_checksum / ic_batch_verify fused (checksum.hpp:350-421)
+    if (cpg != 16) throw_invalid("ICBatch: the fused batch checksum is an int8 scheme");
+    if (checks & ABED_CHECK_IC) throw_invalid("ICBatch and IC share the third verdict slot: choose one");
+    if (shape.n > 65536) throw_invalid("ICBatch: batch too large for the 3-digit batch-sum image");
+    n_extra = shape.n <= 256 ? 2 : 3;  // balanced base-256 digits of sum_n x in [-128 N, 127 N]
+  }
+  pl->g = make_geom(shape, cpg, n_extra);
   const ActGeom& g = pl->g;
   ConvTcParams& p = pl->base;
   std::memset(&p, 0, sizeof(p));
@@ -90,6 +100,7 @@ void plan_init_common(abed_conv_plan* pl, const abed_layer_shape& shape, int che
       p.tap_a16[t] = (uint32_t)(p.tap_phase[t] * p.gps * p.strip_pix + p.tap_shift[t]);
     }
   p.m_total = g.m_total;
+  p.m_real = (int64_t)g.n * g.Hl * g.Wl;
   p.m_tiles = g.m_tiles;
   p.Hl = g.Hl; p.Wl = g.Wl; p.P = g.p; p.Q = g.q; p.N = g.n; p.K = g.k;
   p.fault_key = -1;
@@ -112,6 +123,17 @@ void plan_init_common(abed_conv_plan* pl, const abed_layer_shape& shape, int che
   cuda_check(cudaMemset(pl->d_zero_bias, 0, shape.k * 4), "memset bias");
   cuda_check(cudaMalloc(&pl->d_af_acc, 8), "cudaMalloc(af_acc)");
   cuda_check(cudaMemset(pl->d_af_acc, 0, 8), "memset af_acc");
+  if (n_extra) {
+    const size_t kpq = (size_t)shape.k * shape.p * shape.q;
+    cuda_check(cudaMalloc(&pl->d_icb_lhs, kpq * 8), "cudaMalloc(icb_lhs)");
+    cuda_check(cudaMemset(pl->d_icb_lhs, 0, kpq * 8), "memset icb_lhs");
+    cuda_check(cudaMalloc(&pl->d_icb_dig, kpq * 4 * n_extra), "cudaMalloc(icb_dig)");
+    cuda_check(cudaMalloc(&pl->d_icb_ctl, 8), "cudaMalloc(icb_ctl)");
+    cuda_check(cudaMemset(pl->d_icb_ctl, 0, 8), "memset icb_ctl");
+    cuda_check(cudaMalloc(&pl->d_icb_rec, (size_t)abed_dev::kIcbScanBlocks * 4 * 8), "cudaMalloc(icb_rec)");
+    cuda_check(cudaMalloc(&pl->d_icb_out, sizeof(abed_verify_outcome)), "cudaMalloc(icb_out)");
+    cuda_check(cudaMemset(pl->d_icb_out, 0, sizeof(abed_verify_outcome)), "memset icb_out");
+  }
 }
 
 // FIC-SM class table.  A phase row i is reached by the filter rows
@@ -395,9 +417,19 @@ void plan_run(abed_conv_plan* pl, const int8_t* packed, const abed_epilog_params
       }
     }
   }
+  if (pl->checks & ABED_CHECK_ICBATCH) {
+    p.icb_d = pl->g.n_extra;
+    p.icb_lhs = pl->d_icb_lhs;
+    p.icb_dig = pl->d_icb_dig;
+    p.icb_ready = pl->d_icb_ctl;
+    // SMs the conv grid leaves idle help write the digit images
+    if (p.ic_ctas == 0 && num_sms() - p.conv_grid >= 16) p.ic_ctas = num_sms() - p.conv_grid;
+    p.icb_writers = (unsigned)(2 * p.conv_grid + (abed_dev::kConvThreads_host / 32) * p.ic_ctas);
+  }
   pl->last_rhs_mode = p.rhs_mode;
   pl->last_grid = p.conv_grid + p.ic_ctas;
   cuda_check(conv_tc_launch(p, num_sms(), pl->pdl != 0, st), "conv_i8_tc launch");
+  if (p.icb_d) cuda_check(icb_scan_launch(p, pl->d_icb_rec, pl->d_icb_out, st), "icb_scan launch");
 }
 
 abed_dev::VerdictJob plan_verdict_job(const abed_conv_plan* pl, abed_verify_outcome* out_dev) {
@@ -408,6 +440,7 @@ abed_dev::VerdictJob plan_verdict_job(const abed_conv_plan* pl, abed_verify_outc
   j.Q = pl->g.q;
   j.dtype = pl->dtype;
   j.checks = pl->checks & (ABED_CHECK_FC | ABED_CHECK_FIC);
+  j.icb = pl->d_icb_out;  // ICBatch verdict of the last run -> slot 2 (nullptr: not an ICBatch plan)
   j.rhs_mode = pl->last_rhs_mode;
   j.rhs_ext = pl->d_acc;
   j.af_acc = pl->d_af_acc;
@@ -423,14 +456,14 @@ abed_dev::VerdictJob plan_verdict_job(const abed_conv_plan* pl, abed_verify_outc
   j.m_tiles = pl->g.m_tiles;
   j.Hl = pl->g.Hl;
   j.Wl = pl->g.Wl;
-  j.m_total = pl->g.m_total;
+  j.m_total = (int64_t)pl->g.n * pl->g.Hl * pl->g.Wl;  // real images only
   j.tau_fc = pl->tau_fc;
   return j;
 }
 
 void plan_finalize(abed_conv_plan* pl, abed_verify_outcome* out_dev, cudaStream_t st) {
   // FC / FIC: reduce the conv kernel's per-CTA records into VerifyOutcomes
-  if (pl->checks & (ABED_CHECK_FC | ABED_CHECK_FIC)) {
+  if (pl->checks & (ABED_CHECK_FC | ABED_CHECK_FIC | ABED_CHECK_ICBATCH)) {
     const abed_dev::VerdictJob j = plan_verdict_job(pl, out_dev);
     cuda_check(verdict_launch(&j, 1, st), "verdict");
   }
@@ -495,6 +528,8 @@ int abed_conv_plan_destroy(abed_conv_plan* pl) {
   cudaFree(pl->d_facc); cudaFree(pl->d_rhs_f); cudaFree(pl->d_ficwf); cudaFree(pl->d_fsum_f); cudaFree(pl->d_dwf);
   cudaFree(pl->d_af_acc); cudaFree(pl->d_ficc8);  // row / column classes live inside it
   cudaFree(pl->d_acc); cudaFree(pl->d_zero_bias);
+  cudaFree(pl->d_icb_lhs); cudaFree(pl->d_icb_dig); cudaFree(pl->d_icb_ctl); cudaFree(pl->d_icb_rec);
+  cudaFree(pl->d_icb_out);
   delete pl;
   return ABED_OK;
 }
@@ -542,7 +577,8 @@ int abed_conv_plan_finalize_many(abed_conv_plan* const* plans, int32_t n, abed_v
     std::vector<abed_dev::VerdictJob> jobs;
     for (int i = 0; i < n; ++i) {
       abed_conv_plan* pl = plans[i];
-      if (pl->checks & (ABED_CHECK_FC | ABED_CHECK_FIC)) jobs.push_back(plan_verdict_job(pl, outcomes_dev + 3 * i));
+      if (pl->checks & (ABED_CHECK_FC | ABED_CHECK_FIC | ABED_CHECK_ICBATCH))
+        jobs.push_back(plan_verdict_job(pl, outcomes_dev + 3 * i));
       if (pl->checks & ABED_CHECK_IC)
         ic_finalize_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(pl->d_acc + 4, pl->d_filters, pl->d_ic, pl->shape.k,
                                                                pl->shape.c * pl->shape.r * pl->shape.s,

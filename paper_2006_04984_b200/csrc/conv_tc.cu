@@ -130,6 +130,7 @@ __global__ void __launch_bounds__(256) verdict_kernel(const __grid_constant__ Ve
       out[0].rhs_f = __longlong_as_double(r.rhs);
     }
   }
+  if (j.icb) out[2] = *static_cast<const abed_verify_outcome*>(j.icb);  // ICBatch (icb_scan_kernel)
   if (j.checks & CHECK_FIC) {
     if (j.dtype == DT_I8) {
       long long rhs;
@@ -152,6 +153,78 @@ __global__ void __launch_bounds__(256) verdict_kernel(const __grid_constant__ Ve
       if (j.rhs_mode) *j.rhs_ext_f = rhs;
     }
   }
+}
+
+// ICBatch verdict (ic_batch_verify, checksum.hpp:398-421) after the fused conv:
+// for every (k, p, q) the batch sum of the outputs (icb_lhs, accumulated by the
+// epilogue) against conv_batch_checksum = sum_j 256^j conv(d_j) (icb_dig, the
+// digit images' rows); mismatch count and the first mismatch in the reference's
+// (k, p, q) order with its lhs / rhs.  Resets icb_lhs and the writer counter for
+// the next run; the last block (ticket) folds the per-block records.
+__global__ void __launch_bounds__(256) icb_scan_kernel(unsigned long long* __restrict__ lhs,
+                                                       const int32_t* __restrict__ dig, int D, int64_t kpq,
+                                                       int64_t PQ, int Q, int64_t* __restrict__ rec,
+                                                       unsigned int* __restrict__ ctl, abed_verify_outcome* out) {
+  pdl_launch_dependents();  // the next layer's prologue may overlap this scan
+  pdl_wait();
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  FcRec r{0, kNoKey, 0, 0};
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + t; i < kpq;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const long long l = static_cast<long long>(__ldcg(lhs + i));
+    long long rr = __ldcg(dig + i);
+    rr += static_cast<long long>(__ldcg(dig + kpq + i)) << 8;
+    if (D > 2) rr += static_cast<long long>(__ldcg(dig + 2 * kpq + i)) << 16;
+    if (l != rr) fc_note(r, i, l, rr);
+    lhs[i] = 0ull;
+  }
+  __shared__ FcRec s_r[8];
+  __shared__ bool s_last;
+  r = fc_warp_reduce(r);
+  if (lane == 0) s_r[w] = r;
+  __syncthreads();
+  if (t == 0) {
+    FcRec b{0, kNoKey, 0, 0};
+    for (int q = 0; q < static_cast<int>(blockDim.x >> 5); ++q) {
+      b.cnt += s_r[q].cnt;
+      if (s_r[q].key < b.key) b = FcRec{b.cnt, s_r[q].key, s_r[q].lhs, s_r[q].rhs};
+    }
+    int64_t* my = rec + static_cast<int64_t>(blockIdx.x) * 4;
+    my[0] = b.cnt;
+    my[1] = b.key;
+    my[2] = b.lhs;
+    my[3] = b.rhs;
+    __threadfence();
+    s_last = atomicAdd(&ctl[1], 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  FcRec a{0, kNoKey, 0, 0};
+  for (int c = t; c < static_cast<int>(gridDim.x); c += blockDim.x) {
+    const int64_t* q = rec + static_cast<int64_t>(c) * 4;
+    const int64_t cnt = __ldcg(q);
+    if (cnt > 0) {
+      a.cnt += cnt;
+      const int64_t key = __ldcg(q + 1);
+      if (key < a.key) a = FcRec{a.cnt, key, __ldcg(q + 2), __ldcg(q + 3)};
+    }
+  }
+  a = fc_warp_reduce(a);
+  if (lane == 0) s_r[w] = a;
+  __syncthreads();
+  if (t != 0) return;
+  FcRec f{0, kNoKey, 0, 0};
+  for (int q = 0; q < static_cast<int>(blockDim.x >> 5); ++q) {
+    f.cnt += s_r[q].cnt;
+    if (s_r[q].key < f.key) f = FcRec{f.cnt, s_r[q].key, s_r[q].lhs, s_r[q].rhs};
+  }
+  if (f.cnt == 0)  // checksum.hpp:420 VerifyOutcome::ok()
+    write_outcome_dev(out, 0, 0, 0, 0, 0, 0, 0, 0);
+  else  // locus (k, p, q)
+    write_outcome_dev(out, 1, 1, f.key / PQ, (f.key % PQ) / Q, f.key % Q, f.lhs, f.rhs, f.cnt);
+  ctl[0] = 0u;  // icb_ready
+  ctl[1] = 0u;  // ticket
 }
 
 }  // namespace abed_dev
@@ -209,6 +282,23 @@ cudaError_t verdict_launch(const abed_dev::VerdictJob* jobs, int n, cudaStream_t
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
+}
+
+cudaError_t icb_scan_launch(const ConvTcParams& p, int64_t* rec, abed_verify_outcome* out, cudaStream_t stream) {
+  const int64_t kpq = static_cast<int64_t>(p.K) * p.P * p.Q;
+  int blocks = static_cast<int>((kpq + 255) / 256);
+  if (blocks > abed_dev::kIcbScanBlocks) blocks = abed_dev::kIcbScanBlocks;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(256);
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, abed_dev::icb_scan_kernel, p.icb_lhs, static_cast<const int32_t*>(p.icb_dig),
+                            p.icb_d, kpq, static_cast<int64_t>(p.P) * p.Q, p.Q, rec, p.icb_ready, out);
 }
 
 cudaError_t conv_tc_launch(const ConvTcParams& p_in, int num_sms, bool pdl, cudaStream_t stream) {

@@ -51,6 +51,7 @@ enum CheckBits : int {
   CHECK_FC = 1,   // filter checksum columns ride in B (checksum.hpp:211 fc_verify)
   CHECK_FIC = 2,  // full-output int64 sum per tile (checksum.hpp:287 fic_verify)
   CHECK_IC = 4,   // per-output-channel int64 sums (checksum.hpp:319 ic_verify_k)
+  CHECK_ICB = 8,  // ICBatch: the batch-sum image rides as extra A images (checksum.hpp:350-421)
 };
 
 // Geometry of one conv layer in packed form (computed on the host).
@@ -66,7 +67,8 @@ struct ActGeom {
   int Hl, Wl;              // M-space rows per image / pixels per row
   int max_shift;           // largest tap pixel shift
   int m_tiles;             // ceil(m_total / 128)
-  int64_t m_total;         // n * Hl * Wl
+  int n_extra;             // ICBatch: balanced base-256 digit images of the batch sum after the n images
+  int64_t m_total;         // (n + n_extra) * Hl * Wl
   int64_t plane_len;       // pixels per plane (covers the last strip)
 };
 
@@ -143,6 +145,20 @@ struct ConvTcParams {
   int64_t af_HlWl;             // next layer's pixels per image plane
   unsigned long long* ic_sum;  // [K] per-channel output sums (atomic, integer => deterministic)
   unsigned long long* cmp_count;  // OUT_I8_COMPARE mismatch count
+  // ICBatch (ic_batch_checksum + conv_batch_checksum + ic_batch_verify,
+  // checksum.hpp:350-421) fused: the packed input carries icb_d extra images
+  // after the N real ones -- the balanced base-256 digit planes of the batch-sum
+  // image sum_n x[n] -- written inside this kernel by the input-checksum warps
+  // (and input-checksum CTAs); the producer loads an A strip that reaches them
+  // only after every writer warp has signalled icb_ready.  The epilogue adds each
+  // real output into icb_lhs[k][p][q] (int64 reduction) and stores the digit
+  // rows' conv into icb_dig[j][k][p][q]; icb_scan_kernel compares afterwards.
+  int icb_d;                        // digit images (0 = ICBatch off)
+  int64_t m_real;                   // N * Hl * Wl: GEMM rows of the real images
+  unsigned long long* icb_lhs;      // [K*P*Q] sum_n ConvOut (reset by the scan)
+  int32_t* icb_dig;                 // [icb_d][K*P*Q] conv of digit image j
+  unsigned int* icb_ready;          // writer warps done (reset by the scan)
+  unsigned int icb_writers;         // writer warps in this launch
   // ---- fault hook (ConvOut target): flip `fault_bit` of output element
   // (n,k,p,q) = fault_key in reference flat order before checks and epilog.
   int64_t fault_key;  // -1 = none
@@ -183,8 +199,11 @@ struct VerdictJob {
   double* rhs_ext_f;
   double tau_fic;
   void* out;           // abed_verify_outcome[3] {FC, FIC, IC}
+  const void* icb;     // ICBatch outcome of the last run (copied into out[2]) or nullptr
 };
 constexpr int kMaxVerdictJobs = 32;
+// ICBatch verdict (icb_scan_kernel): per-block records {count, first key, lhs, rhs}
+constexpr int kIcbScanBlocks = 296;
 struct VerdictBatch {
   int n;
   VerdictJob job[kMaxVerdictJobs];

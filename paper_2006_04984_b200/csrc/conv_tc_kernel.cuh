@@ -237,6 +237,8 @@ struct EpiCtx {
   bool chunk32, valid, fault_row;
   const uint4* af_row;     // FIC-AF: next layer's digit cell of this pixel, group 0 (nullptr: off)
   int64_t af_gstride;      // uint4 stride between channel groups of the digit planes
+  unsigned long long* icb_lhs;  // ICBatch, real row: &icb_lhs[0][p][q] (nullptr: not a real row)
+  int32_t* icb_dig;             // ICBatch, digit row j: &icb_dig[j][0][p][q] (nullptr: not a digit row)
 };
 
 // One 16-channel chunk of one row: (slow path only: fault hook, filler trim,
@@ -278,6 +280,21 @@ __device__ __forceinline__ int64_t epi_chunk(const ConvTcParams& p, const EpiCtx
     for (int j = 0; j < 16; ++j) {
       const long long s = warp_sum(e.valid ? a[j] : 0);
       if (lane == j && k0 + j < p.K && s != 0) atomicAdd(&p.ic_sum[k0 + j], static_cast<unsigned long long>(s));
+    }
+  }
+  if (SLOW && p.icb_d) {
+    // ICBatch (checksum.hpp:398-421): real rows add their outputs into the
+    // per-(k, p, q) batch sums; rows of digit image j keep conv(d_j) for the scan
+    if (e.icb_lhs) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (k0 + j < p.K)
+          red_add_u64(e.icb_lhs + static_cast<int64_t>(k0 + j) * e.PQ,
+                      static_cast<unsigned long long>(static_cast<long long>(a[j])));
+    } else if (e.icb_dig) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (k0 + j < p.K) e.icb_dig[static_cast<int64_t>(k0 + j) * e.PQ] = a[j];
     }
   }
   if (EPI == EPI_PACKED || EPI == EPI_COMPARE) {
@@ -767,6 +784,83 @@ __device__ __forceinline__ void fr_claim_loop(const ConvTcParams& p, int* s_clai
   }
 }
 
+// ICBatch writer (ic_batch_checksum, checksum.hpp:350-362, fused): cells
+// first, first + stride, ... of (plane, pixel) of the packed input; per cell the
+// 16 channel bytes are summed over the N images (x ^ 0x80 = x + 128 as unsigned
+// bytes, even / odd bytes in 16-bit lanes, flushed every 128 images) and the sum
+// s in [-128 N, 127 N] is stored as icb_d balanced base-256 digit images after
+// the real ones (digit image j at M-space image N + j), so the tensor-core conv of
+// those rows gives conv(d_j) exactly and sum_j 256^j conv(d_j) = conv_batch_checksum.
+// Then one release increment of icb_ready per warp (the producers of tiles that
+// reach the digit images wait for every writer warp).
+__device__ __forceinline__ void icb_write_digits(const ConvTcParams& p, int64_t first, int64_t stride) {
+  const int64_t HlWl = static_cast<int64_t>(p.Hl) * p.Wl;
+  const int64_t cells = static_cast<int64_t>(p.n_phase) * p.c16 * HlWl;
+  for (int64_t idx = first; idx < cells; idx += stride) {
+    const int64_t plane = idx / HlWl, pix = idx - plane * HlWl;
+    const uint4* src = reinterpret_cast<const uint4*>(p.act) + plane * p.plane_len + pix;
+    int32_t s[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) s[e] = 0;
+    for (int n0 = 0; n0 < p.N; n0 += 128) {
+      const int n1 = n0 + 128 < p.N ? n0 + 128 : p.N;
+      uint32_t lo[4] = {0u, 0u, 0u, 0u}, hi[4] = {0u, 0u, 0u, 0u};
+      for (int n = n0; n < n1; n += 8) {
+        uint4 x[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          x[j] = n + j < n1 ? __ldcg(src + static_cast<int64_t>(n + j) * HlWl) : make_uint4(0x80808080u, 0x80808080u,
+                                                                                             0x80808080u, 0x80808080u);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t w[4] = {x[j].x ^ 0x80808080u, x[j].y ^ 0x80808080u, x[j].z ^ 0x80808080u,
+                                 x[j].w ^ 0x80808080u};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            lo[q] += w[q] & 0x00FF00FFu;
+            hi[q] += (w[q] >> 8) & 0x00FF00FFu;
+          }
+        }
+      }
+      // padded slots added 0x80 ^ 0x80 = 0; real ones x + 128
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        s[4 * q + 0] += static_cast<int32_t>(lo[q] & 0xFFFFu);
+        s[4 * q + 2] += static_cast<int32_t>(lo[q] >> 16);
+        s[4 * q + 1] += static_cast<int32_t>(hi[q] & 0xFFFFu);
+        s[4 * q + 3] += static_cast<int32_t>(hi[q] >> 16);
+      }
+    }
+    uint32_t dw[3][4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) dw[0][q] = dw[1][q] = dw[2][q] = 0u;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      int32_t v = s[e] - 128 * p.N;
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const int32_t dg = d < 2 ? ((v + 128) & 0xFF) - 128 : v;  // the last digit takes the rest (|v| <= 128)
+        v = (v - dg) >> 8;                                         // exact: v - dg is a multiple of 256
+        dw[d][e >> 2] |= (static_cast<uint32_t>(dg) & 0xFFu) << (8 * (e & 3));
+      }
+    }
+    uint4* dst = reinterpret_cast<uint4*>(const_cast<int8_t*>(p.act)) + plane * p.plane_len +
+                 static_cast<int64_t>(p.N) * HlWl + pix;
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+      if (d < p.icb_d) dst[static_cast<int64_t>(d) * HlWl] = make_uint4(dw[d][0], dw[d][1], dw[d][2], dw[d][3]);
+  }
+  __threadfence();
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) red_release_gpu_add(p.icb_ready, 1u);
+}
+
+// producer side: every digit writer warp of the grid has released its stores
+__device__ __forceinline__ void icb_wait_ready(const ConvTcParams& p) {
+  while (ld_acquire_gpu(p.icb_ready) < p.icb_writers) __nanosleep(64);
+  fence_proxy_async_global();  // the bulk copies (async proxy) now see them
+}
+
 // pattern ids (host: mma_pattern_of in plan.cu)
 enum MmaPattern : int {
   PAT_GENERIC = 0,
@@ -806,6 +900,12 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
     long long acc = 0;
     double facc_rhs = 0.0;
     pdl_wait();
+    if (DT == DT_I8 && p.icb_d) {
+      const int64_t writers = static_cast<int64_t>(p.conv_grid) * (kRhsWarps * 32) +
+                              static_cast<int64_t>(p.ic_ctas) * kConvThreads;
+      icb_write_digits(p, static_cast<int64_t>(p.conv_grid) * (kRhsWarps * 32) +
+                              static_cast<int64_t>(blockIdx.x - p.conv_grid) * kConvThreads + threadIdx.x, writers);
+    }
     if (FIC && p.rhs_mode == 1)
       fic_rhs_fr<DT, 16>(p, static_cast<int64_t>(blockIdx.x - p.conv_grid) * kConvThreads + threadIdx.x,
                      static_cast<int64_t>(p.ic_ctas) * kConvThreads, acc, facc_rhs);
@@ -930,10 +1030,15 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt_));
         trace[16] = static_cast<int64_t>(gt_);
       }
+      bool icb_seen = false;
       for (int u = 0; u < n_units; ++u) {
         int mt, nt;
         decode_tile(p, u, mt, nt);
         const int64_t m0 = static_cast<int64_t>(mt) * kBlockM;
+        if (DT == DT_I8 && p.icb_d && !icb_seen && m0 + p.strip_pix > p.m_real) {
+          icb_wait_ready(p);  // this tile's strips reach the ICBatch digit images
+          icb_seen = true;
+        }
         for (int ks = 0; ks < p.k_stages; ++ks) {
           const bool prefetched = u * p.k_stages + ks < pre;
           if (!prefetched) {
@@ -1055,6 +1160,17 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
         qq = rem - pp * p.Wl;
         valid = pp < static_cast<uint32_t>(p.P) && qq < static_cast<uint32_t>(p.Q);
       }
+      e.icb_lhs = nullptr;
+      e.icb_dig = nullptr;
+      if (DT == DT_I8 && p.icb_d && valid) {
+        const int64_t kq = static_cast<int64_t>(pp) * p.Q + qq;
+        if (n_img >= static_cast<uint32_t>(p.N)) {  // ICBatch digit row: no output, no FC / FIC
+          e.icb_dig = p.icb_dig + static_cast<int64_t>(n_img - p.N) * p.K * e.PQ + kq;
+          valid = false;
+        } else {
+          e.icb_lhs = p.icb_lhs + kq;
+        }
+      }
       e.valid = valid;
       const int64_t key = static_cast<int64_t>(n_img) * e.PQ + static_cast<int64_t>(pp) * p.Q + qq;
       e.fault_row = valid && p.fault_key >= 0 && n_img == fk_n && (key - static_cast<int64_t>(n_img) * e.PQ) == fk_pq;
@@ -1103,7 +1219,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
       uint32_t dig[4] = {0u, 0u, 0u, 0u};
       if (FC && part == 0) tmem_ld4(t_row + p.block_n, dig);
       // fast path: no fault hook, no filler channels, no IC column sums (warp-uniform)
-      const bool slow = p.fault_key >= 0 || (p.check & CHECK_IC) || k_base + c_hi * 16 > p.K;
+      const bool slow = p.fault_key >= 0 || (p.check & CHECK_IC) || p.icb_d || k_base + c_hi * 16 > p.K;
       Acc row_sum = 0;
       if (p.dbg & 1) {
       } else if (!slow) {
@@ -1230,6 +1346,13 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
     const int rw = warp - (2 + kEpiWarps);
     long long acc = 0;
     double facc_rhs = 0.0;
+    if (DT == DT_I8 && p.icb_d) {
+      // ICBatch digit images first: the producers of the last tiles wait for them
+      pdl_wait();
+      icb_write_digits(p, static_cast<int64_t>(blockIdx.x) * (kRhsWarps * 32) + rw * 32 + lane,
+                       static_cast<int64_t>(p.conv_grid) * (kRhsWarps * 32) +
+                           static_cast<int64_t>(p.ic_ctas) * kConvThreads);
+    }
     if (DT != DT_I8 && FIC && p.rhs_mode == 1 && p.ic_ctas == 0) {
       pdl_wait();
       if (fr_share) {
@@ -1276,7 +1399,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
 #pragma unroll
         for (int x = 0; x < kPx; ++x) {
           const uint32_t t = static_cast<uint32_t>(mt) * kBlockM + it + x * kIcThreads;
-          ok[x] = own && t < static_cast<uint64_t>(p.m_total);
+          ok[x] = own && t < static_cast<uint64_t>(p.m_real);  // real images only
           uint32_t i = 0, j = 0;
           if (ok[x]) {
             uint32_t n_img = __float2uint_rz(__fmul_rz(__uint2float_rz(t), rcp_hlwl));

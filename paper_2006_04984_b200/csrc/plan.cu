@@ -24,7 +24,7 @@ using abed_dev::ConvTcParams;
 
 static inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
-ActGeom make_geom(const abed_layer_shape& s, int cpg) {
+ActGeom make_geom(const abed_layer_shape& s, int cpg, int n_extra) {
   ActGeom g{};
   g.n = (int)s.n; g.c = (int)s.c; g.h = (int)s.h; g.w = (int)s.w;
   g.k = (int)s.k; g.r = (int)s.r; g.s = (int)s.s;
@@ -47,7 +47,8 @@ ActGeom make_geom(const abed_layer_shape& s, int cpg) {
   g.Hl = extent(g.p, g.h, g.r, g.sh, g.ph, g.nph_h);
   g.Wl = extent(g.q, g.w, g.s, g.sw, g.pw, g.nph_w);
   g.max_shift = ((g.r - 1) / g.sh) * g.Wl + (g.s - 1) / g.sw;
-  g.m_total = (int64_t)g.n * g.Hl * g.Wl;
+  g.n_extra = n_extra;
+  g.m_total = (int64_t)(g.n + n_extra) * g.Hl * g.Wl;
   g.m_tiles = (int)ceil_div(g.m_total, abed_dev::kBlockM);
   const int strip = (int)((abed_dev::kBlockM + g.max_shift + 7) / 8 * 8);
   g.plane_len = (int64_t)(g.m_tiles - 1) * abed_dev::kBlockM + strip;
@@ -74,7 +75,7 @@ __global__ void pack_input_kernel(const int8_t* __restrict__ x, ActGeom g, int8_
     const int grp = (int)(plane % g.c16);
     const int phase = (int)(plane / g.c16);
     uint32_t w4[4] = {0, 0, 0, 0};
-    if (t < g.m_total) {
+    if (t < (int64_t)g.n * HlWl) {
       const int n = (int)(t / HlWl);
       const int64_t rem = t - n * HlWl;
       const int i = (int)(rem / g.Wl), j = (int)(rem % g.Wl);

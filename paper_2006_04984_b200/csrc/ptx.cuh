@@ -264,6 +264,25 @@ __device__ __forceinline__ unsigned long long atom_add_acq_rel_gpu(unsigned long
   return old;
 }
 
+// cross-CTA hand-off of generic-proxy global stores to later bulk copies
+// (async proxy) in other CTAs: the writer fences and releases a counter, the
+// reader acquires it and fences the async proxy before issuing its copies
+__device__ __forceinline__ void red_release_gpu_add(unsigned int* addr, unsigned int v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned int ld_acquire_gpu(const unsigned int* addr) {
+  unsigned int v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+// fire-and-forget 64-bit integer reduction into global memory (L2 atomics)
+__device__ __forceinline__ void red_add_u64(unsigned long long* addr, unsigned long long v) {
+  asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(addr), "l"(v) : "memory");
+}
+
 // named barrier over `count` threads (count multiple of 32)
 __device__ __forceinline__ void named_bar(uint32_t id, uint32_t count) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
