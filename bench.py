@@ -53,6 +53,16 @@ WORKLOAD = "resnet50-3x3-convs-int8-b32 (16 layers, fused bias+ReLU+requant, FIC
 PEAK_INT8_NOMINAL = 4500.0
 
 
+def workload_config(per_gpu_batch, world, global_batch=0):
+    """The `config` object both arms print (identical for the same workload)."""
+    return {"workload": WORKLOAD if not global_batch else WORKLOAD.replace("-b32", f"-b{per_gpu_batch * world}"),
+            "global_batch": per_gpu_batch * world, "per_gpu_batch": per_gpu_batch, "layers": 16,
+            "shapes": "ResNet-50 conv2 3x3 of every bottleneck (network_config.hpp:233-282), stride 2 at the first of "
+                      "layer2-4, pad 1", "epilog": "bias linspace(-2,2), scale 0.05, ReLU, int8 requantise",
+            "check": "FIC", "parallelism": f"dp{world}",
+            "l2": "GPU arm: flushed (512 MiB memset) before every timed step"}
+
+
 def layer_ops(c, h, w, k, stride, n=BATCH):
     p = (h + 2 - 3) // stride + 1
     q = (w + 2 - 3) // stride + 1
@@ -151,8 +161,8 @@ def run_reference_arm(args, world, rank):
         "warmup": args.warmup, "ms_per_step": round(1e3 * statistics.mean(per), 2), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int8", "data": "synthetic (random int8, numpy)",
         "impl": "reference",
-        "config": {"workload": WORKLOAD, "global_batch": BATCH, "per_gpu_batch": BATCH, "layers": 16,
-                   "parallelism": "host CPU threads (rank 0 only)"},
+        "config": workload_config(BATCH, world),
+        "method": {"where": "host CPU threads (rank 0 only)", "threads": threads},
         "cpu_baseline": {"value": round(value, 5), "unit": "TOPS", "cores": min(threads, BATCH), "kind": kind,
                          "sample": desc},
         "e2e": {"value": round(value, 5), "unit": "TOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -708,23 +718,33 @@ def run_ours(args, world, rank, local):
         bias = torch.linspace(-2.0, 2.0, k).tolist()
         L = {"name": name, "ls": ls, "x": x, "f": f, "ops": layer_ops(c, h, w, k, st)}
         L["plans"] = {"unprotected": api.ConvPlan(ls, f, 0), "fc": api.ConvPlan(ls, f, abi.CHECK_FC),
-                      "fic": api.ConvPlan(ls, f, abi.CHECK_FIC), "fic_sm": api.ConvPlan(ls, f, abi.CHECK_FIC)}
+                      "fic": api.ConvPlan(ls, f, abi.CHECK_FIC), "fic_sm": api.ConvPlan(ls, f, abi.CHECK_FIC),
+                      "ic": api.ConvPlan(ls, f, abi.CHECK_IC), "icbatch": api.ConvPlan(ls, f, abi.CHECK_ICBATCH)}
         # FIC with the input checksum dotted from the staged shared-memory tiles
         # instead of the default second read of the stored input (FR)
         L["plans"]["fic_sm"].set_input_checksum_source(abi.RHS_STAGED)
         L["packed"] = L["plans"]["unprotected"].pack(x)
-        for pl in L["plans"].values():
-            assert pl.info.packed_input_bytes == L["plans"]["unprotected"].info.packed_input_bytes
+        # ICBatch: the packed input also holds the batch-sum digit images (written in-kernel)
+        L["packed_icb"] = L["plans"]["icbatch"].pack(x)
+        for v, pl in L["plans"].items():
+            if v != "icbatch":
+                assert pl.info.packed_input_bytes == L["plans"]["unprotected"].info.packed_input_bytes
         L["ep"] = {kk: pl.epilog_params(0.05, bias, True) for kk, pl in L["plans"].items()}
         out_bytes = ls.n * k * (ls.p + 1) * (ls.q + 1) + (1 << 16)
         L["out"] = torch.zeros(out_bytes, dtype=torch.int8, device=dev)
         L["out2"] = torch.zeros(out_bytes, dtype=torch.int8, device=dev)
         layers.append(L)
     torch.cuda.synchronize()
-    counts = torch.zeros(4, dtype=torch.int64, device=dev)
-
-    # one verdict launch per pass: every layer's FC / FIC VerifyOutcome
-    sets = {v: api.PlanSet([L["plans"][v] for L in layers]) for v in ("fc", "fic", "fic_sm")}
+    # one verdict launch per pass: every layer's FC / FIC / IC / ICBatch VerifyOutcome
+    CHECKED = ("fc", "fic", "fic_sm", "ic", "icbatch")
+    VARIANTS = ("unprotected",) + CHECKED + ("dup",)
+    sets = {v: api.PlanSet([L["plans"][v] for L in layers]) for v in CHECKED}
+    # multi-GPU verdicts: each rank packs its shard's VerifyOutcomes into
+    # records, ONE all-gather per step moves them (NCCL over NVLink), and a one-block
+    # kernel folds them into the global outcomes (FC counts / first locus, FIC sums)
+    from paper_2006_04984_b200.dist import ShardedVerdicts
+    shards = {v: ShardedVerdicts(sets[v]._out, [abi.FC, abi.FIC, abi.IC if v == "ic" else abi.ICBATCH] * len(layers),
+                                 n_offset=rank * rb) for v in CHECKED}
 
     def step(variant):
         for L in layers:
@@ -736,19 +756,27 @@ def run_ours(args, world, rank, local):
                 # one launch per layer: conv + checks (+ the in-kernel input checksum);
                 # each CTA leaves its partial verdict record
                 pl = L["plans"][variant]
-                pl.run(L["packed"], L["out"], abi.OUT_I8_PACKED, ep=L["ep"][variant])
+                pl.run(L["packed_icb"] if variant == "icbatch" else L["packed"], L["out"], abi.OUT_I8_PACKED,
+                       ep=L["ep"][variant])
         if variant in sets:
             sets[variant].finalize()
+            shards[variant].record()
 
-    launches_per_step = {"unprotected": 16, "dup": 32, "fc": 17, "fic": 17, "fic_sm": 17}
+    # kernels of this library per step: conv per layer, + ICBatch scan per layer,
+    # + IC input-checksum pair per layer and IC verdict per layer, + one verdict
+    # launch (+ with several ranks the verdict-record kernel in the graph and the fold
+    # kernel after the all-gather)
+    xr = 2 if world > 1 else 0
+    launches_per_step = {"unprotected": 16, "dup": 32, "fc": 17 + xr, "fic": 17 + xr, "fic_sm": 17 + xr,
+                         "ic": 65 + xr, "icbatch": 33 + xr}
 
     # warm up eagerly (sets kernel attributes), then capture each variant as one graph
     with torch.cuda.stream(stream):
-        for v in ("unprotected", "fc", "fic", "fic_sm", "dup"):
+        for v in VARIANTS:
             step(v)
     torch.cuda.synchronize()
     graphs = {}
-    for v in ("unprotected", "fc", "fic", "fic_sm", "dup"):
+    for v in VARIANTS:
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=stream):
             step(v)
@@ -776,8 +804,8 @@ def run_ours(args, world, rank, local):
             flush.zero_()
             evs[i][0].record(cur)
             graphs[v].replay()
-            if dist:  # the only collective: error-count reduction over NVLink
-                dist.all_reduce(counts)
+            if v in shards:  # the only collective: the per-shard verdict records, then the fold
+                shards[v].reduce()
             evs[i][1].record(cur)
         torch.cuda.synchronize()
         if sampler:
@@ -793,7 +821,7 @@ def run_ours(args, world, rank, local):
     ops_step = total_ops(rb) * world
     res = {}
     sampler = ClockSampler(local)
-    for v in ("unprotected", "fc", "dup", "fic_sm", "fic"):
+    for v in ("unprotected", "fc", "dup", "fic_sm", "ic", "icbatch", "fic"):
         ms, clk = timed(v, args.steps, args.warmup, sampler if v == "fic" else None)
         res[v] = {"ms": ms, "tops": ops_step / (ms * 1e-3) / 1e12}
         if v == "fic":
@@ -811,8 +839,13 @@ def run_ours(args, world, rank, local):
     if not args.skip_mbv2:
         mbv2 = measure_mobilenetv2_int8(args, dev, stream, flush, world, dist)
 
-    # verdicts of the last FC / FIC passes (fault-free => all pass)
-    fails = sum(o.status for v in ("fic", "fic_sm", "fc") for oc in sets[v].outcomes() for o in oc[:2])
+    # global verdicts of the last pass of every checked variant, folded over the ranks
+    # (fault-free => all pass); slots are {FC, FIC, IC/ICBatch} per layer
+    fails = 0
+    for v in CHECKED:
+        glob = shards[v].outcomes_global()
+        want = {"fc": (0,), "fic": (1,), "fic_sm": (1,), "ic": (2,), "icbatch": (2,)}[v]
+        fails += sum(glob[3 * i + j].status for i in range(len(layers)) for j in want)
 
     # ------------------------------------------------ roofline of the dominant kernel
     # the FIC conv kernel of each layer (the whole per-layer FIC work: conv, checks,
@@ -845,8 +878,12 @@ def run_ours(args, world, rank, local):
     conv_ms = per_layer_ms("fic")
     unprot_ms = per_layer_ms("unprotected")
     conv_tops = total_ops(rb) / (sum(conv_ms) * 1e-3) / 1e12
+    # denominator: the tcgen05 kind::i8 dense peak MEASURED in this run on this device
+    # (all SMs issuing back-to-back M128 N256 K32 MMAs, CUDA events; abed_probe_mma_i8_peak)
+    pk_tops, pk_ms = C.c_double(), C.c_double()
+    abi.call("abed_probe_mma_i8_peak", 4000, C.byref(pk_tops), C.byref(pk_ms))
+    peak = pk_tops.value
     bf16 = peaks.get("bf16_tflops")
-    peak = 2.0 * bf16 if bf16 else 2.0 * 1590.0
     ncu = {}
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as fh:
@@ -858,9 +895,11 @@ def run_ours(args, world, rank, local):
                 "traffic_source": "profiles/ncu_summary.json: dram__bytes_read.sum + dram__bytes_write.sum of one "
                                   "launch of " + str(ncu.get("traffic_layer")) + " (ncu --set full)",
                 "kernel": "conv_i8_tc_kernel<int8, packed out, FIC> (conv + input-checksum warps + output sums + verdict)",
-                "peak_source": ("2 x MEASURED_PEAKS.json bf16_tflops (burst): tcgen05 kind::i8 issues K=32 at the "
-                                "kind::f16 K=16 rate (tools/mma_microbench.cu)" if bf16 else "2 x fallback bf16 1590"),
+                "peak_source": ("measured in this run: tcgen05.mma kind::i8 M128xN256xK32 back to back on all "
+                                f"{torch.cuda.get_device_properties(dev).multi_processor_count} SMs, operands in "
+                                f"shared memory, CUDA events ({pk_ms.value:.2f} ms; abed_probe_mma_i8_peak)"),
                 "frac_of_nominal_4500": round(conv_tops / PEAK_INT8_NOMINAL, 4),
+                "frac_of_2x_bf16_measured": round(conv_tops / (2.0 * bf16), 4) if bf16 else None,
                 "conv_share_of_step": round(sum(conv_ms) / res["fic"]["ms"], 3),
                 "per_layer_conv_us": [round(t * 1e3, 2) for t in conv_ms],
                 "per_layer_unprotected_us": [round(t * 1e3, 2) for t in unprot_ms],
@@ -988,11 +1027,11 @@ def run_ours(args, world, rank, local):
         "vs_baseline": None,
         "dtype": "int8",
         "data": "synthetic: SplitMix64 int8 activations/filters generated on device; bias linspace(-2,2), scale 0.05",
-        "config": {"workload": WORKLOAD if not args.global_batch else WORKLOAD.replace("-b32", f"-b{rb * world}"),
-                   "global_batch": rb * world, "per_gpu_batch": rb, "layers": 16,
-                   "scheme": "FIC-FR in one kernel per layer (input checksum x.G with dp4a from a second read of the stored input, by input-checksum warps or, where the conv grid leaves SMs free, input-checksum CTAs; epilogue output sums; per-CTA verdict records) + one verdict launch per pass for all 16 VerifyOutcomes",
-                   "parallelism": f"dp{world} (batch shards, NCCL error-count all-reduce)",
-                   "l2": "flushed (512 MiB memset) before every timed step", "timing": "CUDA graph replay, CUDA events"},
+        "config": workload_config(rb, world, args.global_batch),
+        "method": {"scheme": "FIC-FR in one kernel per layer (input checksum x.G with dp4a from a second read of the stored input, by input-checksum warps or, where the conv grid leaves SMs free, input-checksum CTAs; epilogue output sums; per-CTA verdict records) + one verdict launch per pass for all 16 VerifyOutcomes",
+                   "parallelism": f"dp{world} (batch shards; one NCCL all-gather of the per-shard verdict records "
+                                  "per step, folded on the device)",
+                   "timing": "CUDA graph replay, CUDA events"},
         "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": e2e,
@@ -1002,6 +1041,8 @@ def run_ours(args, world, rank, local):
         "overhead_pct": {"fic_vs_unprotected": round(100 * (res["fic"]["ms"] / res["unprotected"]["ms"] - 1), 2),
                          "fic_sm_vs_unprotected": round(100 * (res["fic_sm"]["ms"] / res["unprotected"]["ms"] - 1), 2),
                          "fc_vs_unprotected": round(100 * (res["fc"]["ms"] / res["unprotected"]["ms"] - 1), 2),
+                         "ic_vs_unprotected": round(100 * (res["ic"]["ms"] / res["unprotected"]["ms"] - 1), 2),
+                         "icbatch_vs_unprotected": round(100 * (res["icbatch"]["ms"] / res["unprotected"]["ms"] - 1), 2),
                          "duplication_vs_unprotected": round(100 * (res["dup"]["ms"] / res["unprotected"]["ms"] - 1), 2),
                          "fic_throughput_vs_duplication": round(res["dup"]["ms"] / res["fic"]["ms"], 3)},
         "detection": {"layer": "cfg1 1x64x56x56 K=64 3x3 p1, ones data, scale 0.05, trials %d" % trials, **det},

@@ -352,10 +352,36 @@ int abed_abft_plan_destroy(abed_abft_plan* plan);
 int abed_abft_plan_run(abed_abft_plan* plan, const int8_t* a, const int8_t* b, int32_t* c, int64_t* c_aug,
                        abed_verify_outcome* outcomes_dev, int32_t mode, void* stream);
 
+/* ------------------------------------------------------------ multi-GPU verdicts
+ * The batch is sharded across ranks; each rank verifies its shard
+ * and the per-shard VerifyOutcomes are folded into the global ones with one small
+ * collective: abed_verdict_records writes 8 int64 per outcome slot
+ * {status, has_locus, locus[3], lhs, rhs, error_count} (FC locus n made global by
+ * n_offset, the rank's first image), the ranks' records are all-gathered
+ * (world x n x 64 bytes; rank order = batch order), and abed_verdict_combine folds
+ * them.  kinds[i] = scheme of slot i (ABED_FC, ABED_IC, ABED_ICBATCH, ABED_FIC):
+ *   FC: counts add, first mismatch of the lowest failing rank (reference (n,p,q) order)
+ *   FIC: lhs and rhs add (both linear in the batch), status = lhs != rhs
+ *   IC / ICBATCH: per-shard checks: status = any, counts add, lowest failing rank's locus
+ * n <= 256.  Device versions are stream-ordered; the _host versions run the same
+ * fold on host memory (no device needed). */
+int abed_verdict_records(const abed_verify_outcome* outcomes_dev, int32_t n, const int32_t* kinds_host,
+                         int64_t n_offset, int64_t* records_dev, void* stream);
+int abed_verdict_combine(const int64_t* gathered_dev, int32_t world, int32_t n, const int32_t* kinds_host,
+                         abed_verify_outcome* out_dev, void* stream);
+int abed_verdict_records_host(const abed_verify_outcome* outcomes, int32_t n, const int32_t* kinds,
+                              int64_t n_offset, int64_t* records);
+int abed_verdict_combine_host(const int64_t* gathered, int32_t world, int32_t n, const int32_t* kinds,
+                              abed_verify_outcome* out);
+
 /* diagnostics (no reference counterpart): record a per-CTA clock timeline of the
  * conv kernel into trace_dev (16 int64 per CTA, caller-zeroed); NULL disables.
  * flags bit 0 makes the epilogue skip its work (timing experiments only). */
 int abed_debug_set_conv_trace(abed_conv_plan* plan, int64_t* trace_dev, int32_t flags);
+/* measured tcgen05 kind::i8 dense peak of this device (the int8 roofline
+ * denominator): one CTA per SM issuing `iters` x 8 back-to-back M128 N256 K32
+ * MMAs, timed with CUDA events (synchronous).  tops = 2 * MACs / time. */
+int abed_probe_mma_i8_peak(int32_t iters, double* tops, double* ms);
 
 #ifdef __cplusplus
 }

@@ -187,6 +187,11 @@ SIGNATURES = {
     "abed_conv_plan_set_af_input": (C.c_int, [P, i32]),
     "abed_conv_plan_set_reuse_input_checksum": (C.c_int, [P, i32]),
     "abed_conv_plan_set_input_checksum_source": (C.c_int, [P, i32]),
+    "abed_probe_mma_i8_peak": (C.c_int, [i32, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "abed_verdict_records": (C.c_int, [P, i32, P, i64, P, P]),
+    "abed_verdict_combine": (C.c_int, [P, i32, i32, P, P, P]),
+    "abed_verdict_records_host": (C.c_int, [P, i32, P, i64, P]),
+    "abed_verdict_combine_host": (C.c_int, [P, i32, i32, P, P]),
 }
 
 _lib = None

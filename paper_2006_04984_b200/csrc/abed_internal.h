@@ -69,8 +69,13 @@ __global__ void fc_finalize_part2_kernel(const int64_t* part, abed_dev::ActGeom 
                                          const unsigned long long* scratch, abed_verify_outcome* out);
 __global__ void fic_finalize_kernel(const int64_t* part, int n, const unsigned long long* rhs_p,
                                     abed_verify_outcome* out);
-__global__ void ic_finalize_kernel(const unsigned long long* ksum, const int8_t* f, const int32_t* ic, int64_t K,
-                                   int64_t crs, abed_verify_outcome* out);
+// IC: ic[c,r,s] (and FIC's rhs when fic_rhs != nullptr) from the in-kernel class sums
+void ic_from_classes_launch(const int64_t* S, const uint64_t* rowmask, const uint64_t* colmask,
+                            const abed_dev::ActGeom& g, int nrc, int ncc, const int32_t* fsum, int32_t* ic,
+                            unsigned long long* fic_rhs, cudaStream_t st);
+// ic_verify_k verdict: scr = plan-owned {count, first k (init ~0), ticket, -, dot[K]}
+void ic_finalize_launch(const unsigned long long* ksum, const int8_t* f, const int32_t* ic, int64_t K, int64_t crs,
+                        unsigned long long* scr, abed_verify_outcome* out, cudaStream_t st);
 
 // conv_tc.cu
 uint32_t conv_tc_smem_bytes(const abed_dev::ConvTcParams& p);
@@ -150,6 +155,14 @@ struct abed_conv_plan {
   unsigned long long* d_kacc = nullptr;  // kernel accumulators {FIC lhs, FIC rhs, done ticket, -}
   abed_verify_outcome* d_outcome = nullptr;  // {FC, FIC, IC} verdicts written by the conv kernel
   unsigned long long* d_acc = nullptr;  // [0]=fic rhs, [1]=cmp count, [2..3]=fc scratch, [4..4+K) ic sums
+  unsigned long long* d_ic_scr = nullptr;  // IC verdict scratch {count, first k, ticket, -, dot[K]}
+  // IC input checksum in-kernel: class sums [n_phase][nrc][ncc][c16*16] (int64),
+  // row / column classes [nph_h][Hl] / [nph_w][Wl], filter-row / -column masks per class
+  int64_t* d_ic_S = nullptr;
+  uint8_t* d_ic_cls = nullptr;
+  uint64_t* d_ic_mask = nullptr;
+  int ic_nrc = 0, ic_ncc = 0;
+  size_t ic_S_bytes = 0;
   float* d_zero_bias = nullptr;
   // when set, runs skip the input-checksum kernels and keep d_ic / the FIC
   // right-hand side of an earlier run (fault campaigns: checksums come from

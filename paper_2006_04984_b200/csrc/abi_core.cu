@@ -76,14 +76,18 @@ void plan_init_common(abed_conv_plan* pl, const abed_layer_shape& shape, int che
   std::memset(&p, 0, sizeof(p));
   // int8 FIC: shared memory for the staged input checksum's class table
   const uint32_t fic_smem = (cpg == 16 && (checks & ABED_CHECK_FIC)) ? fic_classes_host(pl) : 0u;
-  bool tiled = choose_tiling(g, (checks & ABED_CHECK_FC) != 0, force_bn, p, fic_smem);
+  // IC: per-CTA shared per-channel output sums (K int64)
+  const uint32_t ic_smem = (checks & ABED_CHECK_IC) ? (uint32_t)((shape.k * 8 + 15) & ~15) : 0u;
+  const uint32_t ic_res = ic_smem ? ic_smem + 16 : 0u;  // + alignment
+  bool tiled = choose_tiling(g, (checks & ABED_CHECK_FC) != 0, force_bn, p, fic_smem + ic_res);
   if (tiled && fic_smem) {
     p.fic_smem = fic_smem;
     p.fic_tab_bytes = (uint32_t)(pl->h_rep.size() * g.c16 * 48);
   } else if (fic_smem) {
     pl->h_rep.clear();  // no room: FIC keeps the FR re-read
-    tiled = choose_tiling(g, (checks & ABED_CHECK_FC) != 0, force_bn, p);
+    tiled = choose_tiling(g, (checks & ABED_CHECK_FC) != 0, force_bn, p, ic_res);
   }
+  if (tiled && ic_smem) p.ic_smem = ic_smem;
   if (!tiled) throw_invalid("conv: no tiling fits shared memory for this layer");
   p.plane_len = g.plane_len;
   p.n_phase = g.n_phase;
@@ -123,6 +127,11 @@ void plan_init_common(abed_conv_plan* pl, const abed_layer_shape& shape, int che
   cuda_check(cudaMemset(pl->d_zero_bias, 0, shape.k * 4), "memset bias");
   cuda_check(cudaMalloc(&pl->d_af_acc, 8), "cudaMalloc(af_acc)");
   cuda_check(cudaMemset(pl->d_af_acc, 0, 8), "memset af_acc");
+  if (checks & ABED_CHECK_IC) {
+    cuda_check(cudaMalloc(&pl->d_ic_scr, (4 + shape.k) * 8), "cudaMalloc(ic_scr)");
+    const unsigned long long init[4] = {0ull, ~0ull, 0ull, 0ull};
+    cuda_check(cudaMemcpy(pl->d_ic_scr, init, sizeof(init), cudaMemcpyHostToDevice), "ic_scr init");
+  }
   if (n_extra) {
     const size_t kpq = (size_t)shape.k * shape.p * shape.q;
     cuda_check(cudaMalloc(&pl->d_icb_lhs, kpq * 8), "cudaMalloc(icb_lhs)");
@@ -134,6 +143,66 @@ void plan_init_common(abed_conv_plan* pl, const abed_layer_shape& shape, int che
     cuda_check(cudaMalloc(&pl->d_icb_out, sizeof(abed_verify_outcome)), "cudaMalloc(icb_out)");
     cuda_check(cudaMemset(pl->d_icb_out, 0, sizeof(abed_verify_outcome)), "memset icb_out");
   }
+}
+
+// Position classes of a plane axis: phase row i is reached by the filter rows
+// {r : r % st == a, 0 <= i - r / st < P}; rows with equal sets share a class.
+// cls[a * L + i] = class id, masks[a * ncls + id] = its filter-row bit mask.
+static void axis_classes(int L, int R, int st, int P, int nph, std::vector<uint8_t>& cls, std::vector<uint64_t>& masks,
+                         int& ncls) {
+  cls.assign((size_t)nph * L, 0);
+  std::vector<std::vector<uint64_t>> m(nph);
+  for (int a = 0; a < nph; ++a)
+    for (int i = 0; i < L; ++i) {
+      uint64_t b = 0;
+      for (int r = 0; r < R; ++r)
+        if (r % st == a && i - r / st >= 0 && i - r / st < P) b |= uint64_t(1) << r;
+      int id = -1;
+      for (size_t k = 0; k < m[a].size(); ++k)
+        if (m[a][k] == b) id = (int)k;
+      if (id < 0) {
+        id = (int)m[a].size();
+        m[a].push_back(b);
+      }
+      cls[(size_t)a * L + i] = (uint8_t)std::min(id, 255);
+    }
+  ncls = 0;
+  for (int a = 0; a < nph; ++a) ncls = std::max(ncls, (int)m[a].size());
+  masks.assign((size_t)nph * ncls, 0);
+  for (int a = 0; a < nph; ++a)
+    for (size_t k = 0; k < m[a].size(); ++k) masks[(size_t)a * ncls + k] = m[a][k];
+}
+
+// IC input checksum in-kernel: classes, masks and the class-sum buffer
+static void build_ic_classes(abed_conv_plan* pl) {
+  const ActGeom& g = pl->g;
+  std::vector<uint8_t> rc, cc;
+  std::vector<uint64_t> rm, cm;
+  axis_classes(g.Hl, g.r, g.sh, g.p, g.nph_h, rc, rm, pl->ic_nrc);
+  axis_classes(g.Wl, g.s, g.sw, g.q, g.nph_w, cc, cm, pl->ic_ncc);
+  if (pl->ic_nrc > 255 || pl->ic_ncc > 255 || g.r > 64 || g.s > 64) throw_invalid("IC: too many position classes");
+  cuda_check(cudaMalloc(&pl->d_ic_cls, rc.size() + cc.size()), "cudaMalloc(ic_cls)");
+  cuda_check(cudaMemcpy(pl->d_ic_cls, rc.data(), rc.size(), cudaMemcpyHostToDevice), "ic_cls h2d");
+  cuda_check(cudaMemcpy(pl->d_ic_cls + rc.size(), cc.data(), cc.size(), cudaMemcpyHostToDevice), "ic_cls h2d");
+  cuda_check(cudaMalloc(&pl->d_ic_mask, (rm.size() + cm.size()) * 8), "cudaMalloc(ic_mask)");
+  cuda_check(cudaMemcpy(pl->d_ic_mask, rm.data(), rm.size() * 8, cudaMemcpyHostToDevice), "ic_mask h2d");
+  cuda_check(cudaMemcpy(pl->d_ic_mask + rm.size(), cm.data(), cm.size() * 8, cudaMemcpyHostToDevice), "ic_mask h2d");
+  pl->ic_S_bytes = (size_t)g.n_phase * pl->ic_nrc * pl->ic_ncc * g.c16 * 16 * 8;
+  cuda_check(cudaMalloc(&pl->d_ic_S, pl->ic_S_bytes), "cudaMalloc(ic_S)");
+  cuda_check(cudaMemset(pl->d_ic_S, 0, pl->ic_S_bytes), "memset ic_S");
+}
+
+// IC verdict chain: ic (+ FIC rhs) from the class sums, then ic_verify_k
+static void ic_verdict(abed_conv_plan* pl, abed_verify_outcome* out, cudaStream_t st) {
+  const ActGeom& g = pl->g;
+  if (pl->d_ic_S) {
+    const bool fic = (pl->checks & ABED_CHECK_FIC) != 0;
+    if (fic) cuda_check(cudaMemsetAsync(pl->d_acc, 0, 8, st), "memset rhs");
+    ic_from_classes_launch(pl->d_ic_S, pl->d_ic_mask, pl->d_ic_mask + (size_t)g.nph_h * pl->ic_nrc, g, pl->ic_nrc,
+                           pl->ic_ncc, fic ? pl->d_fsum : nullptr, pl->d_ic, fic ? pl->d_acc : nullptr, st);
+  }
+  ic_finalize_launch(pl->d_acc + 4, pl->d_filters, pl->d_ic, pl->shape.k, pl->shape.c * pl->shape.r * pl->shape.s,
+                     pl->d_ic_scr, out, st);
 }
 
 // FIC-SM class table.  A phase row i is reached by the filter rows
@@ -265,6 +334,7 @@ abed_conv_plan* plan_create(const abed_layer_shape& shape, const int8_t* filters
       cuda_check(cudaGetLastError(), "fic_weight");
       if (pl->ficw8_ok && !pl->h_rep.empty()) build_fic_classes(pl);
     }
+    if (checks & ABED_CHECK_IC) build_ic_classes(pl);
     cuda_check(cudaDeviceSynchronize(), "plan_create sync");
   } catch (...) {
     abed_conv_plan_destroy(pl);
@@ -385,13 +455,16 @@ void plan_run(abed_conv_plan* pl, const int8_t* packed, const abed_epilog_params
     // input checksum of the pristine input (FR option)
     const ActGeom& g = pl->g;
     if (pl->checks & ABED_CHECK_IC) {
-      // per-tap input checksum needed (IC): batch sum, then window sums + FIC dot,
-      // ahead of the convolution
-      cuda_check(cudaMemsetAsync(pl->d_acc, 0, 8, st), "memset rhs");
-      const int64_t cnt = (int64_t)g.n_phase * g.c16 * g.Hl * g.Wl;
-      batch_sum_packed_kernel<<<grid_for(cnt), 256, 0, st>>>(packed, g, pl->d_bsum);
-      box_sum_dot_kernel<<<g.c, 256, 0, st>>>(pl->d_bsum, g, pl->d_fsum, pl->d_ic, pl->d_acc);
-      cuda_check(cudaGetLastError(), "input checksum");
+      // IC (and FIC's rhs, derived from ic at the verdict): the input checksum's
+      // class sums accumulated in-kernel by the input-checksum warps / CTAs
+      cuda_check(cudaMemsetAsync(pl->d_ic_S, 0, pl->ic_S_bytes, st), "memset ic_S");
+      p.rhs_mode = 4;
+      p.ic_S = pl->d_ic_S;
+      p.ic_rowcls = pl->d_ic_cls;
+      p.ic_colcls = pl->d_ic_cls + (size_t)g.nph_h * g.Hl;
+      p.ic_nrc = pl->ic_nrc;
+      p.ic_ncc = pl->ic_ncc;
+      p.rhs_nsplit = fr_split(g);
     } else {
       const int64_t cells = (int64_t)g.n_phase * g.c16 * g.Hl * g.Wl;
       if (pl->ficw8_ok && pl->d_ficc8 && pl->rhs_src == ABED_RHS_STAGED && g.n_phase <= 4) {
@@ -462,14 +535,13 @@ abed_dev::VerdictJob plan_verdict_job(const abed_conv_plan* pl, abed_verify_outc
 }
 
 void plan_finalize(abed_conv_plan* pl, abed_verify_outcome* out_dev, cudaStream_t st) {
+  // IC first: with FIC its input checksum also gives FIC's rhs
+  if (pl->checks & ABED_CHECK_IC) ic_verdict(pl, out_dev + 2, st);
   // FC / FIC: reduce the conv kernel's per-CTA records into VerifyOutcomes
   if (pl->checks & (ABED_CHECK_FC | ABED_CHECK_FIC | ABED_CHECK_ICBATCH)) {
     const abed_dev::VerdictJob j = plan_verdict_job(pl, out_dev);
     cuda_check(verdict_launch(&j, 1, st), "verdict");
   }
-  if (pl->checks & ABED_CHECK_IC)
-    ic_finalize_kernel<<<1, 256, 0, st>>>(pl->d_acc + 4, pl->d_filters, pl->d_ic, pl->shape.k,
-                                          pl->shape.c * pl->shape.r * pl->shape.s, out_dev + 2);
   cuda_check(cudaGetLastError(), "finalize");
 }
 
@@ -529,7 +601,7 @@ int abed_conv_plan_destroy(abed_conv_plan* pl) {
   cudaFree(pl->d_af_acc); cudaFree(pl->d_ficc8);  // row / column classes live inside it
   cudaFree(pl->d_acc); cudaFree(pl->d_zero_bias);
   cudaFree(pl->d_icb_lhs); cudaFree(pl->d_icb_dig); cudaFree(pl->d_icb_ctl); cudaFree(pl->d_icb_rec);
-  cudaFree(pl->d_icb_out);
+  cudaFree(pl->d_icb_out); cudaFree(pl->d_ic_scr); cudaFree(pl->d_ic_S); cudaFree(pl->d_ic_cls); cudaFree(pl->d_ic_mask);
   delete pl;
   return ABED_OK;
 }
@@ -579,10 +651,7 @@ int abed_conv_plan_finalize_many(abed_conv_plan* const* plans, int32_t n, abed_v
       abed_conv_plan* pl = plans[i];
       if (pl->checks & (ABED_CHECK_FC | ABED_CHECK_FIC | ABED_CHECK_ICBATCH))
         jobs.push_back(plan_verdict_job(pl, outcomes_dev + 3 * i));
-      if (pl->checks & ABED_CHECK_IC)
-        ic_finalize_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(pl->d_acc + 4, pl->d_filters, pl->d_ic, pl->shape.k,
-                                                               pl->shape.c * pl->shape.r * pl->shape.s,
-                                                               outcomes_dev + 3 * i + 2);
+      if (pl->checks & ABED_CHECK_IC) ic_verdict(pl, outcomes_dev + 3 * i + 2, (cudaStream_t)stream);
     }
     cuda_check(verdict_launch(jobs.data(), (int)jobs.size(), (cudaStream_t)stream), "verdict");
   });

@@ -115,7 +115,9 @@ struct ConvTcParams {
   unsigned long long* rhs_ext;  // FIC rhs of the pristine input: read (rhs_mode 0) or stored (rhs_mode 1)
   int rhs_mode;                // 1: input-checksum warps compute the FIC rhs in this kernel (FR re-read),
                                // 2: AF -- the previous layer's epilogue produced it (af accumulator),
-                               // 3: SM -- input-checksum warps read the staged A tiles (no re-read)
+                               // 3: SM -- input-checksum warps read the staged A tiles (no re-read),
+                               // 4: IC -- they accumulate the class sums of the input checksum
+                               //    (ic_S; FIC's rhs then comes from ic at the verdict)
   int rhs_nsplit;              // image split of the rhs work items
   int rhs_deep;                // int8 FR: 16 image loads in flight per item (large inputs) instead of 8
   unsigned fc_epoch;           // FC, several N tiles: value a CTA writes into its M tile's flag
@@ -136,6 +138,7 @@ struct ConvTcParams {
   int nrc, ncc;
   uint32_t fic_smem;           // bytes of the kernel's smem copy of {ficc8, rowcls, colcls} (0: none)
   uint32_t fic_tab_bytes;      // ficc8 part of it
+  uint32_t ic_smem;            // IC: bytes of the CTA's per-channel output-sum accumulators (K int64; 0: off)
   void* outcome;               // abed_verify_outcome[3] {FC, FIC, IC}: FC and FIC written here
   // FIC-AF (fused_conv_epilog's next-layer input checksum tap, checksum.hpp:605-631,
   // cost_model "AF"): the epilogue accumulates the NEXT layer's FIC rhs
@@ -153,6 +156,13 @@ struct ConvTcParams {
   // only after every writer warp has signalled icb_ready.  The epilogue adds each
   // real output into icb_lhs[k][p][q] (int64 reduction) and stores the digit
   // rows' conv into icb_dig[j][k][p][q]; icb_scan_kernel compares afterwards.
+  // IC input checksum in-kernel (rhs_mode 4): the FR pass adds each plane pixel's
+  // batch sum into ic_S[phase][row class][column class][channel]; the verdict
+  // turns the class sums into gen_input_checksum's ic[c,r,s] (checksum.hpp:248-266)
+  int64_t* ic_S;
+  const uint8_t* ic_rowcls;         // [nph_h][Hl] row class
+  const uint8_t* ic_colcls;         // [nph_w][Wl] column class
+  int ic_nrc, ic_ncc;
   int icb_d;                        // digit images (0 = ICBatch off)
   int64_t m_real;                   // N * Hl * Wl: GEMM rows of the real images
   unsigned long long* icb_lhs;      // [K*P*Q] sum_n ConvOut (reset by the scan)

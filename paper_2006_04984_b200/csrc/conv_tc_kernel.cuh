@@ -57,7 +57,7 @@ constexpr int64_t kNoKey = 0x7fffffffffffffffll;
 enum EpiKind : int { EPI_NONE = 0, EPI_NCHW = 1, EPI_PACKED = 2, EPI_COMPARE = 3 };
 
 struct SmemLayout {
-  uint32_t a_off, a_stage_bytes, b_off, bar_off, tab_off, fic_off, total;
+  uint32_t a_off, a_stage_bytes, b_off, bar_off, tab_off, fic_off, ic_off, total;
 };
 
 __host__ __device__ inline SmemLayout smem_layout(const ConvTcParams& p) {
@@ -76,6 +76,9 @@ __host__ __device__ inline SmemLayout smem_layout(const ConvTcParams& p) {
   off = (off + 15u) & ~15u;
   L.fic_off = off;  // FIC-SM class table + row / column classes, then its mbarrier
   off += p.fic_smem ? p.fic_smem + 16u : 0u;
+  off = (off + 15u) & ~15u;
+  L.ic_off = off;  // IC per-channel output sums of this CTA (flushed once at exit)
+  off += p.ic_smem;
   L.total = off;
   return L;
 }
@@ -237,14 +240,65 @@ struct EpiCtx {
   bool chunk32, valid, fault_row;
   const uint4* af_row;     // FIC-AF: next layer's digit cell of this pixel, group 0 (nullptr: off)
   int64_t af_gstride;      // uint4 stride between channel groups of the digit planes
+  unsigned long long* ic_acc;   // IC: the CTA's shared per-channel sums (nullptr: straight to global)
   unsigned long long* icb_lhs;  // ICBatch, real row: &icb_lhs[0][p][q] (nullptr: not a real row)
   int32_t* icb_dig;             // ICBatch, digit row j: &icb_dig[j][0][p][q] (nullptr: not a digit row)
 };
 
-// One 16-channel chunk of one row: (slow path only: fault hook, filler trim,
-// IC sums), row sum, requantise + store (or compare).  Returns the chunk's
+// IC (ic_verify_k's lhs, checksum.hpp:319-347): per-channel sums of one chunk
+// over the warp's 32 rows by a transpose-reduce butterfly -- xor 16 / 8 / 4 / 2
+// halve the channels each lane carries (int32: 16 rows of |acc| < 2^27), xor 1
+// adds the two 16-row halves in int64 -- 17 shuffles per 16 channels instead of
+// 16 separate 64-bit warp reductions; each even lane then owns one channel's sum
+// and adds it into the CTA's shared accumulator (flushed to global once per CTA:
+// per-warp global reductions on the same K addresses serialised in L2).
+__device__ __forceinline__ void ic_chunk_sums(const ConvTcParams& p, unsigned long long* ic_acc, bool valid,
+                                              const int32_t (&a)[16], int k0) {
+  const int lane = threadIdx.x & 31;
+  int32_t v[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) v[j] = valid ? a[j] : 0;
+  int32_t w8[8], w4[4], w2[2];
+  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) w8[j] = (b4 ? v[j + 8] : v[j]) + __shfl_xor_sync(0xffffffffu, b4 ? v[j] : v[j + 8], 16);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) w4[j] = (b3 ? w8[j + 4] : w8[j]) + __shfl_xor_sync(0xffffffffu, b3 ? w8[j] : w8[j + 4], 8);
+#pragma unroll
+  for (int j = 0; j < 2; ++j) w2[j] = (b2 ? w4[j + 2] : w4[j]) + __shfl_xor_sync(0xffffffffu, b2 ? w4[j] : w4[j + 2], 4);
+  const int32_t w1 = (b1 ? w2[1] : w2[0]) + __shfl_xor_sync(0xffffffffu, b1 ? w2[0] : w2[1], 2);
+  const long long sum = static_cast<long long>(w1) + __shfl_xor_sync(0xffffffffu, static_cast<long long>(w1), 1);
+  const int ch = (b4 ? 8 : 0) + (b3 ? 4 : 0) + (b2 ? 2 : 0) + (b1 ? 1 : 0);
+  if (!(lane & 1) && k0 + ch < p.K && sum != 0) {
+    if (ic_acc)
+      atomicAdd(ic_acc + k0 + ch, static_cast<unsigned long long>(sum));
+    else
+      red_add_u64(&p.ic_sum[k0 + ch], static_cast<unsigned long long>(sum));
+  }
+}
+
+// ICBatch (checksum.hpp:398-421): a real row adds its 16 outputs into the
+// per-(k, p, q) batch sums; a row of digit image j stores conv(d_j) for the scan
+template <bool TRIM>
+__device__ __forceinline__ void icb_chunk(const ConvTcParams& p, const EpiCtx& e, const int32_t (&a)[16], int k0) {
+  if (e.icb_lhs) {
+    unsigned long long* q = e.icb_lhs + static_cast<int64_t>(k0) * e.PQ;
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (!TRIM || k0 + j < p.K) red_add_u64(q + j * e.PQ, static_cast<unsigned long long>(static_cast<long long>(a[j])));
+  } else if (e.icb_dig) {
+    int32_t* q = e.icb_dig + static_cast<int64_t>(k0) * e.PQ;
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (!TRIM || k0 + j < p.K) q[j * e.PQ] = a[j];
+  }
+}
+
+// One 16-channel chunk of one row: (slow path only: fault hook, filler trim),
+// row sum, IC / ICBatch extras (XTRA 1 / 2 on the fast path; by plan on the slow
+// path), requantise + store (or compare).  Returns the chunk's
 // contribution to the row sum.  b = the chunk's 16 biases.
-template <int EPI, bool RELU, bool SUMS, bool SLOW, bool C32 = false>
+template <int EPI, bool RELU, bool SUMS, bool SLOW, bool C32 = false, int XTRA = 0>
 __device__ __forceinline__ int64_t epi_chunk(const ConvTcParams& p, const EpiCtx& e, int32_t (&a)[16],
                                              const float (&b)[16], int k0, long long& af_out) {
   if (SLOW) {
@@ -272,31 +326,8 @@ __device__ __forceinline__ int64_t epi_chunk(const ConvTcParams& p, const EpiCtx
       for (int j = 0; j < 16; ++j) sum += a[j];
     }
   }
-  if (SLOW && (p.check & CHECK_IC)) {
-    // IC scheme: per-channel column sums over the warp's 32 rows, one atomic per
-    // channel (ic_verify_k's lhs, checksum.hpp:319-347)
-    const int lane = threadIdx.x & 31;
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const long long s = warp_sum(e.valid ? a[j] : 0);
-      if (lane == j && k0 + j < p.K && s != 0) atomicAdd(&p.ic_sum[k0 + j], static_cast<unsigned long long>(s));
-    }
-  }
-  if (SLOW && p.icb_d) {
-    // ICBatch (checksum.hpp:398-421): real rows add their outputs into the
-    // per-(k, p, q) batch sums; rows of digit image j keep conv(d_j) for the scan
-    if (e.icb_lhs) {
-#pragma unroll
-      for (int j = 0; j < 16; ++j)
-        if (k0 + j < p.K)
-          red_add_u64(e.icb_lhs + static_cast<int64_t>(k0 + j) * e.PQ,
-                      static_cast<unsigned long long>(static_cast<long long>(a[j])));
-    } else if (e.icb_dig) {
-#pragma unroll
-      for (int j = 0; j < 16; ++j)
-        if (k0 + j < p.K) e.icb_dig[static_cast<int64_t>(k0 + j) * e.PQ] = a[j];
-    }
-  }
+  if (XTRA == 1 || (SLOW && (p.check & CHECK_IC))) ic_chunk_sums(p, e.ic_acc, e.valid, a, k0);
+  if (XTRA == 2 || (SLOW && p.icb_d)) icb_chunk<SLOW>(p, e, a, k0);
   if (EPI == EPI_PACKED || EPI == EPI_COMPARE) {
     int32_t y[16];
     if (p.dbg & 16) {  // timing experiment: skip the requantise math
@@ -463,7 +494,7 @@ __device__ __forceinline__ void load_bias16(const ConvTcParams& p, const EpiCtx&
 // processed) and the biases are read before the wait.  The loop body is not
 // unrolled across steps, so the epilogue stays resident in the instruction cache.
 // An odd trailing chunk is loaded as a 16-column step.
-template <int DT, int EPI, bool RELU, bool SUMS, bool SLOW, bool C32 = false>
+template <int DT, int EPI, bool RELU, bool SUMS, bool SLOW, bool C32 = false, int XTRA = 0>
 __device__ __forceinline__ std::conditional_t<DT == DT_I8, int64_t, double> epi_columns(
     const ConvTcParams& p, const EpiCtx& e, uint32_t t_row, int k_base, int c_lo, int c_hi, long long& af_out) {
   std::conditional_t<DT == DT_I8, int64_t, double> row_sum = 0;
@@ -472,7 +503,7 @@ __device__ __forceinline__ std::conditional_t<DT == DT_I8, int64_t, double> epi_
       int32_t a[16];
 #pragma unroll
       for (int j = 0; j < 16; ++j) a[j] = static_cast<int32_t>(v[j]);
-      row_sum += epi_chunk<EPI, RELU, SUMS, SLOW, C32>(p, e, a, b, k0, af_out);
+      row_sum += epi_chunk<EPI, RELU, SUMS, SLOW, C32, XTRA>(p, e, a, b, k0, af_out);
     } else {
       row_sum += epi_chunk_h<DT, EPI, RELU, SUMS, SLOW>(p, e, v, b, k0);
     }
@@ -855,6 +886,104 @@ __device__ __forceinline__ void icb_write_digits(const ConvTcParams& p, int64_t 
   if ((threadIdx.x & 31) == 0) red_release_gpu_add(p.icb_ready, 1u);
 }
 
+// IC input checksum, FR option (rhs_mode 4): items first, first + stride, ... of
+// (plane, pixel, image split); per item the 16 channel bytes summed over the
+// split's images (biased bytes in 16-bit lanes, flushed every 128 images), added
+// into the class sums ic_S[phase][row class][column class][channel] (integer
+// reductions: deterministic).  A plane pixel's position class fixes which taps
+// (r, s) it feeds, so gen_input_checksum's ic[c,r,s] (checksum.hpp:248-266) is a
+// sum of class sums (ic_from_classes_kernel, at the verdict).
+__device__ __forceinline__ void ic_class_sums_fr(const ConvTcParams& p, int64_t first, int64_t stride) {
+  const int64_t HlWl = static_cast<int64_t>(p.Hl) * p.Wl;
+  const int nsplit = p.rhs_nsplit;
+  const int64_t total = static_cast<int64_t>(p.n_phase) * p.c16 * HlWl * nsplit;
+  const int c256 = p.c16 * 16;
+  // warp-uniform loop (the aggregation below shuffles): lanes past the end idle
+  for (int64_t base = first - (threadIdx.x & 31); base < total; base += stride) {
+    const int64_t idx = base + (threadIdx.x & 31);
+    const bool ok = idx < total;
+    const int64_t it = ok ? idx : 0;
+    const int64_t pix = it % HlWl;
+    const int64_t rest = it / HlWl;
+    const int split = static_cast<int>(rest % nsplit);
+    const int64_t plane = rest / nsplit;
+    const int phase = static_cast<int>(plane / p.c16), grp = static_cast<int>(plane % p.c16);
+    const int i = static_cast<int>(pix / p.Wl), j = static_cast<int>(pix % p.Wl);
+    const int a = phase / p.nph_w, b = phase - (phase / p.nph_w) * p.nph_w;
+    const int cell = (phase * p.ic_nrc + p.ic_rowcls[a * p.Hl + i]) * p.ic_ncc + p.ic_colcls[b * p.Wl + j];
+    const uint4* src = reinterpret_cast<const uint4*>(p.act) + plane * p.plane_len + pix;
+    const int n0 = ok ? static_cast<int>(static_cast<int64_t>(p.N) * split / nsplit) : 0;
+    const int n1 = ok ? static_cast<int>(static_cast<int64_t>(p.N) * (split + 1) / nsplit) : 0;
+    int32_t s[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) s[e] = 0;
+    for (int m0 = n0; m0 < n1; m0 += 128) {
+      const int m1 = m0 + 128 < n1 ? m0 + 128 : n1;
+      uint32_t lo[4] = {0u, 0u, 0u, 0u}, hi[4] = {0u, 0u, 0u, 0u};
+      for (int n = m0; n < m1; n += 8) {
+        uint4 x[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          x[q] = n + q < m1 ? __ldcg(src + static_cast<int64_t>(n + q) * HlWl)
+                            : make_uint4(0x80808080u, 0x80808080u, 0x80808080u, 0x80808080u);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const uint32_t w[4] = {x[q].x ^ 0x80808080u, x[q].y ^ 0x80808080u, x[q].z ^ 0x80808080u,
+                                 x[q].w ^ 0x80808080u};
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            lo[u] += w[u] & 0x00FF00FFu;
+            hi[u] += (w[u] >> 8) & 0x00FF00FFu;
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        s[4 * u + 0] += static_cast<int32_t>(lo[u] & 0xFFFFu);
+        s[4 * u + 2] += static_cast<int32_t>(lo[u] >> 16);
+        s[4 * u + 1] += static_cast<int32_t>(hi[u] & 0xFFFFu);
+        s[4 * u + 3] += static_cast<int32_t>(hi[u] >> 16);
+      }
+    }
+    // warp aggregation: interior pixels share one class, so per-lane L2
+    // reductions on the same addresses serialise.  The warp's lanes are split
+    // into groups of equal (class, channel group) -- a row edge gives 2-4 groups
+    // -- and each group's 16 channel sums are reduced across the warp (int32
+    // transpose-reduce, |sum| <= 32 * 128 * N) into one reduction per channel.
+    const int lane = threadIdx.x & 31;
+    const int key = ok ? cell * 4096 + grp : -1;
+    unsigned long long* dst = reinterpret_cast<unsigned long long*>(p.ic_S) +
+                              static_cast<int64_t>(ok ? cell : 0) * c256 + (ok ? grp : 0) * 16;
+    int32_t v[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) v[e] = ok ? s[e] - 128 * (n1 - n0) : 0;
+    const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
+    const int ch = (b4 ? 8 : 0) + (b3 ? 4 : 0) + (b2 ? 2 : 0) + (b1 ? 1 : 0);
+    unsigned remaining = __ballot_sync(0xffffffffu, ok);
+    while (remaining) {
+      const int leader = __ffs(remaining) - 1;
+      const int lkey = __shfl_sync(0xffffffffu, key, leader);
+      const bool mine = ok && key == lkey;
+      remaining &= ~__ballot_sync(0xffffffffu, mine);
+      int32_t w8[8], w4[4], w2[2];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int32_t lo = mine ? v[e] : 0, hi = mine ? v[e + 8] : 0;
+        w8[e] = (b4 ? hi : lo) + __shfl_xor_sync(0xffffffffu, b4 ? lo : hi, 16);
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) w4[e] = (b3 ? w8[e + 4] : w8[e]) + __shfl_xor_sync(0xffffffffu, b3 ? w8[e] : w8[e + 4], 8);
+#pragma unroll
+      for (int e = 0; e < 2; ++e) w2[e] = (b2 ? w4[e + 2] : w4[e]) + __shfl_xor_sync(0xffffffffu, b2 ? w4[e] : w4[e + 2], 4);
+      int32_t w1 = (b1 ? w2[1] : w2[0]) + __shfl_xor_sync(0xffffffffu, b1 ? w2[0] : w2[1], 2);
+      w1 += __shfl_xor_sync(0xffffffffu, w1, 1);
+      unsigned long long* d0 =
+          reinterpret_cast<unsigned long long*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(dst), leader));
+      if (!(lane & 1) && w1 != 0) red_add_u64(d0 + ch, static_cast<unsigned long long>(static_cast<long long>(w1)));
+    }
+  }
+}
+
 // producer side: every digit writer warp of the grid has released its stores
 __device__ __forceinline__ void icb_wait_ready(const ConvTcParams& p) {
   while (ld_acquire_gpu(p.icb_ready) < p.icb_writers) __nanosleep(64);
@@ -906,6 +1035,9 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
       icb_write_digits(p, static_cast<int64_t>(p.conv_grid) * (kRhsWarps * 32) +
                               static_cast<int64_t>(blockIdx.x - p.conv_grid) * kConvThreads + threadIdx.x, writers);
     }
+    if (DT == DT_I8 && p.rhs_mode == 4)
+      ic_class_sums_fr(p, static_cast<int64_t>(blockIdx.x - p.conv_grid) * kConvThreads + threadIdx.x,
+                       static_cast<int64_t>(p.ic_ctas) * kConvThreads);
     if (FIC && p.rhs_mode == 1)
       fic_rhs_fr<DT, 16>(p, static_cast<int64_t>(blockIdx.x - p.conv_grid) * kConvThreads + threadIdx.x,
                      static_cast<int64_t>(p.ic_ctas) * kConvThreads, acc, facc_rhs);
@@ -964,6 +1096,9 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
   }
   __shared__ int s_fr_claim;
   __shared__ long long s_rhs_all[kConvThreads / 32];
+  unsigned long long* const s_ic = p.ic_smem ? reinterpret_cast<unsigned long long*>(smem + L.ic_off) : nullptr;
+  if (s_ic)
+    for (int i = threadIdx.x; i < p.K; i += kConvThreads) s_ic[i] = 0ull;
   if (threadIdx.x == 0) s_fr_claim = 0;
   if (threadIdx.x < kConvThreads / 32) s_rhs_all[threadIdx.x] = 0;
   if (warp == 1) tmem_alloc(tmem_slot, tmem_cols);
@@ -1117,6 +1252,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
     EpiCtx e;
     e.PQ = static_cast<int64_t>(p.P) * p.Q;
     e.bias_smem = p.K <= kBiasSmem ? s_bias : nullptr;
+    e.ic_acc = s_ic;
     // chunk-sum in int32 is exact when 16 * max|acc| < 2^31 (CRS < 8192)
     e.chunk32 = p.ntaps * p.c16 * 16 < 8192;
     // ConvOut fault hook target (faults.hpp:230-233), decoded once
@@ -1219,9 +1355,17 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
       uint32_t dig[4] = {0u, 0u, 0u, 0u};
       if (FC && part == 0) tmem_ld4(t_row + p.block_n, dig);
       // fast path: no fault hook, no filler channels, no IC column sums (warp-uniform)
-      const bool slow = p.fault_key >= 0 || (p.check & CHECK_IC) || p.icb_d || k_base + c_hi * 16 > p.K;
+      const bool slow = p.fault_key >= 0 || k_base + c_hi * 16 > p.K;
+      // IC column sums / ICBatch batch sums on the fast path (int8 plans only)
+      const int xtra = DT != DT_I8 ? 0 : (p.check & CHECK_IC) ? 1 : (p.icb_d ? 2 : 0);
       Acc row_sum = 0;
       if (p.dbg & 1) {
+      } else if (!slow && xtra == 1) {
+        row_sum = p.relu ? epi_columns<DT, EPI, true, FC || FIC, false, false, 1>(p, e, t_row, k_base, c_lo, c_hi, af_sum)
+                         : epi_columns<DT, EPI, false, FC || FIC, false, false, 1>(p, e, t_row, k_base, c_lo, c_hi, af_sum);
+      } else if (!slow && xtra == 2) {
+        row_sum = p.relu ? epi_columns<DT, EPI, true, FC || FIC, false, false, 2>(p, e, t_row, k_base, c_lo, c_hi, af_sum)
+                         : epi_columns<DT, EPI, false, FC || FIC, false, false, 2>(p, e, t_row, k_base, c_lo, c_hi, af_sum);
       } else if (!slow) {
         if (p.dbg & 64)
           row_sum = epi_columns<DT, EPI, true, false, false>(p, e, t_row, k_base, c_lo, c_hi, af_sum);
@@ -1471,6 +1615,11 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
           }
         }
       }
+    } else if (DT == DT_I8 && p.rhs_mode == 4 && p.ic_ctas == 0) {
+      // IC input checksum (class sums) by the two input-checksum warps
+      pdl_wait();
+      ic_class_sums_fr(p, static_cast<int64_t>(blockIdx.x) * (kRhsWarps * 32) + rw * 32 + lane,
+                       static_cast<int64_t>(p.conv_grid) * (kRhsWarps * 32));
     } else if (DT == DT_I8 && FIC && p.rhs_mode == 1 && p.ic_ctas == 0) {
       pdl_wait();
       if (fr_share) {
@@ -1512,6 +1661,9 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
     tc_fence_after();
     tmem_dealloc(tmem_base, tmem_cols);
   }
+  if (s_ic)  // IC: this CTA's per-channel output sums, one reduction per channel
+    for (int i = threadIdx.x; i < p.K; i += kConvThreads)
+      if (s_ic[i]) red_add_u64(&p.ic_sum[i], s_ic[i]);
 
   // ---------------------------------------------------------------- verdict records
   // Each CTA stores its partials in its own record and exits; verdict_kernel

@@ -597,33 +597,58 @@ __global__ void fic_finalize_kernel(const int64_t* __restrict__ part, int n, con
   }
 }
 
-// IC per-channel: out_sum[k] vs dot(f[k,:], ic) in i64; first mismatching k
-__global__ void ic_finalize_kernel(const unsigned long long* __restrict__ ksum, const int8_t* __restrict__ f,
-                                   const int32_t* __restrict__ ic, int64_t K, int64_t crs, abed_verify_outcome* out) {
-  __shared__ int s_first;
-  __shared__ long long s_cnt;
-  if (threadIdx.x == 0) { s_first = 0x7fffffff; s_cnt = 0; }
-  __syncthreads();
-  for (int64_t k = threadIdx.x; k < K; k += blockDim.x) {
+// IC per-channel (ic_verify_k, checksum.hpp:319-347): out_sum[k] vs
+// dot(f[k,:], ic) in i64, one block per channel (the CRS-long dot split over 256
+// threads); the count and the first mismatching k go to scr = {count, first k,
+// ticket, -, dot[K]}, and the last block writes the outcome and resets scr[0..2].
+__global__ void __launch_bounds__(256) ic_finalize_kernel(const unsigned long long* __restrict__ ksum,
+                                                          const int8_t* __restrict__ f, const int32_t* __restrict__ ic,
+                                                          int64_t K, int64_t crs, unsigned long long* scr,
+                                                          abed_verify_outcome* out) {
+  __shared__ long long s_part[8];
+  __shared__ bool s_last;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int64_t k = blockIdx.x; k < K; k += gridDim.x) {
     long long dot = 0;
-    for (int64_t i = 0; i < crs; ++i) dot += (long long)f[k * crs + i] * ic[i];
-    const long long lhs = (long long)ksum[k];
-    if (lhs != dot) {
-      atomicAdd((unsigned long long*)&s_cnt, 1ull);
-      atomicMin(&s_first, (int)k);
+    for (int64_t i = threadIdx.x; i < crs; i += blockDim.x) dot += (long long)f[k * crs + i] * ic[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+    if (lane == 0) s_part[w] = dot;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      long long d = 0;
+      for (int q = 0; q < (int)(blockDim.x >> 5); ++q) d += s_part[q];
+      scr[4 + k] = (unsigned long long)d;
+      if ((long long)ksum[k] != d) {
+        atomicAdd(&scr[0], 1ull);
+        atomicMin(&scr[1], (unsigned long long)k);
+      }
     }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(&scr[2], 1ull) == gridDim.x - 1;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    if (s_cnt == 0) {
-      write_outcome(out, 0, 0, 0, 0, 0, 0, 0, 0);
-    } else {
-      const int64_t k = s_first;
-      long long dot = 0;
-      for (int64_t i = 0; i < crs; ++i) dot += (long long)f[k * crs + i] * ic[i];
-      write_outcome(out, 1, 1, k, -1, -1, (long long)ksum[k], dot, s_cnt);
-    }
+  if (!s_last || threadIdx.x != 0) return;
+  __threadfence();
+  const unsigned long long cnt = __ldcg(&scr[0]);
+  if (cnt == 0) {
+    write_outcome(out, 0, 0, 0, 0, 0, 0, 0, 0);
+  } else {
+    const int64_t k = (int64_t)__ldcg(&scr[1]);
+    write_outcome(out, 1, 1, k, -1, -1, (long long)ksum[k], (long long)__ldcg(&scr[4 + k]), (long long)cnt);
   }
+  scr[0] = 0ull;
+  scr[1] = ~0ull;
+  scr[2] = 0ull;
+}
+
+void ic_finalize_launch(const unsigned long long* ksum, const int8_t* f, const int32_t* ic, int64_t K, int64_t crs,
+                        unsigned long long* scr, abed_verify_outcome* out, cudaStream_t st) {
+  const int blocks = (int)std::min<int64_t>(K, 4 * num_sms());
+  ic_finalize_kernel<<<blocks, 256, 0, st>>>(ksum, f, ic, K, crs, scr, out);
 }
 
 // ---------------------------------------------------------------------------

@@ -126,3 +126,39 @@ def test_icbatch_argument_errors():
     plain = api.ConvPlan(ls, f.cuda(), 0)
     icb = api.ConvPlan(ls, f.cuda(), abi.CHECK_ICBATCH)
     assert icb.info.packed_input_bytes > plain.info.packed_input_bytes
+
+
+def test_device_verdict_fold_equals_host_fold():
+    """abed_verdict_records / abed_verdict_combine on the device (the bench's
+    multi-GPU path) against the host fold, on a synthetic 3-rank gather."""
+    import ctypes as C
+    from paper_2006_04984_b200.dist import OUTCOME_BYTES, ShardedVerdicts, combine_host, records_host
+    kinds = [abi.FC, abi.FIC, abi.ICBATCH, abi.FC, abi.FIC, abi.IC]
+    ranks = []
+    for r in range(3):
+        outs = []
+        for i, k in enumerate(kinds):
+            o = abi.VerifyOutcome()
+            fail = (r + i) % 3 == 0
+            o.status, o.has_locus = int(fail and k != abi.FIC), int(fail and k != abi.FIC)
+            o.locus[0], o.locus[1], o.locus[2] = r + i, 2 * i, 3
+            o.lhs, o.rhs = 1000 * r + i, 1000 * r + (i if not fail else i + 7)
+            o.error_count = 2 if o.status else 0
+            outs.append(o)
+        ranks.append(outs)
+    gathered = [v for r, outs in enumerate(ranks) for v in records_host(outs, kinds, n_offset=4 * r)]
+    want = combine_host(gathered, 3, kinds)
+    dev = torch.zeros(len(kinds) * OUTCOME_BYTES, dtype=torch.uint8, device="cuda")
+    host = (abi.VerifyOutcome * len(kinds))(*ranks[0])
+    dev.copy_(torch.frombuffer(bytearray(host), dtype=torch.uint8))
+    sv = ShardedVerdicts(dev, kinds, n_offset=0, force=True)
+    sv.record()
+    torch.cuda.synchronize()
+    assert sv.rec.cpu().tolist() == gathered[: len(kinds) * 8]
+    sv.gathered = torch.tensor(gathered, dtype=torch.int64, device="cuda")
+    sv.world = 3
+    sv._fold(C.c_void_p(torch.cuda.current_stream().cuda_stream))
+    got = sv.outcomes_global()
+    for a, b in zip(got, want):
+        assert (a.status, a.has_locus, tuple(a.locus), a.lhs, a.rhs, a.error_count) == \
+               (b.status, b.has_locus, tuple(b.locus), b.lhs, b.rhs, b.error_count)
