@@ -597,6 +597,45 @@ __global__ void fic_finalize_kernel(const int64_t* __restrict__ part, int n, con
   }
 }
 
+// IC input checksum from the in-kernel class sums (rhs_mode 4): thread per
+// (c, r, s) of gen_input_checksum (checksum.hpp:248-266): ic[c,r,s] = sum of
+// S[phase(r,s)][rc][cc][c] over the row classes whose filter-row mask holds r and
+// the column classes whose mask holds s; also FIC's rhs = sum fsum * ic (fic_dot,
+// :275-285) into *fic_rhs (zeroed by the caller).
+__global__ void ic_from_classes_kernel(const int64_t* __restrict__ S, const uint64_t* __restrict__ rowmask,
+                                       const uint64_t* __restrict__ colmask, ActGeom g, int nrc, int ncc,
+                                       const int32_t* __restrict__ fsum, int32_t* __restrict__ ic,
+                                       unsigned long long* fic_rhs) {
+  const int64_t crs = (int64_t)g.c * g.r * g.s;
+  const int c256 = g.c16 * 16;
+  long long dot = 0;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < crs; t += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(t / (g.r * g.s)), r = (int)((t / g.s) % g.r), sc = (int)(t % g.s);
+    const int a = r % g.sh, b = sc % g.sw, phase = a * g.nph_w + b;
+    long long v = 0;
+    for (int rc = 0; rc < nrc; ++rc) {
+      if (!((rowmask[a * nrc + rc] >> r) & 1ull)) continue;
+      for (int cc = 0; cc < ncc; ++cc)
+        if ((colmask[b * ncc + cc] >> sc) & 1ull) v += S[((int64_t)(phase * nrc + rc) * ncc + cc) * c256 + c];
+    }
+    ic[t] = (int32_t)v;
+    if (fsum) dot += (long long)fsum[t] * v;
+  }
+  if (fic_rhs) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+    if ((threadIdx.x & 31) == 0 && dot != 0) atomicAdd(fic_rhs, (unsigned long long)dot);
+  }
+}
+
+void ic_from_classes_launch(const int64_t* S, const uint64_t* rowmask, const uint64_t* colmask, const ActGeom& g,
+                            int nrc, int ncc, const int32_t* fsum, int32_t* ic, unsigned long long* fic_rhs,
+                            cudaStream_t st) {
+  const int64_t crs = (int64_t)g.c * g.r * g.s;
+  ic_from_classes_kernel<<<(int)std::min<int64_t>((crs + 127) / 128, 4 * num_sms()), 128, 0, st>>>(
+      S, rowmask, colmask, g, nrc, ncc, fsum, ic, fic_rhs);
+}
+
 // IC per-channel (ic_verify_k, checksum.hpp:319-347): out_sum[k] vs
 // dot(f[k,:], ic) in i64, one block per channel (the CRS-long dot split over 256
 // threads); the count and the first mismatching k go to scr = {count, first k,
