@@ -123,37 +123,36 @@ __device__ __forceinline__ void transpose_store4(const uint32_t (&cw)[16], uint4
     if (u < n_pix) dst[u] = make_uint4(o[u][0], o[u][1], o[u][2], o[u][3]);
 }
 
-__global__ void pack_input_v4_kernel(const int8_t* __restrict__ x, ActGeom g, int64_t x_bytes, int vec_ok,
-                                     int8_t* __restrict__ out) {
-  const int qpr = (g.Wl + 3) >> 2;                       // quads per M-space row
-  const int64_t rows = (int64_t)g.n * g.Hl;
-  const int64_t planes = (int64_t)g.n_phase * g.c16;
-  const int64_t body = planes * rows * qpr;
-  const int64_t tail_pix = g.plane_len - g.m_total;       // zero pixels after the last image
-  const int64_t tail_q = (tail_pix + 3) >> 2;
-  const int64_t total = body + planes * tail_q;
+__global__ void __launch_bounds__(256) pack_input_v4_kernel(const int8_t* __restrict__ x, ActGeom g, int64_t x_bytes,
+                                                            int vec_ok, int8_t* __restrict__ out) {
+  // blockIdx.y = plane (phase, channel group); 32-bit index math inside a plane
+  // (64-bit divisions per quad made this kernel issue-bound)
+  const int plane = blockIdx.y;
+  const int grp = plane % g.c16;
+  const int phase = plane / g.c16;
+  const int a = phase / g.nph_w, b = phase % g.nph_w;
+  const uint32_t qpr = (uint32_t)((g.Wl + 3) >> 2);  // quads per M-space row
+  const uint32_t rows = (uint32_t)g.n * (uint32_t)g.Hl;
+  const uint32_t body = rows * qpr;
+  const uint32_t tail_q = (uint32_t)((g.plane_len - g.m_total + 3) >> 2);  // zero quads after the last image
+  const uint32_t total = body + tail_q;
   const int64_t HW = (int64_t)g.h * g.w;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
+  uint4* const pbase = reinterpret_cast<uint4*>(out) + (int64_t)plane * g.plane_len;
+  for (uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
     if (idx >= body) {
-      const int64_t k = idx - body;
-      const int64_t plane = k / tail_q, t0 = g.m_total + (k % tail_q) * 4;
-      uint4* dst = reinterpret_cast<uint4*>(out) + plane * g.plane_len + t0;
+      const int64_t t0 = g.m_total + (int64_t)(idx - body) * 4;
+      uint4* dst = pbase + t0;
       const int np = (int)(g.plane_len - t0 < 4 ? g.plane_len - t0 : 4);
       for (int u = 0; u < np; ++u) dst[u] = make_uint4(0, 0, 0, 0);
       continue;
     }
-    const int qi = (int)(idx % qpr);
-    const int64_t rest = idx / qpr;
-    const int64_t row = rest % rows;  // n * Hl + i
-    const int64_t plane = rest / rows;
-    const int grp = (int)(plane % g.c16);
-    const int phase = (int)(plane / g.c16);
-    const int n = (int)(row / g.Hl), i = (int)(row % g.Hl);
-    const int j0 = qi * 4;
+    const uint32_t row = idx / qpr;  // n * Hl + i
+    const uint32_t qi = idx - row * qpr;
+    const uint32_t n = row / (uint32_t)g.Hl;
+    const int i = (int)(row - n * (uint32_t)g.Hl);
+    const int j0 = (int)qi * 4;
     const int n_pix = min(4, g.Wl - j0);
-    uint4* dst = reinterpret_cast<uint4*>(out) + plane * g.plane_len + row * g.Wl + j0;
-    const int a = phase / g.nph_w, b = phase % g.nph_w;
+    uint4* dst = pbase + (int64_t)row * g.Wl + j0;
     const int hh = i * g.sh + a - g.ph;
     const int ww0 = j0 * g.sw + b - g.pw;
     uint32_t cw[16];
@@ -169,18 +168,26 @@ __global__ void pack_input_v4_kernel(const int8_t* __restrict__ x, ActGeom g, in
         if (u < n_pix && ww >= 0 && ww < g.w) keep |= 0xFFu << (8 * u);
       }
       const int64_t row0 = ((int64_t)n * g.c + grp * 16) * HW + (int64_t)hh * g.w;
-      if (g.sw == 1 && vec_ok) {
+      if (g.sw == 1 && vec_ok && x_bytes >= 4) {
+        // all 32 aligned words first (clamped addresses, no branches), then the
+        // funnel shifts: with load -> use per channel only two loads were in flight
+        uint32_t lo[16], hi[16];
+        int64_t al[16];
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
-          uint32_t v = 0;
-          if (grp * 16 + e < g.c && keep) {
-            const int64_t off = row0 + (int64_t)e * HW + ww0;
-            const int64_t al = off & ~int64_t(3);
-            const uint32_t lo = al >= 0 ? __ldg(reinterpret_cast<const uint32_t*>(x + al)) : 0u;
-            const uint32_t hi = al + 4 < x_bytes ? __ldg(reinterpret_cast<const uint32_t*>(x + al + 4)) : 0u;
-            v = __funnelshift_r(lo, hi, (uint32_t)(off & 3) * 8) & keep;
-          }
-          cw[e] = v;
+          const int ce = min(grp * 16 + e, g.c - 1);
+          al[e] = ((int64_t)n * g.c + ce) * HW + (int64_t)hh * g.w + ww0;
+          const int64_t a = al[e] & ~int64_t(3);
+          const int64_t a0 = a < 0 ? 0 : a, a1 = a + 4 > x_bytes - 4 ? x_bytes - 4 : a + 4;
+          lo[e] = __ldg(reinterpret_cast<const uint32_t*>(x + a0));
+          hi[e] = __ldg(reinterpret_cast<const uint32_t*>(x + a1));
+        }
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const int64_t a = al[e] & ~int64_t(3);
+          const uint32_t l = a >= 0 ? lo[e] : 0u, h = a + 4 < x_bytes ? hi[e] : 0u;
+          const uint32_t v = __funnelshift_r(l, h, (uint32_t)(al[e] & 3) * 8) & keep;
+          cw[e] = grp * 16 + e < g.c ? v : 0u;
         }
       } else {
 #pragma unroll
@@ -201,13 +208,17 @@ __global__ void pack_input_v4_kernel(const int8_t* __restrict__ x, ActGeom g, in
 }
 
 void launch_pack_input(const int8_t* x, const ActGeom& g, int8_t* packed, cudaStream_t st) {
-  const int64_t quads = (int64_t)g.n_phase * g.c16 * ((int64_t)g.n * g.Hl * ((g.Wl + 3) / 4) + g.plane_len / 4);
+  const int64_t per_plane = (int64_t)g.n * g.Hl * ((g.Wl + 3) / 4) + (g.plane_len - g.m_total + 3) / 4;
+  if (per_plane >= (int64_t(1) << 31)) throw_invalid("pack_input: plane too large");
+  const int planes = g.n_phase * g.c16;
   const int64_t x_bytes = (int64_t)g.n * g.c * g.h * g.w;
-  int64_t blocks = (quads + 255) / 256;
-  const int64_t cap = (int64_t)num_sms() * 16;
-  if (blocks > cap) blocks = cap;
+  // about 8 resident 256-thread blocks per SM over all planes
+  int64_t bx = ((int64_t)num_sms() * 8 + planes - 1) / planes;
+  const int64_t need = (per_plane + 255) / 256;
+  if (bx > need) bx = need;
+  if (bx < 1) bx = 1;
   const int vec_ok = (reinterpret_cast<uintptr_t>(x) & 3) == 0;  // aligned 32-bit source loads
-  pack_input_v4_kernel<<<(unsigned)blocks, 256, 0, st>>>(x, g, x_bytes, vec_ok, packed);
+  pack_input_v4_kernel<<<dim3((unsigned)bx, (unsigned)planes), 256, 0, st>>>(x, g, x_bytes, vec_ok, packed);
 }
 
 // ---------------------------------------------------------------------------

@@ -3,6 +3,7 @@
 // reductions are exact (order-independent) and float-mode reductions keep the
 // reference's sequential order so results are bit-identical to its -march=native
 // build (FMA contraction spelled out with fma/fmaf).
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -181,39 +182,43 @@ __global__ void recombine_kernel(const int32_t* __restrict__ e, int64_t n, int64
 // once -- with an integer atomic only when several blocks split the rows (exact
 // and deterministic either way).  `out` must be zeroed when row_splits > 1.
 constexpr int kColsumWarps = 8;
-__global__ void __launch_bounds__(kColsumWarps * 32) colsum_i8_v16_kernel(const int8_t* __restrict__ x, int64_t rows,
-                                                                        int64_t len, int64_t rows_per,
-                                                                        int32_t* __restrict__ out) {
-  __shared__ int32_t red[kColsumWarps][16][32];  // [warp][column in vector][lane]: conflict-free
+// Cluster variant (no atomics, no memset): the row splits of one 512-column tile
+// form a thread-block cluster; every CTA reduces its rows into shared memory, then
+// each CTA sums its share of the tile's columns across the cluster's CTAs through
+// distributed shared memory and stores them.  One launch, plain stores.
+__global__ void __launch_bounds__(kColsumWarps * 32) colsum_i8_cluster_kernel(const int8_t* __restrict__ x,
+                                                                            int64_t rows, int64_t len,
+                                                                            int64_t rows_per,
+                                                                            int32_t* __restrict__ out) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  __shared__ int32_t red[kColsumWarps][16][32];
+  __shared__ int32_t s_part[512];
+  const int cs = static_cast<int>(cluster.num_blocks());
+  const int rank = static_cast<int>(cluster.block_rank());
   const int64_t cols16 = len >> 4;
-  const int64_t col_tiles = (cols16 + 31) / 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t tile = blockIdx.x % col_tiles, split = blockIdx.x / col_tiles;
+  const int64_t tile = blockIdx.x / cs;
   const int64_t c16 = tile * 32 + lane;
-  const int64_t r0 = split * rows_per, r1 = r0 + rows_per < rows ? r0 + rows_per : rows;
+  const int64_t r0 = rank * rows_per, r1 = r0 + rows_per < rows ? r0 + rows_per : rows;
   int32_t acc[16];
 #pragma unroll
   for (int j = 0; j < 16; ++j) acc[j] = 0;
   if (c16 < cols16) {
-    // SIMD byte sums: x ^ 0x80 is x + 128 as an unsigned byte; bytes 0/2 and 1/3
-    // of each word accumulate in the two 16-bit halves of one register (LOP3 +
-    // SHF + LOP3 + 2 IADD per 4 bytes), flushed to int32 every 256 rows (255 x 256
-    // < 2^16) and un-biased by 128 x rows at the end
-    const uint4* base = reinterpret_cast<const uint4*>(x) + c16;
-    int64_t nrows = 0;
-    int64_t r = r0 + warp;
-    while (r < r1) {
+    // the warp's rows r0 + warp, + 8, ...: full batches of 8 rows with every load
+    // issued before use (pointer increments, no predicates), then a masked tail
+    const int64_t step = (int64_t)kColsumWarps * cols16;  // uint4 stride between a warp's rows
+    const uint4* ptr = reinterpret_cast<const uint4*>(x) + c16 + (r0 + warp) * cols16;
+    const int64_t mine = r1 - r0 > warp ? (r1 - r0 - warp + kColsumWarps - 1) / kColsumWarps : 0;
+    int64_t done = 0;
+    while (done < mine) {
       uint32_t ev[4] = {0u, 0u, 0u, 0u}, od[4] = {0u, 0u, 0u, 0u};
-      for (int it = 0; it < 32 && r < r1; ++it, r += 8 * kColsumWarps) {  // <= 256 rows, eight in flight
+      int64_t batch_end = done + 256 < mine ? done + 256 : mine;  // 16-bit lanes: <= 256 rows per flush
+      for (; done + 8 <= batch_end; done += 8) {
         uint4 v[8];
-        bool ok[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          ok[u] = r + u * kColsumWarps < r1;
-          v[u] = ok[u] ? __ldcs(base + (r + u * kColsumWarps) * cols16) : make_uint4(0x80808080u, 0x80808080u,
-                                                                                      0x80808080u, 0x80808080u);
-          nrows += ok[u] ? 1 : 0;
-        }
+        for (int u = 0; u < 8; ++u) v[u] = __ldcs(ptr + u * step);
+        ptr += 8 * step;
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const uint32_t w[4] = {v[u].x ^ 0x80808080u, v[u].y ^ 0x80808080u, v[u].z ^ 0x80808080u,
@@ -225,6 +230,16 @@ __global__ void __launch_bounds__(kColsumWarps * 32) colsum_i8_v16_kernel(const 
           }
         }
       }
+      for (; done < batch_end; ++done) {
+        const uint4 v = __ldcs(ptr);
+        ptr += step;
+        const uint32_t w[4] = {v.x ^ 0x80808080u, v.y ^ 0x80808080u, v.z ^ 0x80808080u, v.w ^ 0x80808080u};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          ev[q] += w[q] & 0x00FF00FFu;
+          od[q] += (w[q] >> 8) & 0x00FF00FFu;
+        }
+      }
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         acc[4 * q] += static_cast<int32_t>(ev[q] & 0xFFFFu);
@@ -234,26 +249,30 @@ __global__ void __launch_bounds__(kColsumWarps * 32) colsum_i8_v16_kernel(const 
       }
     }
 #pragma unroll
-    for (int j = 0; j < 16; ++j) acc[j] -= static_cast<int32_t>(128 * nrows);
+    for (int j = 0; j < 16; ++j) acc[j] -= static_cast<int32_t>(128 * mine);
   }
 #pragma unroll
   for (int j = 0; j < 16; ++j) red[warp][j][lane] = acc[j];
   __syncthreads();
-  const bool split_rows = rows_per < rows;
-  for (int e = threadIdx.x; e < 32 * 16; e += kColsumWarps * 32) {
+  for (int e = threadIdx.x; e < 512; e += kColsumWarps * 32) {
     const int j = e >> 5, ln = e & 31;
-    const int64_t col = tile * 512 + ln * 16 + j;
-    if (col >= len) continue;
-    int32_t s = 0;
+    int32_t sum = 0;
 #pragma unroll
-    for (int q = 0; q < kColsumWarps; ++q) s += red[q][j][ln];
-    if (split_rows) {
-      if (s != 0) atomicAdd(out + col, s);
-    } else {
-      out[col] = s;
-    }
+    for (int q = 0; q < kColsumWarps; ++q) sum += red[q][j][ln];
+    s_part[ln * 16 + j] = sum;  // column tile * 512 + ln * 16 + j
   }
+  cluster.sync();
+  const int per = (512 + cs - 1) / cs;
+  for (int cl = rank * per + threadIdx.x; cl < (rank + 1) * per && cl < 512; cl += kColsumWarps * 32) {
+    const int64_t col = tile * 512 + cl;
+    if (col >= len) continue;
+    int32_t sum = 0;
+    for (int q = 0; q < cs; ++q) sum += cluster.map_shared_rank(s_part, q)[cl];
+    out[col] = sum;
+  }
+  cluster.sync();  // keep this CTA's partials alive until every peer has read them
 }
+
 // any length / alignment: one column per thread, the same row split
 __global__ void colsum_i8_kernel(const int8_t* __restrict__ x, int64_t rows, int64_t len, int64_t rows_per,
                                  int32_t* __restrict__ out) {
@@ -501,21 +520,33 @@ int guarded2(Fn&& fn) {
 void dev_colsum_i8(const int8_t* x, int64_t rows, int64_t len, int32_t* out, cudaStream_t st) {
   const bool v16 = (len % 16 == 0) && (reinterpret_cast<uintptr_t>(x) % 16 == 0);
   if (v16) {
-    // split the rows over blocks so the grid is about one full wave (8 resident
-    // blocks per SM) -- a partial second wave would double the latency tail
+    // row splits of a 512-column tile = one cluster (<= 16 CTAs, DSMEM reduction):
+    // about 8 resident CTAs per SM in one wave, at least one row per warp
     const int64_t col_tiles = (len / 16 + 31) / 32;
-    int64_t splits = ((int64_t)num_sms() * 8) / col_tiles;
-    const int64_t max_splits = (rows + kColsumWarps - 1) / kColsumWarps;  // >= one row per warp
-    if (splits > max_splits) splits = max_splits;
-    // every split adds one integer atomic per column: same-address atomics
-    // serialise in L2 (394 splits over 1152 columns measured 38 us for 29 MB),
-    // so cap the contention per column
-    if (splits > 64) splits = 64;
-    if (splits < 1) splits = 1;
-    const int64_t rows_per = (rows + splits - 1) / splits;
-    splits = (rows + rows_per - 1) / rows_per;
-    if (rows_per < rows) cuda_check(cudaMemsetAsync(out, 0, (size_t)len * 4, st), "colsum memset");
-    colsum_i8_v16_kernel<<<(unsigned)(col_tiles * splits), kColsumWarps * 32, 0, st>>>(x, rows, len, rows_per, out);
+    int64_t cs = ((int64_t)num_sms() * 8) / col_tiles;
+    const int64_t max_cs = (rows + kColsumWarps - 1) / kColsumWarps;
+    if (cs > max_cs) cs = max_cs;
+    if (cs > 16) cs = 16;
+    if (cs < 1) cs = 1;
+    const int64_t rows_per = (rows + cs - 1) / cs;
+    static bool attr = false;
+    if (!attr) {
+      cuda_check(cudaFuncSetAttribute(colsum_i8_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
+                 "colsum cluster attr");
+      attr = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(col_tiles * cs));
+    cfg.blockDim = dim3(kColsumWarps * 32);
+    cfg.stream = st;
+    cudaLaunchAttribute la[1];
+    la[0].id = cudaLaunchAttributeClusterDimension;
+    la[0].val.clusterDim.x = (unsigned)cs;
+    la[0].val.clusterDim.y = 1;
+    la[0].val.clusterDim.z = 1;
+    cfg.attrs = la;
+    cfg.numAttrs = 1;
+    cuda_check(cudaLaunchKernelEx(&cfg, colsum_i8_cluster_kernel, x, rows, len, rows_per, out), "colsum launch");
   } else {
     cuda_check(cudaMemsetAsync(out, 0, (size_t)len * 4, st), "colsum memset");
     const int64_t want = (int64_t)num_sms() * 4 * 256;
