@@ -232,6 +232,27 @@ int abed_run_trial(const abed_layer_shape* shape, const int8_t* input, const int
  * pass 0, config->trials for the whole campaign. */
 int abed_run_campaign(const abed_campaign_config* config, int64_t trial_begin, int64_t trial_end,
                       abed_campaign_report* report);
+/* faults.hpp:276-333 run_campaign, trial-parallel: the same report as
+ * abed_run_campaign, every trial of [trial_begin, trial_end) evaluated in ONE
+ * launch (one CTA per trial) from the golden int32 ConvOut, the pristine
+ * checksums and the ConvOut elements the flip perturbs (exact: the reference's
+ * int32 ConvOut wrap, int64 verify sums and epilog).  abed_run_campaign re-runs
+ * the fused protected conv per trial instead; both give identical reports. */
+int abed_run_campaign_batched(const abed_campaign_config* config, int64_t trial_begin, int64_t trial_end,
+                              abed_campaign_report* report);
+/* Device-resident form (bench / multi-GPU sharding): create draws the data, the
+ * golden ConvOut, the pristine checksums and every trial's flip once; run adds the
+ * classification counts of trials [trial_begin, trial_end) into counts_dev[4]
+ * (int64, indexed by ABED_DETECTED / _SDC / _MASKED / _DETECTED_BENIGN) as one
+ * stream-ordered launch -- counts_dev is what an NCCL all-reduce sums across
+ * ranks; report_of folds host counts into an abed_campaign_report. */
+typedef struct abed_campaign abed_campaign;
+int abed_campaign_create(const abed_campaign_config* config, abed_campaign** campaign);
+int abed_campaign_run(abed_campaign* campaign, int64_t trial_begin, int64_t trial_end, int64_t* counts_dev,
+                      void* stream);
+int abed_campaign_report_of(const abed_campaign* campaign, const int64_t* counts_host, int64_t trials,
+                            abed_campaign_report* report);
+int abed_campaign_destroy(abed_campaign* campaign);
 
 /* ------------------------------------------------------------ protected conv (hot path)
  * A plan holds the packed filters (+ FC checksum-digit rows), the filter checksum

@@ -171,6 +171,11 @@ SIGNATURES = {
     "abed_run_trial": (C.c_int, [SHP, P, P, i32, i32, C.c_float, P, i64, i32, i32, u64,
                                  C.POINTER(TrialOutcome)]),
     "abed_run_campaign": (C.c_int, [C.POINTER(CampaignConfig), i64, i64, C.POINTER(CampaignReport)]),
+    "abed_run_campaign_batched": (C.c_int, [C.POINTER(CampaignConfig), i64, i64, C.POINTER(CampaignReport)]),
+    "abed_campaign_create": (C.c_int, [C.POINTER(CampaignConfig), C.POINTER(P)]),
+    "abed_campaign_run": (C.c_int, [P, i64, i64, P, P]),
+    "abed_campaign_report_of": (C.c_int, [P, C.POINTER(i64), i64, C.POINTER(CampaignReport)]),
+    "abed_campaign_destroy": (C.c_int, [P]),
     "abed_conv_plan_create": (C.c_int, [SHP, P, i32, i32, C.POINTER(P)]),
     "abed_conv_plan_destroy": (C.c_int, [P]),
     "abed_conv_plan_info": (C.c_int, [P, C.POINTER(PlanInfo)]),

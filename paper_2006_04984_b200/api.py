@@ -29,6 +29,17 @@ def _stream():
     return C.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
+def _keep_alive(t, stream):
+    """A temporary read by a kernel on a caller-supplied stream: tell the caching
+    allocator, so its memory is not reused before that stream has consumed it."""
+    if t is None or stream is None:
+        return
+    raw = stream.value if isinstance(stream, C.c_void_p) else getattr(stream, "cuda_stream", stream)
+    if raw is None or raw == torch.cuda.current_stream().cuda_stream:
+        return
+    t.record_stream(torch.cuda.ExternalStream(int(raw)))
+
+
 def _dims(t: torch.Tensor) -> abi.Dims4:
     d = list(t.shape) + [1] * (4 - t.dim())
     return abi.Dims4(*d)
@@ -289,16 +300,57 @@ def run_trial(ls, x, f, scheme, target, scale=0.05, bias=None, relu=True, output
     return o
 
 
-def run_campaign(ls, scheme, target, trials=1000, root_seed=1, mode=abi.DATA_ONES, scale=0.05, bias=None, relu=True,
-                 output_kind=I8, begin=0, end=None):
+def campaign_config(ls, scheme, target, trials=1000, root_seed=1, mode=abi.DATA_ONES, scale=0.05, bias=None,
+                    relu=True, output_kind=I8):
+    """faults.hpp:77-86 CampaignConfig (the bias array rides on the returned config)."""
     b = (C.c_float * len(bias))(*bias) if bias is not None else None
     cfg = abi.CampaignConfig(shape=ls, scheme=scheme, target=target, trials=trials, root_seed=root_seed, mode=mode,
                              scale=scale, bias_host=C.cast(b, C.c_void_p) if b is not None else None,
                              bias_len=0 if bias is None else len(bias), activation=abi.RELU if relu else abi.IDENTITY,
                              output_kind=output_kind, jobs=0)
+    cfg._bias_keepalive = b
+    return cfg
+
+
+def run_campaign(ls, scheme, target, trials=1000, root_seed=1, mode=abi.DATA_ONES, scale=0.05, bias=None, relu=True,
+                 output_kind=I8, begin=0, end=None, batched=False):
+    """faults.hpp:276 run_campaign over trials [begin, end).  batched=False re-runs
+    the fused protected conv per trial; batched=True evaluates every trial in one
+    trial-parallel launch (abed_run_campaign_batched); the reports are identical."""
+    cfg = campaign_config(ls, scheme, target, trials, root_seed, mode, scale, bias, relu, output_kind)
     rep = abi.CampaignReport()
-    call("abed_run_campaign", C.byref(cfg), begin, trials if end is None else end, C.byref(rep))
+    call("abed_run_campaign_batched" if batched else "abed_run_campaign", C.byref(cfg), begin,
+         trials if end is None else end, C.byref(rep))
     return rep
+
+
+class Campaign:
+    """Device-resident trial-parallel campaign (abed_campaign_*): run(begin, end)
+    adds the classification counts of those trials into a device int64[4]
+    (detected, sdc, masked, detected_benign) with one launch."""
+
+    def __init__(self, ls, scheme, target, trials=1000, root_seed=1, mode=abi.DATA_ONES, scale=0.05, bias=None,
+                 relu=True, output_kind=I8):
+        self.cfg = campaign_config(ls, scheme, target, trials, root_seed, mode, scale, bias, relu, output_kind)
+        self.handle = C.c_void_p()
+        call("abed_campaign_create", C.byref(self.cfg), C.byref(self.handle))
+
+    def run(self, counts: torch.Tensor, begin=0, end=None, stream=None):
+        call("abed_campaign_run", self.handle, begin, self.cfg.trials if end is None else end, _p(counts),
+             stream or _stream())
+
+    def report(self, counts, trials):
+        h = (C.c_int64 * 4)(*[int(v) for v in counts.cpu().tolist()])
+        rep = abi.CampaignReport()
+        call("abed_campaign_report_of", self.handle, h, trials, C.byref(rep))
+        return rep
+
+    def __del__(self):
+        try:
+            if self.handle:
+                call("abed_campaign_destroy", self.handle)
+        except Exception:
+            pass
 
 
 # ------------------------------------------------------------------ protected conv plan (hot path)
@@ -390,6 +442,7 @@ class ConvPlan:
             fault_key=-1, fault_bit=0, stream=None, ep=None):
         if ep is None:
             ep = self.epilog_params(scale, bias, relu)
+            _keep_alive(self._bias, stream)
         call("abed_conv_plan_run", self.handle, _p(packed), C.byref(ep) if ep is not None else None, out_mode,
              C.c_void_p(out.data_ptr()) if out is not None else None, next_plan.handle if next_plan else None,
              fault_key, fault_bit, stream or _stream())
@@ -479,8 +532,10 @@ class ConvPlanH(ConvPlan):
 
     def pack(self, x_nchw_f32: torch.Tensor, packed: torch.Tensor | None = None, stream=None) -> torch.Tensor:
         packed = self.packed_buffer() if packed is None else packed
-        call("abed_pack_input_h", self.handle, _p(x_nchw_f32.contiguous().to(torch.float32)), _p(packed),
-             stream or _stream())
+        x = x_nchw_f32.contiguous().to(torch.float32)
+        call("abed_pack_input_h", self.handle, _p(x), _p(packed), stream or _stream())
+        if x is not x_nchw_f32:
+            _keep_alive(x, stream)
         return packed
 
     def run(self, packed, out=None, out_mode=abi.OUT_F32_NCHW, scale=1.0, bias=None, relu=False, next_plan=None,

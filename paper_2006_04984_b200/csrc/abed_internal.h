@@ -150,7 +150,6 @@ struct abed_conv_plan {
   int rhs_src = ABED_RHS_REREAD;
   int64_t* d_fc_part = nullptr;     // FC row partials per N tile (n_tiles > 1)
   unsigned int* d_tile_sem = nullptr;  // FC per-M-tile flags (several N tiles), epoch-tagged
-  unsigned fc_epoch = 0;               // incremented per run; never 0 (the flags' initial value)
   int64_t* d_cta_rec = nullptr;     // FC per-CTA records
   unsigned long long* d_kacc = nullptr;  // kernel accumulators {FIC lhs, FIC rhs, done ticket, -}
   abed_verify_outcome* d_outcome = nullptr;  // {FC, FIC, IC} verdicts written by the conv kernel

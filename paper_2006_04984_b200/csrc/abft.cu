@@ -511,7 +511,10 @@ void run(abed_abft_plan* p, const int8_t* a, const int8_t* b, int32_t* c, int64_
   }
 }
 
-abed_abft_plan* create(int64_t m, int64_t n, int64_t k) {
+// all_modes: build the plain and fused GEMM plans too (abed_abft_plan_create, so
+// later runs in any mode stay allocation- and sync-free for graph capture); the
+// one-shot abed_abft_gemm_i8 runs only the checked mode and builds only `aug`.
+abed_abft_plan* create(int64_t m, int64_t n, int64_t k, bool all_modes) {
   require_device();
   validate_abft(m, n, k);
   auto* p = new abed_abft_plan();
@@ -524,9 +527,10 @@ abed_abft_plan* create(int64_t m, int64_t n, int64_t k) {
       cuda_check(cudaMalloc(&p->fc_out, 3 * sizeof(abed_verify_outcome)), "cudaMalloc(abft fc)");
       check_ws_alloc(p->ws, m, n);
       p->aug = gemm_plan(p, kDigits, 0);
-    // all three GEMM plans up front: runs stay allocation- and sync-free (graph capture)
-    p->plain = gemm_plan(p, 0, 0);
-    p->fused = gemm_plan(p, 0, ABED_CHECK_FC);
+      if (all_modes) {
+        p->plain = gemm_plan(p, 0, 0);
+        p->fused = gemm_plan(p, 0, ABED_CHECK_FC);
+      }
       cuda_check(cudaMalloc(&p->packed, (size_t)geom_packed_bytes(p->aug->g)), "cudaMalloc(abft packed)");
   } catch (...) {
     destroy(p);
@@ -540,7 +544,7 @@ abed_abft_plan* create(int64_t m, int64_t n, int64_t k) {
 extern "C" {
 
 int abed_abft_plan_create(int64_t m, int64_t n, int64_t k, abed_abft_plan** plan) {
-  return guarded([&] { *plan = create(m, n, k); });
+  return guarded([&] { *plan = create(m, n, k, true); });
 }
 
 int abed_abft_plan_destroy(abed_abft_plan* plan) {
@@ -563,7 +567,7 @@ int abed_abft_gemm_i8(const int8_t* a, int64_t m, int64_t k, const int8_t* b, in
                       int64_t* c_aug, abed_verify_outcome* row_check, abed_verify_outcome* col_check) {
   return guarded([&] {
     if (k != kb) throw_invalid("abft_gemm: inner dimensions do not match");
-    abed_abft_plan* p = create(m, n, k);
+    abed_abft_plan* p = create(m, n, k, false);
     abed_verify_outcome* d_out = nullptr;
     try {
       cuda_check(cudaMalloc(&d_out, 2 * sizeof(abed_verify_outcome)), "cudaMalloc(abft outcomes)");

@@ -24,14 +24,22 @@ int set_error(int code, const std::string& msg) {
 
 
 void require_device() {
-  static int ok = -1;
-  if (ok < 0) {
-    int dev = 0, n = 0;
-    ok = 0;
-    if (cudaGetDeviceCount(&n) == cudaSuccess && n > 0 && cudaGetDevice(&dev) == cudaSuccess) {
+  // checked per device ordinal (a process may drive several GPUs)
+  static int ok_dev[64];
+  static bool init = false;
+  if (!init) {
+    for (int& v : ok_dev) v = -1;
+    init = true;
+  }
+  int dev = 0, n = 0, ok = 0;
+  if (cudaGetDeviceCount(&n) == cudaSuccess && n > 0 && cudaGetDevice(&dev) == cudaSuccess) {
+    if (dev >= 0 && dev < 64 && ok_dev[dev] >= 0) {
+      ok = ok_dev[dev];
+    } else {
       int major = 0;
       cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
       ok = major == 10 ? 1 : 0;
+      if (dev >= 0 && dev < 64) ok_dev[dev] = ok;
     }
   }
   if (!ok) throw AbedError(ABED_ERR_NO_DEVICE, "abed: no sm_100 (B200) device available; the library has no host fallback");
@@ -110,8 +118,10 @@ void plan_init_common(abed_conv_plan* pl, const abed_layer_shape& shape, int che
   p.fault_key = -1;
   if (p.n_tiles > 1) {
     cuda_check(cudaMalloc(&pl->d_fc_part, (size_t)p.n_tiles * p.m_tiles * 128 * 2 * 8), "cudaMalloc(fc_part)");
-    cuda_check(cudaMalloc(&pl->d_tile_sem, (size_t)p.m_tiles * 4), "cudaMalloc(tile_sem)");
-    cuda_check(cudaMemset(pl->d_tile_sem, 0, (size_t)p.m_tiles * 4), "memset tile_sem");
+    // int8: per-(N tile, M tile, lane quarter) FC flags; float: per-M-tile counters
+    const size_t sem_bytes = (size_t)p.n_tiles * p.m_tiles * 4 * 4;
+    cuda_check(cudaMalloc(&pl->d_tile_sem, sem_bytes), "cudaMalloc(tile_sem)");
+    cuda_check(cudaMemset(pl->d_tile_sem, 0, sem_bytes), "memset tile_sem");
   }
   // one record per CTA of any launch (conv CTAs + input-checksum CTAs <= SMs)
   cuda_check(cudaMalloc(&pl->d_cta_rec, (size_t)std::max(num_sms(), conv_tc_grid(p, num_sms())) * abed_dev::kCtaRec * 8),
@@ -402,8 +412,6 @@ void plan_run(abed_conv_plan* pl, const int8_t* packed, const abed_epilog_params
   }
   p.fc_part = pl->d_fc_part;
   p.tile_sem = pl->d_tile_sem;
-  if (++pl->fc_epoch == 0u) pl->fc_epoch = 1u;
-  p.fc_epoch = pl->fc_epoch;
   p.cta_rec = pl->d_cta_rec;
   p.kacc = pl->d_kacc;
   p.outcome = pl->d_outcome;
@@ -522,7 +530,6 @@ abed_dev::VerdictJob plan_verdict_job(const abed_conv_plan* pl, abed_verify_outc
   j.out = out_dev;
   j.fc_part = pl->d_fc_part;
   j.tile_flag = pl->d_tile_sem;
-  j.fc_epoch = pl->fc_epoch;
   // int8 plans with several N tiles: the verdict rechecks flagged M tiles; float
   // plans keep the full-channel FC check in-kernel
   j.n_tiles = (pl->dw || pl->dtype != abed_dev::DT_I8) ? 1 : pl->base.n_tiles;

@@ -223,6 +223,285 @@ void draw(uint64_t seed, const abed_layer_shape& s, int target, int64_t& flat, i
   bit = (int)g.below(target == ABED_TARGET_CONVOUT ? 32u : 8u);
 }
 
+
+// ---------------------------------------------------------------------------
+// Trial-parallel campaign (faults.hpp:276-333 semantics, one CTA per trial).
+// A single-bit flip perturbs a known, small set of ConvOut elements -- one
+// element (ConvOut target), one channel's N x P x Q outputs scaled by the flipped
+// filter byte's delta times the input patch values (filter target), or the
+// K x (taps covering the pixel) outputs of one image (input target) -- so each
+// trial is evaluated exactly from the golden int32 ConvOut, the pristine
+// checksums and the perturbed elements alone, with the reference's int32
+// ConvOut wrap, its int64 verify sums and its epilog:
+//   FC  fc_verify (:211-236): row (n,p,q) sum vs the extra fmap.  The extra comes
+//       from the pristine filter checksum over the (possibly flipped) patches, so
+//       an input flip moves both sides by dx * fsum[c,r,s];
+//   FIC fic_verify (:287-294): total sum vs the pristine fic_dot;
+//   IC  ic_verify_k (:319-347): per-channel sums vs dot(filters used, pristine ic);
+//       a filter flip moves both sides of channel k by df * ic[c,r,s];
+//   output differs: epilog of every perturbed element vs its golden epilog.
+// The exhaustive path above (abed_run_campaign) re-runs the fused protected conv
+// per trial; tests check both give the same report.
+struct BatchedCampaignArgs {
+  abed_layer_shape s;
+  int scheme, target;
+  const int8_t* x;       // NCHW, pristine
+  const int8_t* f;       // KCRS, pristine
+  const int32_t* conv;   // golden ConvOut NKPQ
+  const int32_t* fsum;   // gen_filter_checksum (c,r,s)
+  const int32_t* ic;     // gen_input_checksum (c,r,s), pristine input
+  const float* bias;
+  float scale;
+  int relu, f32out;
+  const int64_t* flat;   // per trial: flat index, bit
+  const int32_t* bit;
+  int64_t n_trials;
+  unsigned long long* counts;  // [4] by classification (ABED_DETECTED, _SDC, _MASKED, _DETECTED_BENIGN)
+};
+
+__device__ __forceinline__ uint32_t epi_bits(int32_t a, float scale, float b, int relu, int f32out) {
+  float v = __fmaf_rn(static_cast<float>(a), scale, b);  // convolution.hpp:353-387 (FMA-contracted)
+  if (relu && v < 0.0f) v = 0.0f;
+  if (f32out) return __float_as_uint(v);
+  return static_cast<uint32_t>(static_cast<int32_t>(truncf(fminf(127.0f, fmaxf(-128.0f, v))))) & 0xFFu;
+}
+
+__device__ __forceinline__ int32_t wrap_add(int32_t v, int64_t d) {  // int32 ConvOut of the flipped operands
+  return static_cast<int32_t>(static_cast<uint32_t>(v) + static_cast<uint32_t>(static_cast<uint64_t>(d)));
+}
+
+__global__ void __launch_bounds__(256) campaign_batched_kernel(const __grid_constant__ BatchedCampaignArgs A) {
+  const abed_layer_shape& s = A.s;
+  const int64_t P = s.p, Q = s.q, PQ = P * Q, K = s.k, C = s.c, R = s.r, S = s.s;
+  __shared__ long long sh_tap[64];  // FC, input target: per-tap (= per-(p,q)) delta of the row sum
+  __shared__ int sh_flag[2];        // [0] detected (FC / IC), [1] output differs
+  __shared__ long long sh_red[8];
+  for (int64_t t = blockIdx.x; t < A.n_trials; t += gridDim.x) {
+    const int64_t flat = A.flat[t];
+    const int bit = A.bit[t];
+    if (threadIdx.x < 64) sh_tap[threadIdx.x] = 0;
+    if (threadIdx.x < 2) sh_flag[threadIdx.x] = 0;
+    __syncthreads();
+    int differs = 0, hit = 0;
+    long long total = 0;  // FIC: change of the ConvOut sum
+    if (A.target == ABED_TARGET_CONVOUT) {
+      if (threadIdx.x == 0) {
+        const int64_t k = (flat / PQ) % K;
+        const int32_t v = A.conv[flat];
+        const int32_t v2 = static_cast<int32_t>(static_cast<uint32_t>(v) ^ (1u << bit));
+        const long long d = static_cast<long long>(v2) - v;
+        total = d;
+        hit = d != 0;  // FC: its row; IC: its channel
+        differs = epi_bits(v2, A.scale, A.bias[k], A.relu, A.f32out) != epi_bits(v, A.scale, A.bias[k], A.relu, A.f32out);
+      }
+    } else if (A.target == ABED_TARGET_FILTER) {
+      const int64_t ss = flat % S, r = (flat / S) % R, c = (flat / (S * R)) % C, k = flat / (S * R * C);
+      const int8_t f0 = A.f[flat];
+      const long long df = static_cast<long long>(static_cast<int8_t>(f0 ^ static_cast<int8_t>(1 << bit))) - f0;
+      const float b = A.bias[k];
+      const int64_t npq = s.n * PQ;
+      for (int64_t i = threadIdx.x; i < npq; i += blockDim.x) {
+        const int64_t n = i / PQ, pq = i - n * PQ, pp = pq / Q, qq = pq - pp * Q;
+        const int64_t h = pp * s.stride_h + r - s.pad_h, w = qq * s.stride_w + ss - s.pad_w;
+        if (h < 0 || h >= s.h || w < 0 || w >= s.w) continue;
+        const int8_t xv = A.x[((n * C + c) * s.h + h) * s.w + w];
+        if (xv == 0) continue;
+        const int64_t o = (n * K + k) * PQ + pq;
+        const int32_t v = A.conv[o], v2 = wrap_add(v, df * xv);
+        const long long d = static_cast<long long>(v2) - v;
+        total += d;
+        hit |= d != 0;  // FC: row (n,p,q) moves, its extra does not
+        differs |= epi_bits(v2, A.scale, b, A.relu, A.f32out) != epi_bits(v, A.scale, b, A.relu, A.f32out);
+      }
+      if (A.scheme == ABED_IC) hit = 0;  // decided on the channel sum below
+    } else {
+      const int64_t w0 = flat % s.w, h0 = (flat / s.w) % s.h, c = (flat / (s.w * s.h)) % C, n = flat / (s.w * s.h * C);
+      const int8_t x0 = A.x[flat];
+      const long long dx = static_cast<long long>(static_cast<int8_t>(x0 ^ static_cast<int8_t>(1 << bit))) - x0;
+      const int taps = static_cast<int>(R * S);
+      for (int64_t k = threadIdx.x; k < K; k += blockDim.x) {
+        const float b = A.bias[k];
+        long long ksum = 0;
+        for (int tap = 0; tap < taps; ++tap) {
+          const int64_t r = tap / S, ss = tap - r * S;
+          const int64_t hp = h0 + s.pad_h - r, wp = w0 + s.pad_w - ss;
+          if (hp < 0 || wp < 0 || hp % s.stride_h || wp % s.stride_w) continue;
+          const int64_t pp = hp / s.stride_h, qq = wp / s.stride_w;
+          if (pp >= P || qq >= Q) continue;
+          const int8_t fv = A.f[((k * C + c) * R + r) * S + ss];
+          if (fv == 0) continue;
+          const int64_t o = (n * K + k) * PQ + pp * Q + qq;
+          const int32_t v = A.conv[o], v2 = wrap_add(v, dx * fv);
+          const long long d = static_cast<long long>(v2) - v;
+          ksum += d;
+          if (A.scheme == ABED_FC && d) atomicAdd(reinterpret_cast<unsigned long long*>(&sh_tap[tap]),
+                                                  static_cast<unsigned long long>(d));
+          differs |= epi_bits(v2, A.scale, b, A.relu, A.f32out) != epi_bits(v, A.scale, b, A.relu, A.f32out);
+        }
+        total += ksum;
+        if (A.scheme == ABED_IC) hit |= ksum != 0;  // channel k's sum moves, its dot does not
+      }
+    }
+    // block reductions: hit / differs (or), total (sum)
+    if (hit) sh_flag[0] = 1;
+    if (differs) sh_flag[1] = 1;
+    long long tsum = total;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) tsum += __shfl_xor_sync(0xffffffffu, tsum, o);
+    if ((threadIdx.x & 31) == 0) sh_red[threadIdx.x >> 5] = tsum;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      long long tot = 0;
+      for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) tot += sh_red[w];
+      bool detected;
+      if (A.scheme == ABED_FIC) {
+        detected = tot != 0;
+      } else if (A.scheme == ABED_FC && A.target == ABED_TARGET_INPUT) {
+        // per covering tap: the row sum moved by sh_tap[tap], the extra fmap by dx * fsum[c,r,s]
+        const int64_t w0 = flat % s.w, h0 = (flat / s.w) % s.h, c = (flat / (s.w * s.h)) % C;
+        const int8_t x0 = A.x[flat];
+        const long long dx = static_cast<long long>(static_cast<int8_t>(x0 ^ static_cast<int8_t>(1 << bit))) - x0;
+        detected = false;
+        for (int tap = 0; tap < static_cast<int>(R * S); ++tap) {
+          const int64_t r = tap / S, ss = tap - r * S;
+          const int64_t hp = h0 + s.pad_h - r, wp = w0 + s.pad_w - ss;
+          if (hp < 0 || wp < 0 || hp % s.stride_h || wp % s.stride_w || hp / s.stride_h >= P || wp / s.stride_w >= Q)
+            continue;
+          if (sh_tap[tap] != dx * static_cast<long long>(A.fsum[(c * R + r) * S + ss])) detected = true;
+        }
+      } else if (A.scheme == ABED_IC && A.target == ABED_TARGET_FILTER) {
+        // channel k: sum moved by tot, dot(flipped filter, ic) by df * ic[c,r,s]
+        const int64_t crs = flat % (C * R * S);
+        const int8_t f0 = A.f[flat];
+        const long long df = static_cast<long long>(static_cast<int8_t>(f0 ^ static_cast<int8_t>(1 << bit))) - f0;
+        detected = tot != df * static_cast<long long>(A.ic[crs]);
+      } else {
+        detected = sh_flag[0] != 0;
+      }
+      const int cls = detected ? (sh_flag[1] ? ABED_DETECTED : ABED_DETECTED_BENIGN)
+                               : (sh_flag[1] ? ABED_SDC : ABED_MASKED);  // faults.hpp:255-261
+      atomicAdd(A.counts + cls, 1ull);
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+// device-resident campaign: data, golden ConvOut, pristine checksums and every
+// trial's flip drawn once; runs are single launches over trial ranges
+struct abed_campaign {
+  abed_campaign_config cfg{};
+  int8_t* x = nullptr;
+  int8_t* f = nullptr;
+  int32_t* conv = nullptr;
+  int32_t* fsum = nullptr;
+  int32_t* ic = nullptr;
+  float* bias = nullptr;
+  int64_t* flat = nullptr;
+  int32_t* bit = nullptr;
+  unsigned long long* counts = nullptr;
+  ~abed_campaign() {
+    cudaFree(x); cudaFree(f); cudaFree(conv); cudaFree(fsum); cudaFree(ic); cudaFree(bias);
+    cudaFree(flat); cudaFree(bit); cudaFree(counts);
+  }
+};
+
+namespace {
+
+abed_campaign* campaign_create(const abed_campaign_config& cfg) {
+  if (cfg.trials < 1) throw_invalid("run_campaign: trials must be >= 1");
+  const abed_layer_shape& s = cfg.shape;
+  validate_shape(s);
+  scheme_checks(cfg.scheme);  // ICBatch is not an injection scheme
+  if (cfg.target < ABED_TARGET_INPUT || cfg.target > ABED_TARGET_CONVOUT) throw_invalid("run_campaign: bad target");
+  if (cfg.output_kind != ABED_I8 && cfg.output_kind != ABED_F32) throw_invalid("epilog: output kind must be i8 or f32");
+  if (!std::isfinite(cfg.scale)) throw_invalid("epilog: non-finite scale");
+  if (s.r * s.s > 64) throw_invalid("run_campaign: filters with more than 64 taps are not supported");
+  std::vector<float> hb((size_t)s.k, 0.0f);  // faults.hpp:167-168: empty bias -> zeros
+  if (cfg.bias_host && cfg.bias_len > 0) {
+    if (cfg.bias_len != s.k) throw_invalid("epilog: bias length must equal the channel count");
+    for (int64_t i = 0; i < s.k; ++i) {
+      if (!std::isfinite(cfg.bias_host[i])) throw_invalid("epilog: non-finite bias");
+      hb[(size_t)i] = cfg.bias_host[i];
+    }
+  }
+  auto* c = new abed_campaign();
+  c->cfg = cfg;
+  c->cfg.bias_host = nullptr;
+  try {
+    cudaStream_t st = nullptr;
+    const int64_t nchw = s.n * s.c * s.h * s.w, kcrs = s.k * s.c * s.r * s.s, crs = s.c * s.r * s.s;
+    const int64_t nkpq = s.n * s.k * s.p * s.q;
+    cuda_check(cudaMalloc(&c->x, (size_t)nchw), "cudaMalloc(x)");
+    cuda_check(cudaMalloc(&c->f, (size_t)kcrs), "cudaMalloc(f)");
+    cuda_check(cudaMalloc(&c->conv, (size_t)nkpq * 4), "cudaMalloc(conv)");
+    cuda_check(cudaMalloc(&c->fsum, (size_t)crs * 4), "cudaMalloc(fsum)");
+    cuda_check(cudaMalloc(&c->ic, (size_t)crs * 4), "cudaMalloc(ic)");
+    cuda_check(cudaMalloc(&c->bias, (size_t)s.k * 4), "cudaMalloc(bias)");
+    cuda_check(cudaMalloc(&c->flat, (size_t)cfg.trials * 8), "cudaMalloc(flat)");
+    cuda_check(cudaMalloc(&c->bit, (size_t)cfg.trials * 4), "cudaMalloc(bit)");
+    cuda_check(cudaMalloc(&c->counts, 4 * 8), "cudaMalloc(counts)");
+    cuda_check(cudaMemcpy(c->bias, hb.data(), hb.size() * 4, cudaMemcpyHostToDevice), "bias h2d");
+    if (cfg.mode == ABED_DATA_ONES) {  // faults.hpp:280-283
+      cuda_check(cudaMemset(c->x, 1, (size_t)nchw), "memset");
+      cuda_check(cudaMemset(c->f, 1, (size_t)kcrs), "memset");
+    } else {  // faults.hpp:284-288: one stream, input then filters
+      const uint64_t seed = derive(cfg.root_seed, 0x0DA7Au);
+      abed_fill_random_i8(c->x, nchw, seed, 0, st);
+      abed_fill_random_i8(c->f, kcrs, seed, (uint64_t)nchw, st);
+    }
+    tc_conv_nchw(s, c->x, c->f, c->conv, st);  // golden ConvOut on the tensor cores
+    dev_colsum_i8(c->f, s.k, crs, c->fsum, st);
+    dev_gen_input_checksum(c->x, s, c->ic, st);
+    std::vector<int64_t> hf((size_t)cfg.trials);
+    std::vector<int32_t> hbit((size_t)cfg.trials);
+    for (int64_t t = 0; t < cfg.trials; ++t) {  // faults.hpp:200-208, seeds derive_seed(root, t)
+      int b;
+      draw(derive(cfg.root_seed, (uint64_t)t), s, cfg.target, hf[(size_t)t], b);
+      hbit[(size_t)t] = b;
+    }
+    cuda_check(cudaMemcpy(c->flat, hf.data(), hf.size() * 8, cudaMemcpyHostToDevice), "flat h2d");
+    cuda_check(cudaMemcpy(c->bit, hbit.data(), hbit.size() * 4, cudaMemcpyHostToDevice), "bit h2d");
+    cuda_check(cudaDeviceSynchronize(), "campaign golden");
+  } catch (...) {
+    delete c;
+    throw;
+  }
+  return c;
+}
+
+void campaign_run(abed_campaign* c, int64_t t_begin, int64_t t_end, unsigned long long* counts, cudaStream_t st) {
+  if (t_begin < 0) t_begin = 0;
+  if (t_end > c->cfg.trials) t_end = c->cfg.trials;
+  const int64_t nt = t_end > t_begin ? t_end - t_begin : 0;
+  if (!nt) return;
+  BatchedCampaignArgs a{};
+  a.s = c->cfg.shape;
+  a.scheme = c->cfg.scheme;
+  a.target = c->cfg.target;
+  a.x = c->x; a.f = c->f; a.conv = c->conv; a.fsum = c->fsum; a.ic = c->ic; a.bias = c->bias;
+  a.scale = c->cfg.scale;
+  a.relu = c->cfg.activation == ABED_RELU ? 1 : 0;
+  a.f32out = c->cfg.output_kind == ABED_F32 ? 1 : 0;
+  a.flat = c->flat + t_begin;
+  a.bit = c->bit + t_begin;
+  a.n_trials = nt;
+  a.counts = counts;
+  const int64_t grid = nt < (int64_t)num_sms() * 8 ? nt : (int64_t)num_sms() * 8;
+  campaign_batched_kernel<<<(unsigned)grid, 256, 0, st>>>(a);
+  cuda_check(cudaGetLastError(), "campaign_batched");
+}
+
+void fill_report(const abed_campaign_config& cfg, int64_t nt, const unsigned long long* h, abed_campaign_report* rep) {
+  std::memset(rep, 0, sizeof(*rep));
+  rep->scheme = cfg.scheme; rep->target = cfg.target; rep->seed = cfg.root_seed; rep->trials = nt;
+  rep->detected = (int64_t)h[ABED_DETECTED];
+  rep->sdc = (int64_t)h[ABED_SDC];
+  rep->masked = (int64_t)h[ABED_MASKED];
+  rep->detected_benign = (int64_t)h[ABED_DETECTED_BENIGN];
+}
+
 }  // namespace
 
 #define GUARD(...)              \
@@ -347,6 +626,46 @@ int abed_run_campaign(const abed_campaign_config* cfg, int64_t t_begin, int64_t 
           default: ++rep->masked; break;
         }
       });
+}
+
+int abed_campaign_create(const abed_campaign_config* config, abed_campaign** campaign) {
+  GUARD(if (!config || !campaign) throw_invalid("campaign: null argument"); *campaign = campaign_create(*config));
+}
+
+int abed_campaign_destroy(abed_campaign* campaign) {
+  GUARD(delete campaign);
+}
+
+int abed_campaign_run(abed_campaign* campaign, int64_t trial_begin, int64_t trial_end, int64_t* counts_dev,
+                      void* stream) {
+  GUARD(if (!campaign || !counts_dev) throw_invalid("campaign: null argument");
+        campaign_run(campaign, trial_begin, trial_end, reinterpret_cast<unsigned long long*>(counts_dev),
+                     (cudaStream_t)stream));
+}
+
+int abed_campaign_report_of(const abed_campaign* campaign, const int64_t* counts_host, int64_t trials,
+                            abed_campaign_report* report) {
+  GUARD(if (!campaign || !counts_host || !report) throw_invalid("campaign: null argument");
+        fill_report(campaign->cfg, trials, reinterpret_cast<const unsigned long long*>(counts_host), report));
+}
+
+int abed_run_campaign_batched(const abed_campaign_config* cfg, int64_t t_begin, int64_t t_end,
+                              abed_campaign_report* rep) {
+  GUARD(
+      if (!cfg || !rep) throw_invalid("campaign: null argument");
+      abed_campaign* c = campaign_create(*cfg);
+      try {
+        cuda_check(cudaMemset(c->counts, 0, 32), "memset counts");
+        campaign_run(c, t_begin, t_end, c->counts, nullptr);
+        unsigned long long h[4];
+        cuda_check(cudaMemcpy(h, c->counts, 32, cudaMemcpyDeviceToHost), "counts d2h");
+        const int64_t b = t_begin < 0 ? 0 : t_begin, e = t_end > cfg->trials ? cfg->trials : t_end;
+        fill_report(*cfg, e > b ? e - b : 0, h, rep);
+      } catch (...) {
+        delete c;
+        throw;
+      }
+      delete c);
 }
 
 }  // extern "C"

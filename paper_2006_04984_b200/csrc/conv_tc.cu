@@ -4,16 +4,18 @@
 #include "conv_tc_kernel.cuh"
 
 namespace abed_host {
-#define ABED_EXTERN_EPI(DT, EPI) \
-  extern template cudaError_t launch_epi<DT, EPI>(const ConvTcParams&, int, bool, cudaStream_t);
-#define ABED_EXTERN_DT(DT)                 \
-  ABED_EXTERN_EPI(DT, abed_dev::EPI_NONE)  \
-  ABED_EXTERN_EPI(DT, abed_dev::EPI_NCHW)  \
-  ABED_EXTERN_EPI(DT, abed_dev::EPI_PACKED) \
-  ABED_EXTERN_EPI(DT, abed_dev::EPI_COMPARE)
-ABED_EXTERN_DT(abed_dev::DT_I8)
-ABED_EXTERN_DT(abed_dev::DT_F16)
-ABED_EXTERN_DT(abed_dev::DT_BF16)
+#define ABED_EXTERN_EPI(DT, EPI, XT) \
+  extern template cudaError_t launch_epi<DT, EPI, XT>(const ConvTcParams&, int, bool, cudaStream_t);
+#define ABED_EXTERN_DT(DT, XT)                 \
+  ABED_EXTERN_EPI(DT, abed_dev::EPI_NONE, XT)  \
+  ABED_EXTERN_EPI(DT, abed_dev::EPI_NCHW, XT)  \
+  ABED_EXTERN_EPI(DT, abed_dev::EPI_PACKED, XT) \
+  ABED_EXTERN_EPI(DT, abed_dev::EPI_COMPARE, XT)
+ABED_EXTERN_DT(abed_dev::DT_I8, 0)
+ABED_EXTERN_DT(abed_dev::DT_I8, 1)
+ABED_EXTERN_DT(abed_dev::DT_I8, 2)
+ABED_EXTERN_DT(abed_dev::DT_F16, 0)
+ABED_EXTERN_DT(abed_dev::DT_BF16, 0)
 }  // namespace abed_host
 
 namespace abed_dev {
@@ -40,8 +42,18 @@ __global__ void __launch_bounds__(256) verdict_kernel(const __grid_constant__ Ve
     const int64_t HlWl = static_cast<int64_t>(j.Hl) * j.Wl;
     const int64_t PQ = static_cast<int64_t>(j.P) * j.Q;
     const int64_t stride = static_cast<int64_t>(j.m_tiles) * kBlockM * 2;
-    for (int mt = 0; mt < j.m_tiles; ++mt) {
-      if (j.tile_flag[mt] != j.fc_epoch) continue;  // not raised by the last run
+    // flags of the last run, one per (N tile, M tile, lane quarter), read by all
+    // threads in parallel into a count of raised M tiles (usually zero: the
+    // serial per-tile recheck below then costs nothing)
+    const int64_t nflags = static_cast<int64_t>(j.n_tiles) * j.m_tiles * 4;
+    int any = 0;
+    for (int64_t i = t; i < nflags; i += blockDim.x) any |= __ldcg(j.tile_flag + i) != 0u;
+    const bool some_raised = __syncthreads_or(any) != 0;
+    for (int mt = 0; some_raised && mt < j.m_tiles; ++mt) {
+      unsigned raised = 0;
+      for (int i = 0; i < j.n_tiles * 4; ++i)
+        raised |= j.tile_flag[(static_cast<int64_t>(i >> 2) * j.m_tiles + mt) * 4 + (i & 3)];
+      if (!raised) continue;
       for (int r = t; r < kBlockM; r += blockDim.x) {
         const int64_t m = static_cast<int64_t>(mt) * kBlockM + r;
         if (m >= j.m_total) continue;
@@ -270,15 +282,15 @@ int conv_tc_grid(const ConvTcParams& p, int num_sms) {
   return grid;
 }
 
-template <int DT>
+template <int DT, int XT>
 static cudaError_t launch_dt(const ConvTcParams& p, int grid, bool pdl, cudaStream_t stream) {
   switch (p.out_mode) {
-    case abed_dev::OUT_NONE: return launch_epi<DT, abed_dev::EPI_NONE>(p, grid, pdl, stream);
+    case abed_dev::OUT_NONE: return launch_epi<DT, abed_dev::EPI_NONE, XT>(p, grid, pdl, stream);
     case abed_dev::OUT_I8_PACKED:
-    case abed_dev::OUT_H_PACKED: return launch_epi<DT, abed_dev::EPI_PACKED>(p, grid, pdl, stream);
+    case abed_dev::OUT_H_PACKED: return launch_epi<DT, abed_dev::EPI_PACKED, XT>(p, grid, pdl, stream);
     case abed_dev::OUT_I8_COMPARE:
-    case abed_dev::OUT_H_COMPARE: return launch_epi<DT, abed_dev::EPI_COMPARE>(p, grid, pdl, stream);
-    default: return launch_epi<DT, abed_dev::EPI_NCHW>(p, grid, pdl, stream);
+    case abed_dev::OUT_H_COMPARE: return launch_epi<DT, abed_dev::EPI_COMPARE, XT>(p, grid, pdl, stream);
+    default: return launch_epi<DT, abed_dev::EPI_NCHW, XT>(p, grid, pdl, stream);
   }
 }
 
@@ -327,9 +339,12 @@ cudaError_t conv_tc_launch(const ConvTcParams& p_in, int num_sms, bool pdl, cuda
   }
   const int grid = p.conv_grid + p.ic_ctas;
   switch (p.dtype) {
-    case abed_dev::DT_F16: return launch_dt<abed_dev::DT_F16>(p, grid, pdl, stream);
-    case abed_dev::DT_BF16: return launch_dt<abed_dev::DT_BF16>(p, grid, pdl, stream);
-    default: return launch_dt<abed_dev::DT_I8>(p, grid, pdl, stream);
+    case abed_dev::DT_F16: return launch_dt<abed_dev::DT_F16, 0>(p, grid, pdl, stream);
+    case abed_dev::DT_BF16: return launch_dt<abed_dev::DT_BF16, 0>(p, grid, pdl, stream);
+    default:
+      if (p.check & abed_dev::CHECK_IC) return launch_dt<abed_dev::DT_I8, 1>(p, grid, pdl, stream);
+      if (p.icb_d) return launch_dt<abed_dev::DT_I8, 2>(p, grid, pdl, stream);
+      return launch_dt<abed_dev::DT_I8, 0>(p, grid, pdl, stream);
   }
 }
 

@@ -109,7 +109,7 @@ struct ConvTcParams {
   // finish reduces the per-CTA records and writes the reference VerifyOutcomes)
   int check;
   int64_t* fc_part;            // [n_tiles][m_tiles*128][2] {sum_k, extra} row partials (n_tiles > 1)
-  unsigned int* tile_sem;      // [m_tiles] FC flags (several N tiles): fc_epoch where a row failed its tile check
+  unsigned int* tile_sem;      // FC, several N tiles: int8 [n_tiles][m_tiles][4] flags (a row failed its tile check); float [m_tiles] counters
   int64_t* cta_rec;            // [gridDim][kCtaRec] per-CTA {FC count, first key, lhs, rhs, FIC lhs, FIC rhs}
   unsigned long long* kacc;    // [0] FIC lhs, [1] FIC rhs (in-kernel), [2] CTA done ticket
   unsigned long long* rhs_ext;  // FIC rhs of the pristine input: read (rhs_mode 0) or stored (rhs_mode 1)
@@ -120,7 +120,6 @@ struct ConvTcParams {
                                //    (ic_S; FIC's rhs then comes from ic at the verdict)
   int rhs_nsplit;              // image split of the rhs work items
   int rhs_deep;                // int8 FR: 16 image loads in flight per item (large inputs) instead of 8
-  unsigned fc_epoch;           // FC, several N tiles: value a CTA writes into its M tile's flag
   int conv_grid;               // CTAs running conv work units (blockIdx < conv_grid)
   int ic_ctas;                 // extra CTAs (blockIdx >= conv_grid) that only compute the FR
                                // input checksum on SMs the conv grid leaves idle (0: the conv
@@ -200,7 +199,6 @@ struct VerdictJob {
   // the per-M-tile flags the conv CTAs raise (consumed and reset here)
   const int64_t* fc_part;
   unsigned* tile_flag;
-  unsigned fc_epoch;   // flags equal to the last run's epoch are this run's
   int n_tiles, m_tiles, Hl, Wl;
   int64_t m_total;
   double tau_fc;

@@ -326,8 +326,8 @@ __device__ __forceinline__ int64_t epi_chunk(const ConvTcParams& p, const EpiCtx
       for (int j = 0; j < 16; ++j) sum += a[j];
     }
   }
-  if (XTRA == 1 || (SLOW && (p.check & CHECK_IC))) ic_chunk_sums(p, e.ic_acc, e.valid, a, k0);
-  if (XTRA == 2 || (SLOW && p.icb_d)) icb_chunk<SLOW>(p, e, a, k0);
+  if (XTRA == 1) ic_chunk_sums(p, e.ic_acc, e.valid, a, k0);
+  if (XTRA == 2) icb_chunk<SLOW>(p, e, a, k0);
   if (EPI == EPI_PACKED || EPI == EPI_COMPARE) {
     int32_t y[16];
     if (p.dbg & 16) {  // timing experiment: skip the requantise math
@@ -997,7 +997,7 @@ enum MmaPattern : int {
   PAT_1x1_S1_G4 = 5, PAT_1x1_S1_G2 = 6, PAT_1x1_S2_G4 = 7, PAT_1x1_S2_G2 = 8,
 };
 
-template <int DT, int EPI, bool FC, bool FIC>
+template <int DT, int EPI, bool FC, bool FIC, int XT>
 __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __grid_constant__ ConvTcParams p) {
   using Acc = std::conditional_t<DT == DT_I8, int64_t, double>;  // exact int / f64 float-mode sums
   extern __shared__ __align__(128) uint8_t smem[];
@@ -1029,13 +1029,13 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
     long long acc = 0;
     double facc_rhs = 0.0;
     pdl_wait();
-    if (DT == DT_I8 && p.icb_d) {
+    if (DT == DT_I8 && XT == 2 && p.icb_d) {
       const int64_t writers = static_cast<int64_t>(p.conv_grid) * (kRhsWarps * 32) +
                               static_cast<int64_t>(p.ic_ctas) * kConvThreads;
       icb_write_digits(p, static_cast<int64_t>(p.conv_grid) * (kRhsWarps * 32) +
                               static_cast<int64_t>(blockIdx.x - p.conv_grid) * kConvThreads + threadIdx.x, writers);
     }
-    if (DT == DT_I8 && p.rhs_mode == 4)
+    if (DT == DT_I8 && XT == 1 && p.rhs_mode == 4)
       ic_class_sums_fr(p, static_cast<int64_t>(blockIdx.x - p.conv_grid) * kConvThreads + threadIdx.x,
                        static_cast<int64_t>(p.ic_ctas) * kConvThreads);
     if (FIC && p.rhs_mode == 1)
@@ -1096,7 +1096,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
   }
   __shared__ int s_fr_claim;
   __shared__ long long s_rhs_all[kConvThreads / 32];
-  unsigned long long* const s_ic = p.ic_smem ? reinterpret_cast<unsigned long long*>(smem + L.ic_off) : nullptr;
+  unsigned long long* const s_ic = (XT == 1 && p.ic_smem) ? reinterpret_cast<unsigned long long*>(smem + L.ic_off) : nullptr;
   if (s_ic)
     for (int i = threadIdx.x; i < p.K; i += kConvThreads) s_ic[i] = 0ull;
   if (threadIdx.x == 0) s_fr_claim = 0;
@@ -1170,7 +1170,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
         int mt, nt;
         decode_tile(p, u, mt, nt);
         const int64_t m0 = static_cast<int64_t>(mt) * kBlockM;
-        if (DT == DT_I8 && p.icb_d && !icb_seen && m0 + p.strip_pix > p.m_real) {
+        if (DT == DT_I8 && XT == 2 && p.icb_d && !icb_seen && m0 + p.strip_pix > p.m_real) {
           icb_wait_ready(p);  // this tile's strips reach the ICBatch digit images
           icb_seen = true;
         }
@@ -1298,7 +1298,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
       }
       e.icb_lhs = nullptr;
       e.icb_dig = nullptr;
-      if (DT == DT_I8 && p.icb_d && valid) {
+      if (DT == DT_I8 && XT == 2 && p.icb_d && valid) {
         const int64_t kq = static_cast<int64_t>(pp) * p.Q + qq;
         if (n_img >= static_cast<uint32_t>(p.N)) {  // ICBatch digit row: no output, no FC / FIC
           e.icb_dig = p.icb_dig + static_cast<int64_t>(n_img - p.N) * p.K * e.PQ + kq;
@@ -1357,15 +1357,17 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
       // fast path: no fault hook, no filler channels, no IC column sums (warp-uniform)
       const bool slow = p.fault_key >= 0 || k_base + c_hi * 16 > p.K;
       // IC column sums / ICBatch batch sums on the fast path (int8 plans only)
-      const int xtra = DT != DT_I8 ? 0 : (p.check & CHECK_IC) ? 1 : (p.icb_d ? 2 : 0);
+      constexpr int xtra = DT != DT_I8 ? 0 : XT;
       Acc row_sum = 0;
-      if (p.dbg & 1) {
-      } else if (!slow && xtra == 1) {
-        row_sum = p.relu ? epi_columns<DT, EPI, true, FC || FIC, false, false, 1>(p, e, t_row, k_base, c_lo, c_hi, af_sum)
-                         : epi_columns<DT, EPI, false, FC || FIC, false, false, 1>(p, e, t_row, k_base, c_lo, c_hi, af_sum);
-      } else if (!slow && xtra == 2) {
-        row_sum = p.relu ? epi_columns<DT, EPI, true, FC || FIC, false, false, 2>(p, e, t_row, k_base, c_lo, c_hi, af_sum)
-                         : epi_columns<DT, EPI, false, FC || FIC, false, false, 2>(p, e, t_row, k_base, c_lo, c_hi, af_sum);
+      if constexpr (xtra != 0) {
+        // IC / ICBatch plans (their own kernel instances)
+        if (!slow)
+          row_sum = p.relu ? epi_columns<DT, EPI, true, FC || FIC, false, false, xtra>(p, e, t_row, k_base, c_lo, c_hi, af_sum)
+                           : epi_columns<DT, EPI, false, FC || FIC, false, false, xtra>(p, e, t_row, k_base, c_lo, c_hi, af_sum);
+        else
+          row_sum = p.relu ? epi_columns<DT, EPI, true, FC || FIC, true, false, xtra>(p, e, t_row, k_base, c_lo, c_hi, af_sum)
+                           : epi_columns<DT, EPI, false, FC || FIC, true, false, xtra>(p, e, t_row, k_base, c_lo, c_hi, af_sum);
+      } else if (p.dbg & 1) {
       } else if (!slow) {
         if (p.dbg & 64)
           row_sum = epi_columns<DT, EPI, true, false, false>(p, e, t_row, k_base, c_lo, c_hi, af_sum);
@@ -1421,8 +1423,11 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
             part[0] = acc_bits(row_sum);
             part[1] = acc_bits(extra);
             if constexpr (DT == DT_I8) {
+              // every (N tile, M tile, lane quarter) flag is overwritten by every
+              // run, so a replayed graph never sees a stale flag
               const bool bad = valid && row_sum != extra;
-              if (__any_sync(0xffffffffu, bad) && lane == 0) p.tile_sem[mt] = p.fc_epoch;
+              const unsigned any = __any_sync(0xffffffffu, bad) ? 1u : 0u;
+              if (lane == 0) p.tile_sem[(static_cast<int64_t>(nt) * p.m_tiles + mt) * 4 + quarter] = any;
             } else {
               // float mode: per-tile differences may add up across tiles, so the
               // full-channel check stays in-kernel -- the CTA completing the M
@@ -1490,7 +1495,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
     const int rw = warp - (2 + kEpiWarps);
     long long acc = 0;
     double facc_rhs = 0.0;
-    if (DT == DT_I8 && p.icb_d) {
+    if (DT == DT_I8 && XT == 2 && p.icb_d) {
       // ICBatch digit images first: the producers of the last tiles wait for them
       pdl_wait();
       icb_write_digits(p, static_cast<int64_t>(blockIdx.x) * (kRhsWarps * 32) + rw * 32 + lane,
@@ -1615,7 +1620,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
           }
         }
       }
-    } else if (DT == DT_I8 && p.rhs_mode == 4 && p.ic_ctas == 0) {
+    } else if (DT == DT_I8 && XT == 1 && p.rhs_mode == 4 && p.ic_ctas == 0) {
       // IC input checksum (class sums) by the two input-checksum warps
       pdl_wait();
       ic_class_sums_fr(p, static_cast<int64_t>(blockIdx.x) * (kRhsWarps * 32) + rw * 32 + lane,
@@ -1719,14 +1724,17 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
 namespace abed_host {
 using abed_dev::ConvTcParams;
 inline uint32_t conv_tc_smem_bytes_inl(const ConvTcParams& p) { return abed_dev::smem_layout(p).total; }
-template <int DT, int EPI, bool FC, bool FIC>
+template <int DT, int EPI, bool FC, bool FIC, int XT>
 cudaError_t launch_variant(const ConvTcParams& p, int grid, bool pdl, cudaStream_t stream) {
-  static bool attr_done = false;
-  auto kern = abed_dev::conv_i8_tc_kernel<DT, EPI, FC, FIC>;
-  if (!attr_done) {
+  // the smem opt-in is per device: one flag per ordinal
+  static bool attr_done[64] = {};
+  auto kern = abed_dev::conv_i8_tc_kernel<DT, EPI, FC, FIC, XT>;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64 || !attr_done[dev]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, abed_dev::kConvDynSmemMax);
     if (e != cudaSuccess) return e;
-    attr_done = true;
+    if (dev >= 0 && dev < 64) attr_done[dev] = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -1741,13 +1749,16 @@ cudaError_t launch_variant(const ConvTcParams& p, int grid, bool pdl, cudaStream
   return cudaLaunchKernelEx(&cfg, kern, p);
 }
 
-template <int DT, int EPI>
+// XT: 0 = no per-channel extras, 1 = IC column sums, 2 = ICBatch batch sums
+// (int8 only; separate kernel instances so the FC / FIC / unprotected kernels
+// carry none of their code or registers)
+template <int DT, int EPI, int XT>
 cudaError_t launch_epi(const ConvTcParams& p, int grid, bool pdl, cudaStream_t st) {
   const bool fc = (p.check & abed_dev::CHECK_FC) != 0, fic = (p.check & abed_dev::CHECK_FIC) != 0;
-  if (fc && fic) return launch_variant<DT, EPI, true, true>(p, grid, pdl, st);
-  if (fc) return launch_variant<DT, EPI, true, false>(p, grid, pdl, st);
-  if (fic) return launch_variant<DT, EPI, false, true>(p, grid, pdl, st);
-  return launch_variant<DT, EPI, false, false>(p, grid, pdl, st);
+  if (fc && fic) return launch_variant<DT, EPI, true, true, XT>(p, grid, pdl, st);
+  if (fc) return launch_variant<DT, EPI, true, false, XT>(p, grid, pdl, st);
+  if (fic) return launch_variant<DT, EPI, false, true, XT>(p, grid, pdl, st);
+  return launch_variant<DT, EPI, false, false, XT>(p, grid, pdl, st);
 }
 
 }  // namespace abed_host

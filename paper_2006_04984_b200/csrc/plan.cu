@@ -177,15 +177,20 @@ __global__ void __launch_bounds__(256) pack_input_v4_kernel(const int8_t* __rest
         for (int e = 0; e < 16; ++e) {
           const int ce = min(grp * 16 + e, g.c - 1);
           al[e] = ((int64_t)n * g.c + ce) * HW + (int64_t)hh * g.w + ww0;
+          // clamp into the aligned words that overlap [0, x_bytes): an aligned word
+          // holding a valid byte never crosses a page, and the bytes past the end
+          // are masked by `keep`
           const int64_t a = al[e] & ~int64_t(3);
-          const int64_t a0 = a < 0 ? 0 : a, a1 = a + 4 > x_bytes - 4 ? x_bytes - 4 : a + 4;
+          const int64_t lim = (x_bytes - 1) & ~int64_t(3);
+          const int64_t a0 = a < 0 ? 0 : (a > lim ? lim : a);
+          const int64_t a1 = a + 4 > lim ? lim : (a + 4 < 0 ? 0 : a + 4);
           lo[e] = __ldg(reinterpret_cast<const uint32_t*>(x + a0));
           hi[e] = __ldg(reinterpret_cast<const uint32_t*>(x + a1));
         }
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
           const int64_t a = al[e] & ~int64_t(3);
-          const uint32_t l = a >= 0 ? lo[e] : 0u, h = a + 4 < x_bytes ? hi[e] : 0u;
+          const uint32_t l = (a >= 0 && a < x_bytes) ? lo[e] : 0u, h = a + 4 < x_bytes ? hi[e] : 0u;
           const uint32_t v = __funnelshift_r(l, h, (uint32_t)(al[e] & 3) * 8) & keep;
           cw[e] = grp * 16 + e < g.c ? v : 0u;
         }
@@ -704,15 +709,18 @@ void ic_finalize_launch(const unsigned long long* ksum, const int8_t* f, const i
 // ---------------------------------------------------------------------------
 // plan construction
 // ---------------------------------------------------------------------------
-static int g_num_sms = 0;
+// SM count of the CURRENT device (cached per ordinal: one process may drive several GPUs)
+static int g_num_sms[64] = {};
 int num_sms() {
-  if (g_num_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_num_sms <= 0) g_num_sms = 148;
-  }
-  return g_num_sms;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int* slot = (dev >= 0 && dev < 64) ? &g_num_sms[dev] : nullptr;
+  if (slot && *slot > 0) return *slot;
+  int n = 0;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  if (n <= 0) n = 148;
+  if (slot) *slot = n;
+  return n;
 }
 
 // compile-time unrolled MMA issue routine for this geometry (conv_tc.cu MmaPattern)

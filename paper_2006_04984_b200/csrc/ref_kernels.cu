@@ -529,11 +529,13 @@ void dev_colsum_i8(const int8_t* x, int64_t rows, int64_t len, int32_t* out, cud
     if (cs > 16) cs = 16;
     if (cs < 1) cs = 1;
     const int64_t rows_per = (rows + cs - 1) / cs;
-    static bool attr = false;
-    if (!attr) {
+    static bool attr[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64 || !attr[dev]) {
       cuda_check(cudaFuncSetAttribute(colsum_i8_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
                  "colsum cluster attr");
-      attr = true;
+      if (dev >= 0 && dev < 64) attr[dev] = true;
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(col_tiles * cs));
