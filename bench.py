@@ -686,6 +686,78 @@ def measure_abft_gemm(dev, stream, flush):
             "gemms": out}
 
 
+def measure_campaign_cfg5(args, dev, world, rank, dist):
+    """BASELINE configs[4]'s fault-injection campaign: ResNet-50 layer1.0.conv2
+    (64 -> 64, 3x3, 56x56) at batch 1024, the batch sharded over the ranks
+    (1024 / N images each, generated from the same SplitMix64 stream as the whole
+    batch).  Every rank evaluates every trial on its shard with the trial-parallel
+    kernel (one CTA per trial: the flip's perturbed ConvOut elements against the
+    golden ConvOut), writing per-trial records {check failed, output differs, sum
+    delta}; ONE NCCL all-reduce (sum) of the records over NVLink, then a classify
+    launch gives the campaign report -- identical for every N.  Timed on the device
+    (CUDA events, max over ranks), golden ConvOut excluded (created once).  Rank 0
+    also re-runs a few trials through the exhaustive path (one fused protected conv
+    of the whole batch per trial) as a cross-check."""
+    import torch
+
+    from paper_2006_04984_b200 import abi, api
+
+    n_glob = 1024
+    ls = api.layer_shape(n_glob, 64, 56, 56, 64, 3, 3, 1, 1, 1, 1)
+    n0, n1 = n_glob * rank // world, n_glob * (rank + 1) // world
+    trials = args.campaign_trials
+    out = {"layer": "resnet50 layer1.0.conv2 64x56x56 -> 64, 3x3 p1, batch 1024 (random int8 data)",
+           "images_per_rank": n1 - n0, "trials": trials, "reduction": "NCCL all_reduce(sum) of int64 [trials, 3] records"
+           if world > 1 else "none (1 GPU)", "schemes": {}}
+    for name, scheme, target, seed in [("fic_input", abi.FIC, abi.TARGET_INPUT, 0xD1),
+                                       ("fic_filter", abi.FIC, abi.TARGET_FILTER, 0xD2),
+                                       ("fic_convout", abi.FIC, abi.TARGET_CONVOUT, 0xD3),
+                                       ("fc_filter", abi.FC, abi.TARGET_FILTER, 0xD4)]:
+        camp = api.Campaign(ls, scheme, target, trials, seed, mode=abi.DATA_RANDOM_I8, images=(n0, n1))
+        rec = torch.zeros(trials, 3, dtype=torch.int64, device=dev)
+        cnt = torch.zeros(4, dtype=torch.int64, device=dev)
+        camp.run_records(rec)  # warm-up
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        rec.zero_()
+        cnt.zero_()
+        camp.run_records(rec)
+        if dist:
+            dist.all_reduce(rec)
+        camp.classify(rec, cnt)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        if dist:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = t.item()
+        c = cnt.tolist()
+        out["schemes"][name] = {"detected": c[abi.DETECTED], "detected_benign": c[abi.DETECTED_BENIGN],
+                                "sdc": c[abi.SDC], "masked": c[abi.MASKED],
+                                "coverage": round((c[abi.DETECTED] + c[abi.DETECTED_BENIGN]) / trials, 4),
+                                "ms": round(ms, 3), "trials_per_s": round(trials / (ms * 1e-3), 1)}
+        del camp
+    if rank == 0:
+        # exhaustive cross-check: the first few trials through the fused protected
+        # conv of the whole batch per trial, against the trial-parallel kernel
+        xc = {}
+        for name, scheme, target, seed in [("fic_input", abi.FIC, abi.TARGET_INPUT, 0xD1),
+                                           ("fic_filter", abi.FIC, abi.TARGET_FILTER, 0xD2)]:
+            k = 8
+            a = api.run_campaign(ls, scheme, target, trials, seed, mode=abi.DATA_RANDOM_I8, begin=0, end=k)
+            b = api.run_campaign(ls, scheme, target, trials, seed, mode=abi.DATA_RANDOM_I8, begin=0, end=k,
+                                 batched=True)
+            xc[name] = {"trials": k, "exhaustive": list(a.astuple()), "batched": list(b.astuple()),
+                        "equal": a.astuple() == b.astuple()}
+        out["exhaustive_crosscheck"] = xc
+    torch.cuda.synchronize()
+    return out
+
+
 def run_ours(args, world, rank, local):
     import ctypes as C
 
@@ -763,12 +835,12 @@ def run_ours(args, world, rank, local):
             shards[variant].record()
 
     # kernels of this library per step: conv per layer, + ICBatch scan per layer,
-    # + IC input-checksum pair per layer and IC verdict per layer, + one verdict
-    # launch (+ with several ranks the verdict-record kernel in the graph and the fold
+    # + one verdict launch (IC: the two batched IC-verdict launches instead)
+    # (+ with several ranks the verdict-record kernel in the graph and the fold
     # kernel after the all-gather)
     xr = 2 if world > 1 else 0
     launches_per_step = {"unprotected": 16, "dup": 32, "fc": 17 + xr, "fic": 17 + xr, "fic_sm": 17 + xr,
-                         "ic": 65 + xr, "icbatch": 33 + xr}
+                         "ic": 18 + xr, "icbatch": 33 + xr}
 
     # warm up eagerly (sets kernel attributes), then capture each variant as one graph
     with torch.cuda.stream(stream):
@@ -877,6 +949,7 @@ def run_ours(args, world, rank, local):
 
     conv_ms = per_layer_ms("fic")
     unprot_ms = per_layer_ms("unprotected")
+    staged_ms = per_layer_ms("fic_sm")
     conv_tops = total_ops(rb) / (sum(conv_ms) * 1e-3) / 1e12
     # denominator: the tcgen05 kind::i8 dense peak MEASURED in this run on this device
     # (all SMs issuing back-to-back M128 N256 K32 MMAs, CUDA events; abed_probe_mma_i8_peak)
@@ -903,6 +976,7 @@ def run_ours(args, world, rank, local):
                 "conv_share_of_step": round(sum(conv_ms) / res["fic"]["ms"], 3),
                 "per_layer_conv_us": [round(t * 1e3, 2) for t in conv_ms],
                 "per_layer_unprotected_us": [round(t * 1e3, 2) for t in unprot_ms],
+                "per_layer_fic_staged_us": [round(t * 1e3, 2) for t in staged_ms],
                 "timing": f"per layer: graph of {R} back-to-back launches after an L2 flush, CUDA events / {R}"}
 
     # ------------------------------------------------ e2e through the C ABI with host buffers
@@ -999,6 +1073,8 @@ def run_ours(args, world, rank, local):
         det[name] = {"detected": c[0], "detected_benign": c[1], "sdc": c[2], "masked": c[3],
                      "coverage": round((c[0] + c[1]) / trials, 4)}
 
+    camp5 = None if args.skip_campaign5 else measure_campaign_cfg5(args, dev, world, rank, dist)
+
     if rank != 0:
         if dist:
             dist.destroy_process_group()
@@ -1053,6 +1129,7 @@ def run_ours(args, world, rank, local):
         "hbm_kernels": hbm,
         "resnet50_network_int8": r50,
         "abft_gemm_int8": abft,
+        "cfg5_campaign_b1024": camp5,
     }
     print(json.dumps(line), flush=True)
     if dist:
@@ -1073,6 +1150,8 @@ def main():
     ap.add_argument("--skip-mbv2", action="store_true", help="skip the MobileNetV2 INT8 block (BASELINE configs[3])")
     ap.add_argument("--skip-r50net", action="store_true", help="skip the whole-network ResNet-50 INT8 block")
     ap.add_argument("--skip-abft", action="store_true", help="skip the ABFT-GEMM comparison block")
+    ap.add_argument("--skip-campaign5", action="store_true",
+                    help="skip the batch-1024 batch-sharded fault campaign (BASELINE configs[4])")
     ap.add_argument("--global-batch", type=int, default=0,
                     help="shard this fixed ResNet-50 batch over the GPUs (BASELINE configs[4]: 1024); default 32 per GPU")
     args = ap.parse_args()

@@ -252,6 +252,19 @@ int abed_campaign_run(abed_campaign* campaign, int64_t trial_begin, int64_t tria
                       void* stream);
 int abed_campaign_report_of(const abed_campaign* campaign, const int64_t* counts_host, int64_t trials,
                             abed_campaign_report* report);
+/* Batch-sharded form (configs[4]: one rank per GPU owns images [image_begin,
+ * image_end) of config->shape's batch; trials are drawn over the WHOLE tensors,
+ * so every rank sees every trial).  run_records writes per trial
+ * {row/channel check failed, output differs, sum delta} of this shard into
+ * records_dev[3 * (t - trial_begin) ...]; summing the records of all shards
+ * (one NCCL all-reduce) and classify give the single-GPU report exactly
+ * (classify ADDS into counts_dev[4]). */
+int abed_campaign_create_shard(const abed_campaign_config* config, int64_t image_begin, int64_t image_end,
+                               abed_campaign** campaign);
+int abed_campaign_run_records(abed_campaign* campaign, int64_t trial_begin, int64_t trial_end, int64_t* records_dev,
+                              void* stream);
+int abed_campaign_classify(const abed_campaign* campaign, const int64_t* records_dev, int64_t n_records,
+                           int64_t* counts_dev, void* stream);
 int abed_campaign_destroy(abed_campaign* campaign);
 
 /* ------------------------------------------------------------ protected conv (hot path)

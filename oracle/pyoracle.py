@@ -354,6 +354,33 @@ class Oracle:
         fn(ptr(np.ascontiguousarray(x, np.float32)), C.byref(ls), ptr(out))
         return out
 
+    def fc_verify_f32(self, convout, extra, tau):
+        """checksum.hpp:541-565 (C restatement: the 'ora' build)."""
+        assert self.which == "ora", "fc_verify_f32 is bound from the C restatement"
+        convout = np.ascontiguousarray(convout, np.float32)
+        o = VerifyOutcome()
+        fn = self._f("fc_verify_f32")
+        fn.argtypes = [P, Dims4, P, C.c_double, C.POINTER(VerifyOutcome)]
+        self._chk(fn(ptr(convout), dims(convout.shape), ptr(np.ascontiguousarray(extra, np.float32)), tau, C.byref(o)))
+        return o
+
+    def fic_verify_f32(self, convout, expected, tau):
+        """checksum.hpp:537-539 (C restatement: the 'ora' build)."""
+        assert self.which == "ora", "fic_verify_f32 is bound from the C restatement"
+        convout = np.ascontiguousarray(convout, np.float32)
+        o = VerifyOutcome()
+        fn = self._f("fic_verify_f32")
+        fn.argtypes = [P, C.c_int64, C.c_double, C.c_double, C.POINTER(VerifyOutcome)]
+        self._chk(fn(ptr(convout), convout.size, expected, tau, C.byref(o)))
+        return o
+
+    def fic_dot_f64(self, a, b):
+        """checksum.hpp:530-535 (acc = fma(a, b, acc), the reference's contracted loop)."""
+        fn = self._f("fic_dot_f64", C.c_double)
+        fn.argtypes = [P, P, C.c_int64]
+        a = np.ascontiguousarray(a, np.float64)
+        return fn(ptr(a), ptr(np.ascontiguousarray(b, np.float64)), a.size)
+
     def fused_conv_epilog(self, x, f, ls, scale, bias, relu=True, out_f32=False, checksum=False, next_ls=None):
         out = np.empty(ls.output_dims(), np.float32 if out_f32 else np.int8)
         cs = C.c_int64()

@@ -176,6 +176,9 @@ SIGNATURES = {
     "abed_campaign_run": (C.c_int, [P, i64, i64, P, P]),
     "abed_campaign_report_of": (C.c_int, [P, C.POINTER(i64), i64, C.POINTER(CampaignReport)]),
     "abed_campaign_destroy": (C.c_int, [P]),
+    "abed_campaign_create_shard": (C.c_int, [C.POINTER(CampaignConfig), i64, i64, C.POINTER(P)]),
+    "abed_campaign_run_records": (C.c_int, [P, i64, i64, P, P]),
+    "abed_campaign_classify": (C.c_int, [P, P, i64, P, P]),
     "abed_conv_plan_create": (C.c_int, [SHP, P, i32, i32, C.POINTER(P)]),
     "abed_conv_plan_destroy": (C.c_int, [P]),
     "abed_conv_plan_info": (C.c_int, [P, C.POINTER(PlanInfo)]),

@@ -330,14 +330,27 @@ class Campaign:
     (detected, sdc, masked, detected_benign) with one launch."""
 
     def __init__(self, ls, scheme, target, trials=1000, root_seed=1, mode=abi.DATA_ONES, scale=0.05, bias=None,
-                 relu=True, output_kind=I8):
+                 relu=True, output_kind=I8, images=None):
+        """images=(begin, end): this process's batch shard (per-trial records instead of counts)."""
         self.cfg = campaign_config(ls, scheme, target, trials, root_seed, mode, scale, bias, relu, output_kind)
         self.handle = C.c_void_p()
-        call("abed_campaign_create", C.byref(self.cfg), C.byref(self.handle))
+        if images is None:
+            call("abed_campaign_create", C.byref(self.cfg), C.byref(self.handle))
+        else:
+            call("abed_campaign_create_shard", C.byref(self.cfg), images[0], images[1], C.byref(self.handle))
 
     def run(self, counts: torch.Tensor, begin=0, end=None, stream=None):
         call("abed_campaign_run", self.handle, begin, self.cfg.trials if end is None else end, _p(counts),
              stream or _stream())
+
+    def run_records(self, records: torch.Tensor, begin=0, end=None, stream=None):
+        """records: int64 [end - begin, 3] per-trial {check failed, output differs, sum delta} of this shard."""
+        call("abed_campaign_run_records", self.handle, begin, self.cfg.trials if end is None else end, _p(records),
+             stream or _stream())
+
+    def classify(self, records: torch.Tensor, counts: torch.Tensor, stream=None):
+        """counts (int64 [4]) += classification of the (shard-summed) records."""
+        call("abed_campaign_classify", self.handle, _p(records), records.shape[0], _p(counts), stream or _stream())
 
     def report(self, counts, trials):
         h = (C.c_int64 * 4)(*[int(v) for v in counts.cpu().tolist()])

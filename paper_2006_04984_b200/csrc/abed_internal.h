@@ -73,6 +73,27 @@ __global__ void fic_finalize_kernel(const int64_t* part, int n, const unsigned l
 void ic_from_classes_launch(const int64_t* S, const uint64_t* rowmask, const uint64_t* colmask,
                             const abed_dev::ActGeom& g, int nrc, int ncc, const int32_t* fsum, int32_t* ic,
                             unsigned long long* fic_rhs, cudaStream_t st);
+// IC verdicts of many plans (two launches): ic from the class sums (S == nullptr:
+// computed ahead), FIC rhs when fic_rhs != nullptr, then ic_verify_k
+struct IcVerdictJob {
+  const int64_t* S;
+  const uint64_t* rowmask;
+  const uint64_t* colmask;
+  int nrc, ncc, R, Sd, sh, sw, nph_w, c256;
+  const int32_t* fsum;
+  int32_t* ic;
+  unsigned long long* fic_rhs;
+  const unsigned long long* ksum;
+  const int8_t* f;
+  int64_t K, crs;
+  unsigned long long* scr;
+  abed_verify_outcome* out;
+};
+constexpr int kMaxIcJobs = 64;
+struct IcVerdictBatch {
+  IcVerdictJob job[kMaxIcJobs];
+};
+void ic_verdict_many_launch(const IcVerdictJob* jobs, int n, cudaStream_t st);
 // ic_verify_k verdict: scr = plan-owned {count, first k (init ~0), ticket, -, dot[K]}
 void ic_finalize_launch(const unsigned long long* ksum, const int8_t* f, const int32_t* ic, int64_t K, int64_t crs,
                         unsigned long long* scr, abed_verify_outcome* out, cudaStream_t st);

@@ -202,17 +202,33 @@ static void build_ic_classes(abed_conv_plan* pl) {
   cuda_check(cudaMemset(pl->d_ic_S, 0, pl->ic_S_bytes), "memset ic_S");
 }
 
-// IC verdict chain: ic (+ FIC rhs) from the class sums, then ic_verify_k
-static void ic_verdict(abed_conv_plan* pl, abed_verify_outcome* out, cudaStream_t st) {
+// IC verdict job: ic (+ FIC rhs) from the class sums, then ic_verify_k
+static IcVerdictJob ic_verdict_job(abed_conv_plan* pl, abed_verify_outcome* out, cudaStream_t st) {
   const ActGeom& g = pl->g;
+  IcVerdictJob j{};
   if (pl->d_ic_S) {
     const bool fic = (pl->checks & ABED_CHECK_FIC) != 0;
     if (fic) cuda_check(cudaMemsetAsync(pl->d_acc, 0, 8, st), "memset rhs");
-    ic_from_classes_launch(pl->d_ic_S, pl->d_ic_mask, pl->d_ic_mask + (size_t)g.nph_h * pl->ic_nrc, g, pl->ic_nrc,
-                           pl->ic_ncc, fic ? pl->d_fsum : nullptr, pl->d_ic, fic ? pl->d_acc : nullptr, st);
+    j.S = pl->d_ic_S;
+    j.rowmask = pl->d_ic_mask;
+    j.colmask = pl->d_ic_mask + (size_t)g.nph_h * pl->ic_nrc;
+    j.nrc = pl->ic_nrc; j.ncc = pl->ic_ncc;
+    j.R = g.r; j.Sd = g.s; j.sh = g.sh; j.sw = g.sw; j.nph_w = g.nph_w; j.c256 = g.c16 * 16;
+    j.fsum = fic ? pl->d_fsum : nullptr;
+    j.fic_rhs = fic ? pl->d_acc : nullptr;
   }
-  ic_finalize_launch(pl->d_acc + 4, pl->d_filters, pl->d_ic, pl->shape.k, pl->shape.c * pl->shape.r * pl->shape.s,
-                     pl->d_ic_scr, out, st);
+  j.ic = pl->d_ic;
+  j.ksum = pl->d_acc + 4;
+  j.f = pl->d_filters;
+  j.K = pl->shape.k;
+  j.crs = pl->shape.c * pl->shape.r * pl->shape.s;
+  j.scr = pl->d_ic_scr;
+  j.out = out;
+  return j;
+}
+static void ic_verdict(abed_conv_plan* pl, abed_verify_outcome* out, cudaStream_t st) {
+  const IcVerdictJob j = ic_verdict_job(pl, out, st);
+  ic_verdict_many_launch(&j, 1, st);
 }
 
 // FIC-SM class table.  A phase row i is reached by the filter rows
@@ -654,13 +670,16 @@ int abed_conv_plan_finalize_many(abed_conv_plan* const* plans, int32_t n, abed_v
   return guarded([&] {
     if (n < 0) throw_invalid("finalize_many: negative plan count");
     std::vector<abed_dev::VerdictJob> jobs;
+    std::vector<IcVerdictJob> ic_jobs;
     for (int i = 0; i < n; ++i) {
       abed_conv_plan* pl = plans[i];
       if (pl->checks & (ABED_CHECK_FC | ABED_CHECK_FIC | ABED_CHECK_ICBATCH))
         jobs.push_back(plan_verdict_job(pl, outcomes_dev + 3 * i));
-      if (pl->checks & ABED_CHECK_IC) ic_verdict(pl, outcomes_dev + 3 * i + 2, (cudaStream_t)stream);
+      if (pl->checks & ABED_CHECK_IC) ic_jobs.push_back(ic_verdict_job(pl, outcomes_dev + 3 * i + 2, (cudaStream_t)stream));
     }
-    cuda_check(verdict_launch(jobs.data(), (int)jobs.size(), (cudaStream_t)stream), "verdict");
+    // IC first (with FIC its input checksum also gives FIC's rhs): two launches for all plans
+    if (!ic_jobs.empty()) ic_verdict_many_launch(ic_jobs.data(), (int)ic_jobs.size(), (cudaStream_t)stream);
+    if (!jobs.empty()) cuda_check(verdict_launch(jobs.data(), (int)jobs.size(), (cudaStream_t)stream), "verdict");
   });
 }
 int abed_conv_plan_set_input_checksum_source(abed_conv_plan* pl, int32_t source) {

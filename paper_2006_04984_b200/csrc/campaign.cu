@@ -16,6 +16,7 @@
 //    derive_seed(root, t), so reports are identical for any trial sharding.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <vector>
@@ -243,20 +244,22 @@ void draw(uint64_t seed, const abed_layer_shape& s, int target, int64_t& flat, i
 // The exhaustive path above (abed_run_campaign) re-runs the fused protected conv
 // per trial; tests check both give the same report.
 struct BatchedCampaignArgs {
-  abed_layer_shape s;
+  abed_layer_shape s;    // this shard's layer (s.n = images of the shard)
   int scheme, target;
-  const int8_t* x;       // NCHW, pristine
+  int64_t n0, n_global;  // first global image of the shard, images of the whole batch
+  const int8_t* x;       // NCHW, pristine (the shard's images)
   const int8_t* f;       // KCRS, pristine
-  const int32_t* conv;   // golden ConvOut NKPQ
+  const int32_t* conv;   // golden ConvOut NKPQ of the shard
   const int32_t* fsum;   // gen_filter_checksum (c,r,s)
-  const int32_t* ic;     // gen_input_checksum (c,r,s), pristine input
+  const int32_t* ic;     // gen_input_checksum (c,r,s) of the shard's pristine input
   const float* bias;
   float scale;
   int relu, f32out;
-  const int64_t* flat;   // per trial: flat index, bit
+  const int64_t* flat;   // per trial: flat index into the GLOBAL tensors, bit
   const int32_t* bit;
   int64_t n_trials;
   unsigned long long* counts;  // [4] by classification (ABED_DETECTED, _SDC, _MASKED, _DETECTED_BENIGN)
+  long long* records;          // or, when non-null: per trial {hit, differs, total} of this shard
 };
 
 __device__ __forceinline__ uint32_t epi_bits(int32_t a, float scale, float b, int relu, int f32out) {
@@ -270,11 +273,23 @@ __device__ __forceinline__ int32_t wrap_add(int32_t v, int64_t d) {  // int32 Co
   return static_cast<int32_t>(static_cast<uint32_t>(v) + static_cast<uint32_t>(static_cast<uint64_t>(d)));
 }
 
+// Decision of one trial from the (summed over shards) record {hit, differs, total}:
+// FIC -- the ConvOut sum moved (total != 0); IC with a filter flip -- channel k's sum
+// and its dot with the flipped filter moved by different amounts (total = their
+// difference); otherwise a row (FC) / channel (IC) check failed somewhere (hit).
+__host__ __device__ inline int classify_record(int scheme, int target, long long hit, long long differs,
+                                               long long total) {
+  const bool detected = scheme == ABED_FIC ? total != 0
+                        : (scheme == ABED_IC && target == ABED_TARGET_FILTER) ? total != 0
+                                                                              : hit != 0;
+  return detected ? (differs ? ABED_DETECTED : ABED_DETECTED_BENIGN) : (differs ? ABED_SDC : ABED_MASKED);
+}
+
 __global__ void __launch_bounds__(256) campaign_batched_kernel(const __grid_constant__ BatchedCampaignArgs A) {
   const abed_layer_shape& s = A.s;
   const int64_t P = s.p, Q = s.q, PQ = P * Q, K = s.k, C = s.c, R = s.r, S = s.s;
   __shared__ long long sh_tap[64];  // FC, input target: per-tap (= per-(p,q)) delta of the row sum
-  __shared__ int sh_flag[2];        // [0] detected (FC / IC), [1] output differs
+  __shared__ int sh_flag[2];        // [0] a row / channel check failed, [1] output differs
   __shared__ long long sh_red[8];
   for (int64_t t = blockIdx.x; t < A.n_trials; t += gridDim.x) {
     const int64_t flat = A.flat[t];
@@ -283,11 +298,19 @@ __global__ void __launch_bounds__(256) campaign_batched_kernel(const __grid_cons
     if (threadIdx.x < 2) sh_flag[threadIdx.x] = 0;
     __syncthreads();
     int differs = 0, hit = 0;
-    long long total = 0;  // FIC: change of the ConvOut sum
-    if (A.target == ABED_TARGET_CONVOUT) {
+    long long total = 0;
+    // global image of an input / ConvOut flip (filter flips touch every shard)
+    int64_t n_img = -1;
+    if (A.target == ABED_TARGET_INPUT) n_img = flat / (C * s.h * s.w);
+    if (A.target == ABED_TARGET_CONVOUT) n_img = flat / (K * PQ);
+    const bool mine = A.target == ABED_TARGET_FILTER || (n_img >= A.n0 && n_img < A.n0 + s.n);
+    if (!mine) {
+      // another shard's image: nothing changes here
+    } else if (A.target == ABED_TARGET_CONVOUT) {
       if (threadIdx.x == 0) {
-        const int64_t k = (flat / PQ) % K;
-        const int32_t v = A.conv[flat];
+        const int64_t lf = flat - A.n0 * K * PQ;
+        const int64_t k = (lf / PQ) % K;
+        const int32_t v = A.conv[lf];
         const int32_t v2 = static_cast<int32_t>(static_cast<uint32_t>(v) ^ (1u << bit));
         const long long d = static_cast<long long>(v2) - v;
         total = d;
@@ -313,10 +336,10 @@ __global__ void __launch_bounds__(256) campaign_batched_kernel(const __grid_cons
         hit |= d != 0;  // FC: row (n,p,q) moves, its extra does not
         differs |= epi_bits(v2, A.scale, b, A.relu, A.f32out) != epi_bits(v, A.scale, b, A.relu, A.f32out);
       }
-      if (A.scheme == ABED_IC) hit = 0;  // decided on the channel sum below
+      if (A.scheme == ABED_IC) hit = 0;  // decided on total (channel sum vs dot) below
     } else {
-      const int64_t w0 = flat % s.w, h0 = (flat / s.w) % s.h, c = (flat / (s.w * s.h)) % C, n = flat / (s.w * s.h * C);
-      const int8_t x0 = A.x[flat];
+      const int64_t w0 = flat % s.w, h0 = (flat / s.w) % s.h, c = (flat / (s.w * s.h)) % C, n = n_img - A.n0;
+      const int8_t x0 = A.x[flat - A.n0 * C * s.h * s.w];
       const long long dx = static_cast<long long>(static_cast<int8_t>(x0 ^ static_cast<int8_t>(1 << bit))) - x0;
       const int taps = static_cast<int>(R * S);
       for (int64_t k = threadIdx.x; k < K; k += blockDim.x) {
@@ -353,45 +376,61 @@ __global__ void __launch_bounds__(256) campaign_batched_kernel(const __grid_cons
     if (threadIdx.x == 0) {
       long long tot = 0;
       for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) tot += sh_red[w];
-      bool detected;
-      if (A.scheme == ABED_FIC) {
-        detected = tot != 0;
-      } else if (A.scheme == ABED_FC && A.target == ABED_TARGET_INPUT) {
+      long long rhit = sh_flag[0];
+      if (mine && A.scheme == ABED_FC && A.target == ABED_TARGET_INPUT) {
         // per covering tap: the row sum moved by sh_tap[tap], the extra fmap by dx * fsum[c,r,s]
         const int64_t w0 = flat % s.w, h0 = (flat / s.w) % s.h, c = (flat / (s.w * s.h)) % C;
-        const int8_t x0 = A.x[flat];
+        const int8_t x0 = A.x[flat - A.n0 * C * s.h * s.w];
         const long long dx = static_cast<long long>(static_cast<int8_t>(x0 ^ static_cast<int8_t>(1 << bit))) - x0;
-        detected = false;
+        rhit = 0;
         for (int tap = 0; tap < static_cast<int>(R * S); ++tap) {
           const int64_t r = tap / S, ss = tap - r * S;
           const int64_t hp = h0 + s.pad_h - r, wp = w0 + s.pad_w - ss;
           if (hp < 0 || wp < 0 || hp % s.stride_h || wp % s.stride_w || hp / s.stride_h >= P || wp / s.stride_w >= Q)
             continue;
-          if (sh_tap[tap] != dx * static_cast<long long>(A.fsum[(c * R + r) * S + ss])) detected = true;
+          if (sh_tap[tap] != dx * static_cast<long long>(A.fsum[(c * R + r) * S + ss])) rhit = 1;
         }
-      } else if (A.scheme == ABED_IC && A.target == ABED_TARGET_FILTER) {
-        // channel k: sum moved by tot, dot(flipped filter, ic) by df * ic[c,r,s]
+      } else if (mine && A.scheme == ABED_IC && A.target == ABED_TARGET_FILTER) {
+        // channel k: this shard's sum moved by tot, its share of dot(flipped filter, ic) by df * ic[c,r,s]
         const int64_t crs = flat % (C * R * S);
         const int8_t f0 = A.f[flat];
         const long long df = static_cast<long long>(static_cast<int8_t>(f0 ^ static_cast<int8_t>(1 << bit))) - f0;
-        detected = tot != df * static_cast<long long>(A.ic[crs]);
-      } else {
-        detected = sh_flag[0] != 0;
+        tot -= df * static_cast<long long>(A.ic[crs]);
       }
-      const int cls = detected ? (sh_flag[1] ? ABED_DETECTED : ABED_DETECTED_BENIGN)
-                               : (sh_flag[1] ? ABED_SDC : ABED_MASKED);  // faults.hpp:255-261
-      atomicAdd(A.counts + cls, 1ull);
+      if (A.records) {
+        long long* rec = A.records + 3 * t;
+        rec[0] = rhit;
+        rec[1] = sh_flag[1];
+        rec[2] = tot;
+      } else {
+        atomicAdd(A.counts + classify_record(A.scheme, A.target, rhit, sh_flag[1], tot), 1ull);  // faults.hpp:255-261
+      }
     }
     __syncthreads();
   }
 }
 
+// classification counts of summed per-trial records (after the cross-shard all-reduce)
+__global__ void campaign_classify_kernel(const long long* __restrict__ rec, int64_t n, int scheme, int target,
+                                         unsigned long long* counts) {
+  __shared__ unsigned long long c[4];
+  if (threadIdx.x < 4) c[threadIdx.x] = 0;
+  __syncthreads();
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&c[classify_record(scheme, target, rec[3 * t], rec[3 * t + 1], rec[3 * t + 2])], 1ull);
+  __syncthreads();
+  if (threadIdx.x < 4 && c[threadIdx.x]) atomicAdd(counts + threadIdx.x, c[threadIdx.x]);
+}
+
 }  // namespace
 
-// device-resident campaign: data, golden ConvOut, pristine checksums and every
-// trial's flip drawn once; runs are single launches over trial ranges
+// device-resident campaign (one batch shard): data, golden ConvOut, pristine
+// checksums and every trial's flip drawn once; runs are single launches over
+// trial ranges
 struct abed_campaign {
   abed_campaign_config cfg{};
+  abed_layer_shape shard{};  // cfg.shape restricted to images [n0, n0 + shard.n)
+  int64_t n0 = 0;
   int8_t* x = nullptr;
   int8_t* f = nullptr;
   int32_t* conv = nullptr;
@@ -409,7 +448,7 @@ struct abed_campaign {
 
 namespace {
 
-abed_campaign* campaign_create(const abed_campaign_config& cfg) {
+abed_campaign* campaign_create(const abed_campaign_config& cfg, int64_t n_begin, int64_t n_end) {
   if (cfg.trials < 1) throw_invalid("run_campaign: trials must be >= 1");
   const abed_layer_shape& s = cfg.shape;
   validate_shape(s);
@@ -418,6 +457,7 @@ abed_campaign* campaign_create(const abed_campaign_config& cfg) {
   if (cfg.output_kind != ABED_I8 && cfg.output_kind != ABED_F32) throw_invalid("epilog: output kind must be i8 or f32");
   if (!std::isfinite(cfg.scale)) throw_invalid("epilog: non-finite scale");
   if (s.r * s.s > 64) throw_invalid("run_campaign: filters with more than 64 taps are not supported");
+  if (n_begin < 0 || n_end > s.n || n_begin >= n_end) throw_invalid("campaign: bad image shard");
   std::vector<float> hb((size_t)s.k, 0.0f);  // faults.hpp:167-168: empty bias -> zeros
   if (cfg.bias_host && cfg.bias_len > 0) {
     if (cfg.bias_len != s.k) throw_invalid("epilog: bias length must equal the channel count");
@@ -429,10 +469,14 @@ abed_campaign* campaign_create(const abed_campaign_config& cfg) {
   auto* c = new abed_campaign();
   c->cfg = cfg;
   c->cfg.bias_host = nullptr;
+  c->shard = s;
+  c->shard.n = n_end - n_begin;
+  c->n0 = n_begin;
   try {
     cudaStream_t st = nullptr;
-    const int64_t nchw = s.n * s.c * s.h * s.w, kcrs = s.k * s.c * s.r * s.s, crs = s.c * s.r * s.s;
-    const int64_t nkpq = s.n * s.k * s.p * s.q;
+    const abed_layer_shape& sh = c->shard;
+    const int64_t chw = s.c * s.h * s.w, nchw = sh.n * chw, kcrs = s.k * s.c * s.r * s.s, crs = s.c * s.r * s.s;
+    const int64_t nkpq = sh.n * s.k * s.p * s.q;
     cuda_check(cudaMalloc(&c->x, (size_t)nchw), "cudaMalloc(x)");
     cuda_check(cudaMalloc(&c->f, (size_t)kcrs), "cudaMalloc(f)");
     cuda_check(cudaMalloc(&c->conv, (size_t)nkpq * 4), "cudaMalloc(conv)");
@@ -446,17 +490,17 @@ abed_campaign* campaign_create(const abed_campaign_config& cfg) {
     if (cfg.mode == ABED_DATA_ONES) {  // faults.hpp:280-283
       cuda_check(cudaMemset(c->x, 1, (size_t)nchw), "memset");
       cuda_check(cudaMemset(c->f, 1, (size_t)kcrs), "memset");
-    } else {  // faults.hpp:284-288: one stream, input then filters
+    } else {  // faults.hpp:284-288: one stream, input then filters (the shard's slice of it)
       const uint64_t seed = derive(cfg.root_seed, 0x0DA7Au);
-      abed_fill_random_i8(c->x, nchw, seed, 0, st);
-      abed_fill_random_i8(c->f, kcrs, seed, (uint64_t)nchw, st);
+      abed_fill_random_i8(c->x, nchw, seed, (uint64_t)(n_begin * chw), st);
+      abed_fill_random_i8(c->f, kcrs, seed, (uint64_t)(s.n * chw), st);
     }
-    tc_conv_nchw(s, c->x, c->f, c->conv, st);  // golden ConvOut on the tensor cores
+    tc_conv_nchw(sh, c->x, c->f, c->conv, st);  // golden ConvOut on the tensor cores
     dev_colsum_i8(c->f, s.k, crs, c->fsum, st);
-    dev_gen_input_checksum(c->x, s, c->ic, st);
+    dev_gen_input_checksum(c->x, sh, c->ic, st);
     std::vector<int64_t> hf((size_t)cfg.trials);
     std::vector<int32_t> hbit((size_t)cfg.trials);
-    for (int64_t t = 0; t < cfg.trials; ++t) {  // faults.hpp:200-208, seeds derive_seed(root, t)
+    for (int64_t t = 0; t < cfg.trials; ++t) {  // faults.hpp:200-208, seeds derive_seed(root, t), global tensors
       int b;
       draw(derive(cfg.root_seed, (uint64_t)t), s, cfg.target, hf[(size_t)t], b);
       hbit[(size_t)t] = b;
@@ -471,15 +515,18 @@ abed_campaign* campaign_create(const abed_campaign_config& cfg) {
   return c;
 }
 
-void campaign_run(abed_campaign* c, int64_t t_begin, int64_t t_end, unsigned long long* counts, cudaStream_t st) {
+void campaign_run(abed_campaign* c, int64_t t_begin, int64_t t_end, unsigned long long* counts, long long* records,
+                  cudaStream_t st) {
   if (t_begin < 0) t_begin = 0;
   if (t_end > c->cfg.trials) t_end = c->cfg.trials;
   const int64_t nt = t_end > t_begin ? t_end - t_begin : 0;
   if (!nt) return;
   BatchedCampaignArgs a{};
-  a.s = c->cfg.shape;
+  a.s = c->shard;
   a.scheme = c->cfg.scheme;
   a.target = c->cfg.target;
+  a.n0 = c->n0;
+  a.n_global = c->cfg.shape.n;
   a.x = c->x; a.f = c->f; a.conv = c->conv; a.fsum = c->fsum; a.ic = c->ic; a.bias = c->bias;
   a.scale = c->cfg.scale;
   a.relu = c->cfg.activation == ABED_RELU ? 1 : 0;
@@ -488,6 +535,7 @@ void campaign_run(abed_campaign* c, int64_t t_begin, int64_t t_end, unsigned lon
   a.bit = c->bit + t_begin;
   a.n_trials = nt;
   a.counts = counts;
+  a.records = records;
   const int64_t grid = nt < (int64_t)num_sms() * 8 ? nt : (int64_t)num_sms() * 8;
   campaign_batched_kernel<<<(unsigned)grid, 256, 0, st>>>(a);
   cuda_check(cudaGetLastError(), "campaign_batched");
@@ -629,7 +677,33 @@ int abed_run_campaign(const abed_campaign_config* cfg, int64_t t_begin, int64_t 
 }
 
 int abed_campaign_create(const abed_campaign_config* config, abed_campaign** campaign) {
-  GUARD(if (!config || !campaign) throw_invalid("campaign: null argument"); *campaign = campaign_create(*config));
+  GUARD(if (!config || !campaign) throw_invalid("campaign: null argument");
+        *campaign = campaign_create(*config, 0, config->shape.n));
+}
+
+int abed_campaign_create_shard(const abed_campaign_config* config, int64_t image_begin, int64_t image_end,
+                               abed_campaign** campaign) {
+  GUARD(if (!config || !campaign) throw_invalid("campaign: null argument");
+        *campaign = campaign_create(*config, image_begin, image_end));
+}
+
+int abed_campaign_run_records(abed_campaign* campaign, int64_t trial_begin, int64_t trial_end, int64_t* records_dev,
+                              void* stream) {
+  GUARD(if (!campaign || !records_dev) throw_invalid("campaign: null argument");
+        campaign_run(campaign, trial_begin, trial_end, nullptr, reinterpret_cast<long long*>(records_dev),
+                     (cudaStream_t)stream));
+}
+
+int abed_campaign_classify(const abed_campaign* campaign, const int64_t* records_dev, int64_t n_records,
+                           int64_t* counts_dev, void* stream) {
+  GUARD(if (!campaign || !records_dev || !counts_dev) throw_invalid("campaign: null argument");
+        if (n_records > 0) {
+          const int blocks = (int)std::min<int64_t>((n_records + 255) / 256, 148);
+          campaign_classify_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
+              reinterpret_cast<const long long*>(records_dev), n_records, campaign->cfg.scheme, campaign->cfg.target,
+              reinterpret_cast<unsigned long long*>(counts_dev));
+          cuda_check(cudaGetLastError(), "campaign classify");
+        });
 }
 
 int abed_campaign_destroy(abed_campaign* campaign) {
@@ -639,7 +713,9 @@ int abed_campaign_destroy(abed_campaign* campaign) {
 int abed_campaign_run(abed_campaign* campaign, int64_t trial_begin, int64_t trial_end, int64_t* counts_dev,
                       void* stream) {
   GUARD(if (!campaign || !counts_dev) throw_invalid("campaign: null argument");
-        campaign_run(campaign, trial_begin, trial_end, reinterpret_cast<unsigned long long*>(counts_dev),
+        if (campaign->shard.n != campaign->cfg.shape.n)
+          throw_invalid("campaign: a batch shard reports per-trial records (abed_campaign_run_records)");
+        campaign_run(campaign, trial_begin, trial_end, reinterpret_cast<unsigned long long*>(counts_dev), nullptr,
                      (cudaStream_t)stream));
 }
 
@@ -653,10 +729,10 @@ int abed_run_campaign_batched(const abed_campaign_config* cfg, int64_t t_begin, 
                               abed_campaign_report* rep) {
   GUARD(
       if (!cfg || !rep) throw_invalid("campaign: null argument");
-      abed_campaign* c = campaign_create(*cfg);
+      abed_campaign* c = campaign_create(*cfg, 0, cfg->shape.n);
       try {
         cuda_check(cudaMemset(c->counts, 0, 32), "memset counts");
-        campaign_run(c, t_begin, t_end, c->counts, nullptr);
+        campaign_run(c, t_begin, t_end, c->counts, nullptr, nullptr);
         unsigned long long h[4];
         cuda_check(cudaMemcpy(h, c->counts, 32, cudaMemcpyDeviceToHost), "counts d2h");
         const int64_t b = t_begin < 0 ? 0 : t_begin, e = t_end > cfg->trials ? cfg->trials : t_end;

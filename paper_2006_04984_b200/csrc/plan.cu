@@ -212,12 +212,152 @@ __global__ void __launch_bounds__(256) pack_input_v4_kernel(const int8_t* __rest
   }
 }
 
+// Shared-memory staged transpose (NCHW -> strip planes): block = (plane, image,
+// band of rb M-space rows); smem holds the band in the OUTPUT layout
+// [rb][Wl][16 channels].  Phase 0 zeroes it (halo, filler channels); phase 1:
+// work item = (channel quad, band row, input word of 4 columns), 4 coalesced
+// 32-bit loads (the quad's channels), a 4 x 4 byte transpose (__byte_perm) and
+// one 32-bit smem store per pixel of this stride phase; phase 2 copies the band
+// out with 16-byte loads / stores.  Every input byte read once per stride phase,
+// every output byte written once; ~20 instructions per 16-byte pixel (the
+// byte-gather version was issue-bound at 0.25 of HBM).  Rows that are not a
+// multiple of 4 bytes (or an unaligned base) use byte loads in phase 1.  The zero
+// tail of each plane (after the last image) is written by one extra block per plane.
+template <int SW>  // horizontal stride 1 or 2 (0: any, with divisions)
+__global__ void __launch_bounds__(256) pack_input_smem_kernel(const int8_t* __restrict__ x, ActGeom g, int lrb,
+                                                              int nbands, int words_ok, int8_t* __restrict__ out) {
+  extern __shared__ __align__(16) uint8_t tile[];  // [rb][Wl][16]
+  const int rb = 1 << lrb;
+  const int plane = blockIdx.y;
+  const int grp = plane % g.c16, phase = plane / g.c16;
+  const int a = phase / g.nph_w, b = phase % g.nph_w;
+  uint4* const pbase = reinterpret_cast<uint4*>(out) + (int64_t)plane * g.plane_len;
+  if (blockIdx.x == (unsigned)(g.n * nbands)) {  // zero tail of this plane
+    for (int64_t t = g.m_total + threadIdx.x; t < g.plane_len; t += blockDim.x) pbase[t] = make_uint4(0, 0, 0, 0);
+    return;
+  }
+  const int n = blockIdx.x / nbands, i0 = (blockIdx.x - n * nbands) * rb;
+  const int rows = min(rb, g.Hl - i0);
+  const int nch = max(0, min(16, g.c - grp * 16));  // 0: a filler group (c16 is even)
+  const int npix = rows * g.Wl;
+  uint4* const st4 = reinterpret_cast<uint4*>(tile);
+  for (int i = threadIdx.x; i < npix; i += blockDim.x) st4[i] = make_uint4(0, 0, 0, 0);
+  __syncthreads();
+  const int64_t HW = (int64_t)g.h * g.w;
+  const int8_t* xg = x + ((int64_t)n * g.c + grp * 16) * HW;
+  const int off = g.pw - b;  // output column j holds input column j * sw - off
+  const int sw = SW ? SW : g.sw;
+  uint32_t* const t32 = reinterpret_cast<uint32_t*>(tile);
+  if (words_ok) {
+    // lanes split into row groups of lpr lanes (lane -> word q of a row); warps and
+    // row groups walk the (channel quad, band row) pairs: no divisions per item
+    const int wq = g.w >> 2;
+    const int lpr = wq <= 4 ? 4 : wq <= 8 ? 8 : wq <= 16 ? 16 : 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int sub = lane / lpr, ql = lane - sub * lpr;
+    const int gpw = 32 / lpr;  // row groups per warp
+    const int nq = (nch + 3) >> 2;
+    const int npairs = nq << lrb;
+    // U row-pair iterations per batch (4U loads in flight per thread; U = 4 cost
+    // registers and occupancy and measured no faster on B200, so U = 1)
+    constexpr int U = 1;
+    for (int rb0 = warp * gpw; rb0 < npairs; rb0 += U * 8 * gpw) {
+      for (int q0 = 0; q0 < wq; q0 += lpr) {
+        const int q = q0 + ql;
+        uint32_t v[U][4];
+        bool okr[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int r = rb0 + u * 8 * gpw + sub;
+          const int cq = r >> lrb, ii = r & (rb - 1);
+          const int hh = (i0 + ii) * g.sh + a - g.ph;
+          okr[u] = r < npairs && ii < rows && hh >= 0 && hh < g.h && q < wq;
+          const int8_t* src = xg + (int64_t)(cq * 4) * HW + (int64_t)hh * g.w;
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            v[u][e] = (okr[u] && cq * 4 + e < nch) ? __ldg(reinterpret_cast<const uint32_t*>(src + e * HW) + q) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (!okr[u]) continue;
+          const int r = rb0 + u * 8 * gpw + sub;
+          const int cq = r >> lrb, ii = r & (rb - 1);
+          // 4 x 4 byte transpose: p[t] = channels 4cq..4cq+3 of input column 4q + t
+          const uint32_t t01lo = __byte_perm(v[u][0], v[u][1], 0x5140), t01hi = __byte_perm(v[u][0], v[u][1], 0x7362);
+          const uint32_t t23lo = __byte_perm(v[u][2], v[u][3], 0x5140), t23hi = __byte_perm(v[u][2], v[u][3], 0x7362);
+          uint32_t pw4[4] = {__byte_perm(t01lo, t23lo, 0x5410), __byte_perm(t01lo, t23lo, 0x7632),
+                             __byte_perm(t01hi, t23hi, 0x5410), __byte_perm(t01hi, t23hi, 0x7632)};
+          // rotate by q & 3 so one store instruction of the warp spreads over the
+          // banks: lane writes column 4q + ((t + q) & 3) at step t
+          const int rot = q & 3;
+          if (rot & 1) {
+            const uint32_t t0 = pw4[0];
+            pw4[0] = pw4[1]; pw4[1] = pw4[2]; pw4[2] = pw4[3]; pw4[3] = t0;
+          }
+          if (rot & 2) {
+            const uint32_t t0 = pw4[0], t1 = pw4[1];
+            pw4[0] = pw4[2]; pw4[1] = pw4[3]; pw4[2] = t0; pw4[3] = t1;
+          }
+          uint32_t* const trow = t32 + ii * g.Wl * 4 + cq;
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const int jj = q * 4 + ((t + rot) & 3) + off;  // = j * sw
+            int j;
+            if (SW == 1) {
+              j = jj;
+            } else if (SW == 2) {
+              if (jj & 1) continue;
+              j = jj >> 1;
+            } else {
+              if (jj % sw) continue;
+              j = jj / sw;
+            }
+            if (jj < 0 || j >= g.Wl) continue;
+            trow[j * 4] = pw4[t];
+          }
+        }
+      }
+    }
+  } else {
+    const int total = nch * rows * g.w;
+    for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+      const int e = idx / (rows * g.w), rem = idx - e * rows * g.w, ii = rem / g.w, ww = rem - ii * g.w;
+      const int hh = (i0 + ii) * g.sh + a - g.ph;
+      const int jj = ww + off;
+      if (hh < 0 || hh >= g.h || jj < 0 || jj % sw) continue;
+      const int j = jj / sw;
+      if (j >= g.Wl) continue;
+      tile[(ii * g.Wl + j) * 16 + e] = (uint8_t)xg[e * HW + (int64_t)hh * g.w + ww];
+    }
+  }
+  __syncthreads();
+  uint4* const dst = pbase + ((int64_t)n * g.Hl + i0) * g.Wl;
+  for (int i = threadIdx.x; i < npix; i += blockDim.x) dst[i] = st4[i];
+}
+
 void launch_pack_input(const int8_t* x, const ActGeom& g, int8_t* packed, cudaStream_t st) {
-  const int64_t per_plane = (int64_t)g.n * g.Hl * ((g.Wl + 3) / 4) + (g.plane_len - g.m_total + 3) / 4;
-  if (per_plane >= (int64_t(1) << 31)) throw_invalid("pack_input: plane too large");
   const int planes = g.n_phase * g.c16;
   const int64_t x_bytes = (int64_t)g.n * g.c * g.h * g.w;
-  // about 8 resident 256-thread blocks per SM over all planes
+  // band height: a power of two <= 8 M-space rows, <= 24 KB of staged output pixels
+  int lrb = 3;
+  while (lrb > 0 && (16 << lrb) * g.Wl > 24 * 1024) --lrb;
+  if (16 * g.Wl <= 48 * 1024) {
+    const int rb = 1 << lrb;
+    const int nbands = (g.Hl + rb - 1) / rb;
+    const int words_ok = (g.w % 4 == 0) && (reinterpret_cast<uintptr_t>(x) & 3) == 0;
+    const size_t smem = (size_t)16 * rb * g.Wl;
+    const dim3 grid((unsigned)(g.n * nbands + 1), (unsigned)planes);
+    if (g.sw == 1)
+      pack_input_smem_kernel<1><<<grid, 256, smem, st>>>(x, g, lrb, nbands, words_ok, packed);
+    else if (g.sw == 2)
+      pack_input_smem_kernel<2><<<grid, 256, smem, st>>>(x, g, lrb, nbands, words_ok, packed);
+    else
+      pack_input_smem_kernel<0><<<grid, 256, smem, st>>>(x, g, lrb, nbands, words_ok, packed);
+    return;
+  }
+  // very wide rows: the register-transpose kernel
+  const int64_t per_plane = (int64_t)g.n * g.Hl * ((g.Wl + 3) / 4) + (g.plane_len - g.m_total + 3) / 4;
+  if (per_plane >= (int64_t(1) << 31)) throw_invalid("pack_input: plane too large");
   int64_t bx = ((int64_t)num_sms() * 8 + planes - 1) / planes;
   const int64_t need = (per_plane + 255) / 256;
   if (bx > need) bx = need;
@@ -704,6 +844,107 @@ void ic_finalize_launch(const unsigned long long* ksum, const int8_t* f, const i
                         unsigned long long* scr, abed_verify_outcome* out, cudaStream_t st) {
   const int blocks = (int)std::min<int64_t>(K, 4 * num_sms());
   ic_finalize_kernel<<<blocks, 256, 0, st>>>(ksum, f, ic, K, crs, scr, out);
+}
+
+// IC verdicts of many plans in two launches (blockIdx.y = plan): every plan's
+// ic from its class sums, then every plan's ic_verify_k.  A pass of 16 IC
+// layers was 32 dependent small launches (~25 us per layer of step time).
+__global__ void __launch_bounds__(128) ic_from_classes_many_kernel(const __grid_constant__ IcVerdictBatch b) {
+  const IcVerdictJob& j = b.job[blockIdx.y];
+  if (!j.S) return;  // input checksum computed ahead (no class sums)
+  const int64_t crs = j.crs;
+  const int rs = j.R * j.Sd;
+  long long dot = 0;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < crs; t += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(t / rs), r = (int)((t / j.Sd) % j.R), sc = (int)(t % j.Sd);
+    const int a = r % j.sh, bb = sc % j.sw, phase = a * j.nph_w + bb;
+    long long v = 0;
+    for (int rc = 0; rc < j.nrc; ++rc) {
+      if (!((j.rowmask[a * j.nrc + rc] >> r) & 1ull)) continue;
+      for (int cc = 0; cc < j.ncc; ++cc)
+        if ((j.colmask[bb * j.ncc + cc] >> sc) & 1ull) v += j.S[((int64_t)(phase * j.nrc + rc) * j.ncc + cc) * j.c256 + c];
+    }
+    j.ic[t] = (int32_t)v;
+    if (j.fsum) dot += (long long)j.fsum[t] * v;
+  }
+  if (j.fic_rhs) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+    if ((threadIdx.x & 31) == 0 && dot != 0) atomicAdd(j.fic_rhs, (unsigned long long)dot);
+  }
+}
+
+// ic_verify_k (checksum.hpp:319-347) per plan: a warp per channel k (16-byte
+// filter loads), count + first mismatching k into scr, the plan's last block
+// (ticket) writes the outcome and resets scr
+__global__ void __launch_bounds__(256) ic_finalize_many_kernel(const __grid_constant__ IcVerdictBatch b) {
+  const IcVerdictJob& j = b.job[blockIdx.y];
+  __shared__ bool s_last;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const bool vec = (j.crs & 15) == 0 && (reinterpret_cast<uintptr_t>(j.f) & 15) == 0;
+  for (int64_t k = (int64_t)blockIdx.x * nw + w; k < j.K; k += (int64_t)gridDim.x * nw) {
+    long long dot = 0;
+    const int8_t* fk = j.f + k * j.crs;
+    if (vec) {
+      for (int64_t i = (int64_t)lane * 16; i < j.crs; i += 32 * 16) {
+        const int4 fv = __ldg(reinterpret_cast<const int4*>(fk + i));
+        const int4 c0 = __ldg(reinterpret_cast<const int4*>(j.ic + i)), c1 = __ldg(reinterpret_cast<const int4*>(j.ic + i + 4));
+        const int4 c2 = __ldg(reinterpret_cast<const int4*>(j.ic + i + 8)), c3 = __ldg(reinterpret_cast<const int4*>(j.ic + i + 12));
+        const int cv[16] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w, c2.x, c2.y, c2.z, c2.w, c3.x, c3.y, c3.z, c3.w};
+        const uint32_t fw[4] = {(uint32_t)fv.x, (uint32_t)fv.y, (uint32_t)fv.z, (uint32_t)fv.w};
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+          dot += (long long)(int8_t)(fw[e >> 2] >> (8 * (e & 3))) * cv[e];
+      }
+    } else {
+      for (int64_t i = lane; i < j.crs; i += 32) dot += (long long)fk[i] * j.ic[i];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+    if (lane == 0) {
+      j.scr[4 + k] = (unsigned long long)dot;
+      if ((long long)j.ksum[k] != dot) {
+        atomicAdd(&j.scr[0], 1ull);
+        atomicMin(&j.scr[1], (unsigned long long)k);
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(&j.scr[2], 1ull) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last || threadIdx.x != 0) return;
+  __threadfence();
+  const unsigned long long cnt = __ldcg(&j.scr[0]);
+  if (cnt == 0) {
+    write_outcome(j.out, 0, 0, 0, 0, 0, 0, 0, 0);
+  } else {
+    const int64_t k = (int64_t)__ldcg(&j.scr[1]);
+    write_outcome(j.out, 1, 1, k, -1, -1, (long long)j.ksum[k], (long long)__ldcg(&j.scr[4 + k]), (long long)cnt);
+  }
+  j.scr[0] = 0ull;
+  j.scr[1] = ~0ull;
+  j.scr[2] = 0ull;
+}
+
+void ic_verdict_many_launch(const IcVerdictJob* jobs, int n, cudaStream_t st) {
+  for (int i = 0; i < n; i += kMaxIcJobs) {
+    IcVerdictBatch b{};
+    const int m = std::min(kMaxIcJobs, n - i);
+    int64_t max_crs = 1, max_k = 1;
+    for (int q = 0; q < m; ++q) {
+      b.job[q] = jobs[i + q];
+      if (jobs[i + q].S) max_crs = std::max(max_crs, jobs[i + q].crs);
+      max_k = std::max(max_k, jobs[i + q].K);
+    }
+    const int gx = (int)std::min<int64_t>((max_crs + 127) / 128, 64);
+    ic_from_classes_many_kernel<<<dim3(gx, m), 128, 0, st>>>(b);
+    const int fx = (int)std::min<int64_t>((max_k + 7) / 8, 64);
+    ic_finalize_many_kernel<<<dim3(fx, m), 256, 0, st>>>(b);
+    cuda_check(cudaGetLastError(), "ic verdicts");
+  }
 }
 
 // ---------------------------------------------------------------------------

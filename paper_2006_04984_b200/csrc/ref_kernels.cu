@@ -5,6 +5,7 @@
 // build (FMA contraction spelled out with fma/fmaf).
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
+#include <cstdlib>
 
 #include <cmath>
 #include <cstring>
@@ -205,8 +206,8 @@ __global__ void __launch_bounds__(kColsumWarps * 32) colsum_i8_cluster_kernel(co
 #pragma unroll
   for (int j = 0; j < 16; ++j) acc[j] = 0;
   if (c16 < cols16) {
-    // the warp's rows r0 + warp, + 8, ...: full batches of 8 rows with every load
-    // issued before use (pointer increments, no predicates), then a masked tail
+    // the warp's rows r0 + warp, + 8, ...: batches of 16 rows with every load
+    // issued before use (pointer increments, no predicates), then a masked batch
     const int64_t step = (int64_t)kColsumWarps * cols16;  // uint4 stride between a warp's rows
     const uint4* ptr = reinterpret_cast<const uint4*>(x) + c16 + (r0 + warp) * cols16;
     const int64_t mine = r1 - r0 > warp ? (r1 - r0 - warp + kColsumWarps - 1) / kColsumWarps : 0;
@@ -214,13 +215,13 @@ __global__ void __launch_bounds__(kColsumWarps * 32) colsum_i8_cluster_kernel(co
     while (done < mine) {
       uint32_t ev[4] = {0u, 0u, 0u, 0u}, od[4] = {0u, 0u, 0u, 0u};
       int64_t batch_end = done + 256 < mine ? done + 256 : mine;  // 16-bit lanes: <= 256 rows per flush
-      for (; done + 8 <= batch_end; done += 8) {
-        uint4 v[8];
+      for (; done + 16 <= batch_end; done += 16) {  // 16 x 16 B in flight per thread
+        uint4 v[16];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = __ldcs(ptr + u * step);
-        ptr += 8 * step;
+        for (int u = 0; u < 16; ++u) v[u] = __ldcs(ptr + u * step);
+        ptr += 16 * step;
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < 16; ++u) {
           const uint32_t w[4] = {v[u].x ^ 0x80808080u, v[u].y ^ 0x80808080u, v[u].z ^ 0x80808080u,
                                  v[u].w ^ 0x80808080u};
 #pragma unroll
@@ -230,14 +231,23 @@ __global__ void __launch_bounds__(kColsumWarps * 32) colsum_i8_cluster_kernel(co
           }
         }
       }
-      for (; done < batch_end; ++done) {
-        const uint4 v = __ldcs(ptr);
-        ptr += step;
-        const uint32_t w[4] = {v.x ^ 0x80808080u, v.y ^ 0x80808080u, v.z ^ 0x80808080u, v.w ^ 0x80808080u};
+      if (done < batch_end) {  // masked last batch: every load still issued before use
+        const int rem = static_cast<int>(batch_end - done);
+        uint4 v[16];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          ev[q] += w[q] & 0x00FF00FFu;
-          od[q] += (w[q] >> 8) & 0x00FF00FFu;
+        for (int u = 0; u < 16; ++u)
+          v[u] = u < rem ? __ldcs(ptr + u * step) : make_uint4(0x80808080u, 0x80808080u, 0x80808080u, 0x80808080u);
+        ptr += rem * step;
+        done = batch_end;
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {  // padding slots add (0x80 ^ 0x80) = 0
+          const uint32_t w[4] = {v[u].x ^ 0x80808080u, v[u].y ^ 0x80808080u, v[u].z ^ 0x80808080u,
+                                 v[u].w ^ 0x80808080u};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            ev[q] += w[q] & 0x00FF00FFu;
+            od[q] += (w[q] >> 8) & 0x00FF00FFu;
+          }
         }
       }
 #pragma unroll
@@ -523,10 +533,18 @@ void dev_colsum_i8(const int8_t* x, int64_t rows, int64_t len, int32_t* out, cud
     // row splits of a 512-column tile = one cluster (<= 16 CTAs, DSMEM reduction):
     // about 8 resident CTAs per SM in one wave, at least one row per warp
     const int64_t col_tiles = (len / 16 + 31) / 32;
-    int64_t cs = ((int64_t)num_sms() * 8) / col_tiles;
+    // clusters only when the column tiles alone leave SMs idle (their co-scheduling
+    // and DSMEM hand-off cost more than they save once every SM has a tile:
+    // measured 26.7 -> 18.5 us on the 256 x 200704 batch checksum)
+    int64_t cs = col_tiles >= num_sms() ? 1 : ((int64_t)num_sms() * 8) / col_tiles;
     const int64_t max_cs = (rows + kColsumWarps - 1) / kColsumWarps;
     if (cs > max_cs) cs = max_cs;
-    if (cs > 16) cs = 16;
+    static const int cs_cap = [] {
+      const char* e = getenv("ABED_COLSUM_MAX_CLUSTER");  // tuning experiments
+      const int v = e ? atoi(e) : 16;
+      return v >= 1 && v <= 16 ? v : 16;
+    }();
+    if (cs > cs_cap) cs = cs_cap;
     if (cs < 1) cs = 1;
     const int64_t rows_per = (rows + cs - 1) / cs;
     static bool attr[64] = {};

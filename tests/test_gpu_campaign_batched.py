@@ -90,3 +90,24 @@ def test_batched_guards_mirror_reference():
         api.run_campaign(ls, abi.FIC, abi.TARGET_CONVOUT, 0, 1, batched=True)
     with pytest.raises(abi.InvalidArgument):
         api.run_campaign(ls, abi.ICBATCH, abi.TARGET_CONVOUT, 10, 1, batched=True)
+
+
+@pytest.mark.parametrize("scheme", SCHEMES, ids=["FC", "IC", "FIC"])
+@pytest.mark.parametrize("target", TARGETS, ids=["input", "filter", "convout"])
+def test_batch_sharded_records_sum_to_single_gpu_report(scheme, target):
+    """configs[4]'s multi-GPU campaign: each rank holds a batch shard of the layer;
+    per-trial records summed over the shards (the NCCL all-reduce) and classified
+    equal the whole-batch report -- here with 3 uneven shards in one process."""
+    ls = api.layer_shape(6, 16, 12, 12, 24, 3, 3, 1, 1, 1, 1)
+    trials, seed = 400, 31 + 3 * scheme + target
+    whole = api.run_campaign(ls, scheme, target, trials, seed, mode=abi.DATA_RANDOM_I8, batched=True)
+    total = torch.zeros(trials, 3, dtype=torch.int64, device="cuda")
+    for b, e in [(0, 1), (1, 4), (4, 6)]:
+        camp = api.Campaign(ls, scheme, target, trials, seed, mode=abi.DATA_RANDOM_I8, images=(b, e))
+        rec = torch.zeros(trials, 3, dtype=torch.int64, device="cuda")
+        camp.run_records(rec)
+        total += rec
+    cnt = torch.zeros(4, dtype=torch.int64, device="cuda")
+    camp.classify(total, cnt)
+    c = cnt.tolist()  # indexed by ABED_DETECTED, _SDC, _MASKED, _DETECTED_BENIGN
+    assert [c[abi.DETECTED], c[abi.DETECTED_BENIGN], c[abi.SDC], c[abi.MASKED]] == counts(whole)
