@@ -157,6 +157,7 @@ struct abed_conv_plan {
   int32_t* d_ficw = nullptr;    // FIC position weights G [phase][c16][Hl*Wl][16] (offline)
   int8_t* d_ficw8 = nullptr;    // G as 3 balanced base-256 digit planes [phase][c16][Hl*Wl][3][16]
   int ficw8_ok = 0;             // every |G| < 2^23 (3 digits are exact)
+  int ficw8_ndig = 3;           // digit planes the FR pass needs (2 when every third digit is 0)
   int8_t* d_ficc8 = nullptr;    // G class table [phase][nrc][ncc][c16][3][16] (FIC-SM)
   uint8_t* d_rowcls = nullptr;  // [nph_h][Hl] / [nph_w][Wl] row / column classes
   uint8_t* d_colcls = nullptr;

@@ -356,7 +356,8 @@ abed_conv_plan* plan_create(const abed_layer_shape& shape, const int8_t* filters
       int big = 0;
       cuda_check(cudaMemcpy(&big, d_big, 4, cudaMemcpyDeviceToHost), "flag d2h");
       cudaFree(d_big);
-      pl->ficw8_ok = big ? 0 : 1;
+      pl->ficw8_ok = (big & 1) ? 0 : 1;
+      pl->ficw8_ndig = (big & 2) ? 3 : 2;  // every |G| within two balanced digits: 8 dp4a per chunk
       cuda_check(cudaGetLastError(), "fic_weight");
       if (pl->ficw8_ok && !pl->h_rep.empty()) build_fic_classes(pl);
     }
@@ -467,6 +468,7 @@ void plan_run(abed_conv_plan* pl, const int8_t* packed, const abed_epilog_params
     // ResNet-50 b32: the 256->64/128 1x1 layers at 56x56 (26 MB inputs) gain ~2 us
     // with 16 loads in flight; the <= 7 MB inputs lose ~0.4 us (tools/r50net_layer_times.py)
     p.rhs_deep = geom_packed_bytes(g) >= (int64_t(16) << 20) ? 1 : 0;
+    p.g_ndig = pl->ficw8_ndig;
     return (int)std::max<int64_t>(1, std::min<int64_t>(g.n, (want + cells - 1) / cells));
   };
   if (!fmode && pl->af_input && (pl->checks & ABED_CHECK_FIC) && !pl->reuse_input_checksum) {

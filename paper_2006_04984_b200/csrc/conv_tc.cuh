@@ -120,6 +120,7 @@ struct ConvTcParams {
                                //    (ic_S; FIC's rhs then comes from ic at the verdict)
   int rhs_nsplit;              // image split of the rhs work items
   int rhs_deep;                // int8 FR: 16 image loads in flight per item (large inputs) instead of 8
+  int g_ndig;                  // int8 FR: G digit planes dotted (2 when every third digit is zero, else 3)
   int conv_grid;               // CTAs running conv work units (blockIdx < conv_grid)
   int ic_ctas;                 // extra CTAs (blockIdx >= conv_grid) that only compute the FR
                                // input checksum on SMs the conv grid leaves idle (0: the conv

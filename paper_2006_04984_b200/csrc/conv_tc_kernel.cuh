@@ -43,6 +43,7 @@ namespace abed_dev {
 
 constexpr int kEpiWarps = 8;
 constexpr int kEpiParts = kEpiWarps / 4;  // epilogue warps per TMEM lane quarter
+constexpr int kMaxAcc = 2 * kEpiParts;     // TMEM accumulator stages (unit-interleaved epilogue)
 constexpr int kEpiThreads = kEpiWarps * 32;
 constexpr int kRhsWarps = 2;
 constexpr int kConvThreads = 64 + kEpiThreads + kRhsWarps * 32;
@@ -70,7 +71,7 @@ __host__ __device__ inline SmemLayout smem_layout(const ConvTcParams& p) {
   off += p.b_resident ? p.b_stage_bytes * p.k_stages : p.b_stage_bytes * p.n_stages;
   off = (off + 127u) & ~127u;
   L.bar_off = off;
-  off += 8 * (2 * kStages + 5) + 16;
+  off += 8 * (2 * kStages + 2 * kMaxAcc + 1) + 16;
   L.tab_off = off;  // per-stage MMA operand offset table (uint2 per MMA)
   off += 8u * p.ntaps * (p.gps / 2);
   off = (off + 15u) & ~15u;
@@ -693,6 +694,59 @@ __device__ __forceinline__ void mma_warp_run(const ConvTcParams& p, const MmaEnv
   }
 }
 
+// int8 FR pass body: items first, first + stride, ... of (plane, pixel, image
+// split); per item the NDIG balanced base-256 digit planes of G for the pixel are
+// loaded once and dotted (dp4a) with the pixel's 16 channels of every image of
+// the split, DEPTH image loads in flight.  NDIG = 2 when every third digit of the
+// plan's G is zero (8 instead of 12 dp4a per 16-byte chunk; exact either way).
+template <int DEPTH, int NDIG>
+__device__ __forceinline__ void fic_rhs_fr_i8(const ConvTcParams& p, int64_t first, int64_t stride, long long& acc) {
+  const int64_t HlWl = static_cast<int64_t>(p.Hl) * p.Wl;
+  const int nsplit = p.rhs_nsplit;
+  const int64_t total = static_cast<int64_t>(p.n_phase) * p.c16 * HlWl * nsplit;
+  for (int64_t idx = first; idx < total; idx += stride) {
+    const int64_t pix = idx % HlWl;
+    const int64_t rest = idx / HlWl;
+    const int split = static_cast<int>(rest % nsplit);
+    const int64_t plane = rest / nsplit;
+    const uint4* gw = reinterpret_cast<const uint4*>(p.ficw8) + (plane * HlWl + pix) * 3;
+    const uint4 g0 = __ldg(gw), g1 = __ldg(gw + 1);
+    const uint4 g2 = NDIG == 3 ? __ldg(gw + 2) : make_uint4(0u, 0u, 0u, 0u);
+    const uint4* src = reinterpret_cast<const uint4*>(p.act) + plane * p.plane_len + pix;
+    const int n0 = static_cast<int>(static_cast<int64_t>(p.N) * split / nsplit);
+    const int n1 = static_cast<int>(static_cast<int64_t>(p.N) * (split + 1) / nsplit);
+    int32_t d0 = 0, d1 = 0, d2 = 0;  // |sum| <= 32 images * 16 * 128 * 128 < 2^31
+    for (int n = n0; n < n1; n += DEPTH) {  // DEPTH image loads in flight
+      uint4 x[DEPTH];
+#pragma unroll
+      for (int j = 0; j < DEPTH; ++j)
+        x[j] = n + j < n1 ? __ldcg(src + static_cast<int64_t>(n + j) * HlWl) : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+      for (int j = 0; j < DEPTH; ++j) {
+        d0 = __dp4a(static_cast<int>(x[j].x), static_cast<int>(g0.x), d0);
+        d0 = __dp4a(static_cast<int>(x[j].y), static_cast<int>(g0.y), d0);
+        d0 = __dp4a(static_cast<int>(x[j].z), static_cast<int>(g0.z), d0);
+        d0 = __dp4a(static_cast<int>(x[j].w), static_cast<int>(g0.w), d0);
+        d1 = __dp4a(static_cast<int>(x[j].x), static_cast<int>(g1.x), d1);
+        d1 = __dp4a(static_cast<int>(x[j].y), static_cast<int>(g1.y), d1);
+        d1 = __dp4a(static_cast<int>(x[j].z), static_cast<int>(g1.z), d1);
+        d1 = __dp4a(static_cast<int>(x[j].w), static_cast<int>(g1.w), d1);
+        if (NDIG == 3) {
+          d2 = __dp4a(static_cast<int>(x[j].x), static_cast<int>(g2.x), d2);
+          d2 = __dp4a(static_cast<int>(x[j].y), static_cast<int>(g2.y), d2);
+          d2 = __dp4a(static_cast<int>(x[j].z), static_cast<int>(g2.z), d2);
+          d2 = __dp4a(static_cast<int>(x[j].w), static_cast<int>(g2.w), d2);
+        }
+      }
+      if (((n - n0) & 31) == 32 - DEPTH) {  // keep the digit sums inside int32
+        acc += static_cast<long long>(d0) + (static_cast<long long>(d1) << 8) + (static_cast<long long>(d2) << 16);
+        d0 = d1 = d2 = 0;
+      }
+    }
+    acc += static_cast<long long>(d0) + (static_cast<long long>(d1) << 8) + (static_cast<long long>(d2) << 16);
+  }
+}
+
 // FIC rhs, FR option: sum over the stored input of x * G (checksum.hpp:248-285
 // gen_input_checksum + fic_dot restated as one pass), work items
 // first, first + stride, ... of (plane, pixel, image split).  int8: G as three
@@ -747,47 +801,10 @@ __device__ __forceinline__ void fic_rhs_fr(const ConvTcParams& p, int64_t first,
       facc_rhs += static_cast<double>(item);
     }
   } else {
-    const int64_t HlWl = static_cast<int64_t>(p.Hl) * p.Wl;
-    const int nsplit = p.rhs_nsplit;
-    const int64_t total = static_cast<int64_t>(p.n_phase) * p.c16 * HlWl * nsplit;
-    for (int64_t idx = first; idx < total; idx += stride) {
-      const int64_t pix = idx % HlWl;
-      const int64_t rest = idx / HlWl;
-      const int split = static_cast<int>(rest % nsplit);
-      const int64_t plane = rest / nsplit;
-      const uint4* gw = reinterpret_cast<const uint4*>(p.ficw8) + (plane * HlWl + pix) * 3;
-      const uint4 g0 = __ldg(gw), g1 = __ldg(gw + 1), g2 = __ldg(gw + 2);
-      const uint4* src = reinterpret_cast<const uint4*>(p.act) + plane * p.plane_len + pix;
-      const int n0 = static_cast<int>(static_cast<int64_t>(p.N) * split / nsplit);
-      const int n1 = static_cast<int>(static_cast<int64_t>(p.N) * (split + 1) / nsplit);
-      int32_t d0 = 0, d1 = 0, d2 = 0;  // |sum| <= 32 images * 16 * 128 * 128 < 2^31
-      for (int n = n0; n < n1; n += DEPTH) {  // DEPTH image loads in flight
-        uint4 x[DEPTH];
-#pragma unroll
-        for (int j = 0; j < DEPTH; ++j)
-          x[j] = n + j < n1 ? __ldcg(src + static_cast<int64_t>(n + j) * HlWl) : make_uint4(0u, 0u, 0u, 0u);
-#pragma unroll
-        for (int j = 0; j < DEPTH; ++j) {
-          d0 = __dp4a(static_cast<int>(x[j].x), static_cast<int>(g0.x), d0);
-          d0 = __dp4a(static_cast<int>(x[j].y), static_cast<int>(g0.y), d0);
-          d0 = __dp4a(static_cast<int>(x[j].z), static_cast<int>(g0.z), d0);
-          d0 = __dp4a(static_cast<int>(x[j].w), static_cast<int>(g0.w), d0);
-          d1 = __dp4a(static_cast<int>(x[j].x), static_cast<int>(g1.x), d1);
-          d1 = __dp4a(static_cast<int>(x[j].y), static_cast<int>(g1.y), d1);
-          d1 = __dp4a(static_cast<int>(x[j].z), static_cast<int>(g1.z), d1);
-          d1 = __dp4a(static_cast<int>(x[j].w), static_cast<int>(g1.w), d1);
-          d2 = __dp4a(static_cast<int>(x[j].x), static_cast<int>(g2.x), d2);
-          d2 = __dp4a(static_cast<int>(x[j].y), static_cast<int>(g2.y), d2);
-          d2 = __dp4a(static_cast<int>(x[j].z), static_cast<int>(g2.z), d2);
-          d2 = __dp4a(static_cast<int>(x[j].w), static_cast<int>(g2.w), d2);
-        }
-        if (((n - n0) & 31) == 32 - DEPTH) {  // keep the digit sums inside int32
-          acc += static_cast<long long>(d0) + (static_cast<long long>(d1) << 8) + (static_cast<long long>(d2) << 16);
-          d0 = d1 = d2 = 0;
-        }
-      }
-      acc += static_cast<long long>(d0) + (static_cast<long long>(d1) << 8) + (static_cast<long long>(d2) << 16);
-    }
+    if (p.g_ndig == 2)
+      fic_rhs_fr_i8<DEPTH, 2>(p, first, stride, acc);
+    else
+      fic_rhs_fr_i8<DEPTH, 3>(p, first, stride, acc);
   }
 }
 
@@ -1008,9 +1025,9 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
   uint64_t* full = bars;
   uint64_t* empty = bars + kStages;
   uint64_t* tfull = bars + 2 * kStages;
-  uint64_t* tempty = bars + 2 * kStages + 2;
-  uint64_t* bres = bars + 2 * kStages + 4;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 5);
+  uint64_t* tempty = bars + 2 * kStages + kMaxAcc;
+  uint64_t* bres = bars + 2 * kStages + 2 * kMaxAcc;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 2 * kMaxAcc + 1);
   __shared__ __align__(16) float s_bias[kBiasSmem];
   __shared__ FcRec s_fc[kEpiWarps];
   __shared__ long long s_lhs[kEpiWarps];
@@ -1072,9 +1089,20 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
     trace[1] = t_entry;
   }
 
-  // accumulator stages: columns per stage (multiple of 32), 2 stages when they fit
+  // accumulator stages: columns per stage (multiple of 32), 2 stages when they fit.
+  // Narrow int8 tiles (<= 64 output channels: ResNet-50 layer1 class) interleave
+  // units across the epilogue warps of a lane quarter instead of splitting the
+  // columns: each warp drains whole units (all channels of its 32 rows), the
+  // kEpiParts warps of a quarter take alternate units, so two units' tcgen05.ld
+  // latency and requantise overlap; kEpiParts + 1 .. 2 * kEpiParts stages keep
+  // the MMA warp fed.
+  // (Splitting 64 columns over 2 warps left each warp one 32-column load per unit
+  // with its latency fully exposed: the epilogue set the pace at ~2.1K cycles/unit;
+  // layer1 b1024 FIC 244 -> 182 us, b32 12.5 -> 11.1 us.  For 128-column tiles the
+  // interleave measured no gain at b1024 and a loss at b32, so they keep the split.)
   const int acc_cols = (p.block_n_tot + 31) & ~31;
-  const int n_acc = (2 * acc_cols <= 512) ? 2 : 1;
+  const bool alt = DT == DT_I8 && p.block_n <= 64 && (kEpiParts + 1) * acc_cols <= 512 && !(p.dbg & 512);
+  const int n_acc = alt ? min(kMaxAcc, 512 / acc_cols) : (2 * acc_cols <= 512) ? 2 : 1;
   uint32_t tmem_cols = 32;
   while (tmem_cols < static_cast<uint32_t>(n_acc * acc_cols)) tmem_cols <<= 1;
 
@@ -1086,9 +1114,9 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], rhs_staged ? 1 + kRhsWarps : 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < n_acc; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], kEpiWarps);
+      mbar_init(&tempty[i], alt ? 4 : kEpiWarps);  // alt: one warp per lane quarter drains a unit
     }
     mbar_init(bres, 1);
     if (rhs_staged) mbar_init(reinterpret_cast<uint64_t*>(smem + L.fic_off + p.fic_smem), 1);
@@ -1271,7 +1299,9 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
     e.af_gstride = p.af_HlWl * 3;
     long long tr_wait = 0, tr_acc = 0, tr_proc = 0;  // diagnostics (registers)
     const int nch = p.block_n >> 4;  // 16-column chunks of real output channels
-    const int c_lo = (nch * part) / kEpiParts, c_hi = (nch * (part + 1)) / kEpiParts;
+    // alt: this warp drains units part, part + kEpiParts, ... with all the chunks
+    const int c_lo = alt ? 0 : (nch * part) / kEpiParts, c_hi = alt ? nch : (nch * (part + 1)) / kEpiParts;
+    const int u_first = alt ? part : 0, u_step = alt ? kEpiParts : 1;
     // per-unit coordinates without integer division: exact float-reciprocal
     // quotients (every operand < 2^24), shifts for the 1/2-strided consumer
     const float rcp_hlwl = 1.0f / static_cast<float>(HlWl), rcp_wl = 1.0f / static_cast<float>(p.Wl);
@@ -1283,7 +1313,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
     };
     const bool o_pow2 = (p.o_sh == 1 || p.o_sh == 2) && (p.o_sw == 1 || p.o_sw == 2);
     const int o_shh = p.o_sh == 2 ? 1 : 0, o_shw = p.o_sw == 2 ? 1 : 0;
-    for (int u = 0; u < n_units; ++u) {
+    for (int u = u_first; u < n_units; u += u_step) {
       int mt, nt;
       decode_tile(p, u, mt, nt);
       const uint32_t m = static_cast<uint32_t>(mt) * kBlockM + row;
@@ -1353,7 +1383,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
       const int k_base = nt * p.block_n;
       // FC checksum digits ride in the 16 columns after the tile's channels
       uint32_t dig[4] = {0u, 0u, 0u, 0u};
-      if (FC && part == 0) tmem_ld4(t_row + p.block_n, dig);
+      if (FC && (alt || part == 0)) tmem_ld4(t_row + p.block_n, dig);
       // fast path: no fault hook, no filler channels, no IC column sums (warp-uniform)
       const bool slow = p.fault_key >= 0 || k_base + c_hi * 16 > p.K;
       // IC column sums / ICBatch batch sums on the fast path (int8 plans only)
@@ -1390,12 +1420,16 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
       if (!valid) row_sum = 0;
       if (FIC) fic_sum += row_sum;
       if (FC) {
-        // combine the two column halves of each row
-        if (part > 0) s_rowsum[part - 1][row] = acc_bits(row_sum);
-        named_bar(kBarQuarter0 + quarter, 32 * kEpiParts);
-        if (part == 0) {
+        // combine the two column halves of each row (alt: this warp has the whole row)
+        if (!alt) {
+          if (part > 0) s_rowsum[part - 1][row] = acc_bits(row_sum);
+          named_bar(kBarQuarter0 + quarter, 32 * kEpiParts);
+        }
+        if (alt || part == 0) {
+          if (!alt) {
 #pragma unroll
-          for (int q = 0; q < kEpiParts - 1; ++q) row_sum += bits_acc<Acc>(s_rowsum[q][row]);
+            for (int q = 0; q < kEpiParts - 1; ++q) row_sum += bits_acc<Acc>(s_rowsum[q][row]);
+          }
           Acc extra = 0;
           if (valid) {
             if constexpr (DT == DT_I8) {
@@ -1457,7 +1491,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
           }
         }
         // s_rowsum reuse guard for the next unit
-        named_bar(kBarQuarter0 + quarter, 32 * kEpiParts);
+        if (!alt) named_bar(kBarQuarter0 + quarter, 32 * kEpiParts);
       }
     }
     if (EPI == EPI_PACKED && DT == DT_I8 && p.af_ficw8) {

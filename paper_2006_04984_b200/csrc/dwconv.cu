@@ -358,7 +358,7 @@ abed_conv_plan* plan_create_dw(const abed_layer_shape& shape, const int8_t* filt
       int big = 0;
       cuda_check(cudaMemcpy(&big, d_big, 4, cudaMemcpyDeviceToHost), "flag d2h");
       cudaFree(d_big);
-      pl->ficw8_ok = big ? 0 : 1;
+      pl->ficw8_ok = (big & 1) ? 0 : 1;  // bit 1: a third digit is needed (unused here)
     }
     cuda_check(cudaMalloc(&pl->d_af_acc, 8), "cudaMalloc(af_acc)");
     cuda_check(cudaMemset(pl->d_af_acc, 0, 8), "memset af_acc");

@@ -535,6 +535,7 @@ __global__ void fic_weight_digits_kernel(const int32_t* __restrict__ G, int64_t 
     v = (v - d0) >> 8;
     const int32_t d1 = ((v + 128) & 255) - 128;
     v = (v - d1) >> 8;
+    if (v != 0) atomicOr(too_big, 2);  // the third digit plane is needed
     G8[(cell * 3 + 0) * 16 + e] = (int8_t)d0;
     G8[(cell * 3 + 1) * 16 + e] = (int8_t)d1;
     G8[(cell * 3 + 2) * 16 + e] = (int8_t)v;
