@@ -22,6 +22,9 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
          "-diag-suppress", "177", "-I", os.path.join(ROOT, "include")]
+# diagnostics builds only (e.g. ABED_NVCC_EXTRA=-DABED_CONV_DEBUG=1 for the conv
+# kernel's timing-experiment flags used by tools/epi_probe.py; rebuild from clean)
+FLAGS += os.environ.get("ABED_NVCC_EXTRA", "").split()
 
 
 def _run(cmd):

@@ -14,6 +14,8 @@ namespace abed_host {
 ABED_EXTERN_DT(abed_dev::DT_I8, 0)
 ABED_EXTERN_DT(abed_dev::DT_I8, 1)
 ABED_EXTERN_DT(abed_dev::DT_I8, 2)
+ABED_EXTERN_EPI(abed_dev::DT_I8, abed_dev::EPI_PACKED, 3)
+ABED_EXTERN_DT(abed_dev::DT_I8, 4)
 ABED_EXTERN_DT(abed_dev::DT_F16, 0)
 ABED_EXTERN_DT(abed_dev::DT_BF16, 0)
 }  // namespace abed_host
@@ -343,7 +345,11 @@ cudaError_t conv_tc_launch(const ConvTcParams& p_in, int num_sms, bool pdl, cuda
     case abed_dev::DT_BF16: return launch_dt<abed_dev::DT_BF16, 0>(p, grid, pdl, stream);
     default:
       if (p.check & abed_dev::CHECK_IC) return launch_dt<abed_dev::DT_I8, 1>(p, grid, pdl, stream);
+      if (p.rhs_mode == 3) return launch_dt<abed_dev::DT_I8, 4>(p, grid, pdl, stream);
       if (p.icb_d) return launch_dt<abed_dev::DT_I8, 2>(p, grid, pdl, stream);
+      // FIC-AF producer: packed output dotted into the next layer's rhs
+      if (p.af_ficw8 && p.out_mode == abed_dev::OUT_I8_PACKED)
+        return launch_epi<abed_dev::DT_I8, abed_dev::EPI_PACKED, 3>(p, grid, pdl, stream);
       return launch_dt<abed_dev::DT_I8, 0>(p, grid, pdl, stream);
   }
 }

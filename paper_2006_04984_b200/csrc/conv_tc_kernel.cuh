@@ -44,6 +44,13 @@ namespace abed_dev {
 constexpr int kEpiWarps = 8;
 constexpr int kEpiParts = kEpiWarps / 4;  // epilogue warps per TMEM lane quarter
 constexpr int kMaxAcc = 2 * kEpiParts;     // TMEM accumulator stages (unit-interleaved epilogue)
+// Timing-experiment flags (ConvTcParams::dbg, tools/epi_probe.py) exist only in a
+// diagnostics build (-DABED_CONV_DEBUG=1): the product kernels carry none of their
+// code (the epilogue's extra copies cost instruction-cache footprint)
+#ifndef ABED_CONV_DEBUG
+#define ABED_CONV_DEBUG 0
+#endif
+__device__ __forceinline__ int dbg_of(const ConvTcParams& p) { return ABED_CONV_DEBUG ? p.dbg : 0; }
 constexpr int kEpiThreads = kEpiWarps * 32;
 constexpr int kRhsWarps = 2;
 constexpr int kConvThreads = 64 + kEpiThreads + kRhsWarps * 32;
@@ -329,12 +336,15 @@ __device__ __forceinline__ int64_t epi_chunk(const ConvTcParams& p, const EpiCtx
   }
   if (XTRA == 1) ic_chunk_sums(p, e.ic_acc, e.valid, a, k0);
   if (XTRA == 2) icb_chunk<SLOW>(p, e, a, k0);
+  // the slow path (fault hook, filler channels) is one copy with the activation
+  // read at run time; the fast path has one copy per activation
+  const bool relu = SLOW ? p.relu != 0 : RELU;
   if (EPI == EPI_PACKED || EPI == EPI_COMPARE) {
     int32_t y[16];
-    if (p.dbg & 16) {  // timing experiment: skip the requantise math
+    if (dbg_of(p) & 16) {  // timing experiment: skip the requantise math
 #pragma unroll
       for (int j = 0; j < 16; ++j) y[j] = a[j];
-    } else if (RELU) {
+    } else if (relu) {
 #pragma unroll
       for (int j = 0; j < 16; j += 2) requant_relu_pair(a[j], a[j + 1], p.scale, b[j], b[j + 1], y[j], y[j + 1]);
     } else {
@@ -352,7 +362,7 @@ __device__ __forceinline__ int64_t epi_chunk(const ConvTcParams& p, const EpiCtx
     if (EPI == EPI_PACKED) {
       if (e.valid) {
         *dst = val;
-        if (e.af_row) {  // FIC-AF: the next layer's rhs from the stored values (12 dp4a)
+        if (XTRA != 0 && e.af_row) {  // FIC-AF: the next layer's rhs from the stored values (12 dp4a)
           const uint4* gd = e.af_row + static_cast<int64_t>(k0 >> 4) * e.af_gstride;
           const uint4 g0 = __ldg(gd), g1 = __ldg(gd + 1), g2 = __ldg(gd + 2);
           int32_t d0 = 0, d1 = 0, d2 = 0;
@@ -385,13 +395,13 @@ __device__ __forceinline__ int64_t epi_chunk(const ConvTcParams& p, const EpiCtx
       } else if (p.out_mode == OUT_I8_NCHW) {
         int8_t* o = static_cast<int8_t*>(p.out) + base;
         for (int j = 0; j < 16; ++j)
-          if (k0 + j < p.K) o[j * e.PQ] = static_cast<int8_t>(requant_i8(a[j], p.scale, b[j], RELU ? 1 : 0));
+          if (k0 + j < p.K) o[j * e.PQ] = static_cast<int8_t>(requant_i8(a[j], p.scale, b[j], relu ? 1 : 0));
       } else {  // OUT_F32_NCHW
         float* o = static_cast<float*>(p.out) + base;
         for (int j = 0; j < 16; ++j)
           if (k0 + j < p.K) {
             float f = __fmaf_rn(static_cast<float>(a[j]), p.scale, b[j]);
-            if (RELU && f < 0.0f) f = 0.0f;
+            if (relu && f < 0.0f) f = 0.0f;
             o[j * e.PQ] = f;
           }
       }
@@ -608,7 +618,7 @@ __device__ __forceinline__ void mma_warp_run(const ConvTcParams& p, const MmaEnv
     for (int u = 0; u < v.n_units; ++u) {
       const int as = u % v.n_acc;
       const uint32_t aphase = static_cast<uint32_t>(u / v.n_acc) & 1u;
-      if (p.dbg & 8) {
+      if (dbg_of(p) & 8) {
       } else if (v.trace) {
         const long long w0 = clock64();
         mbar_wait(&v.tempty[as], aphase ^ 1u);
@@ -677,7 +687,7 @@ __device__ __forceinline__ void mma_warp_run(const ConvTcParams& p, const MmaEnv
           phase ^= 1u;
         }
       }
-      if (!(p.dbg & 8) || u >= v.n_units - 2) mma_commit_w(&v.tfull[as]);
+      if (!(dbg_of(p) & 8) || u >= v.n_units - 2) mma_commit_w(&v.tfull[as]);
       if (v.trace && u == v.n_units - 1) {
         tr_last = clock64() - v.t_entry;
         uint64_t gt_;
@@ -1101,14 +1111,14 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
   // layer1 b1024 FIC 244 -> 182 us, b32 12.5 -> 11.1 us.  For 128-column tiles the
   // interleave measured no gain at b1024 and a loss at b32, so they keep the split.)
   const int acc_cols = (p.block_n_tot + 31) & ~31;
-  const bool alt = DT == DT_I8 && p.block_n <= 64 && (kEpiParts + 1) * acc_cols <= 512 && !(p.dbg & 512);
+  const bool alt = DT == DT_I8 && p.block_n <= 64 && (kEpiParts + 1) * acc_cols <= 512 && !(dbg_of(p) & 512);
   const int n_acc = alt ? min(kMaxAcc, 512 / acc_cols) : (2 * acc_cols <= 512) ? 2 : 1;
   uint32_t tmem_cols = 32;
   while (tmem_cols < static_cast<uint32_t>(n_acc * acc_cols)) tmem_cols <<= 1;
 
   // FIC-SM: the input-checksum warps read every A stage too, so a stage is free
   // once the MMA commit and each of them have arrived
-  const bool rhs_staged = DT == DT_I8 && FIC && p.rhs_mode == 3;
+  const bool rhs_staged = DT == DT_I8 && FIC && XT == 4 && p.rhs_mode == 3;
   if (threadIdx.x == 0) {
     for (int i = 0; i < kStages; ++i) {
       mbar_init(&full[i], 1);
@@ -1137,7 +1147,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
   // FR input checksum shared by every warp that has finished its role (dbg 256: off)
   // float mode only: on int8 layers the claims of the producer / MMA warps slowed the
   // epilogue-bound CTAs (ResNet-50 layer1 FIC 12.3 -> 13.4 us); VGG-16 FP16 FIC 18% -> 11%
-  const bool fr_share = DT != DT_I8 && FIC && p.rhs_mode == 1 && p.ic_ctas == 0 && !(p.dbg & 256);
+  const bool fr_share = DT != DT_I8 && FIC && p.rhs_mode == 1 && p.ic_ctas == 0 && !(dbg_of(p) & 256);
   long long fr_acc = 0;
   double fr_facc = 0.0;
   if (trace && threadIdx.x == 0) trace[2] = clock64() - t_entry;
@@ -1357,7 +1367,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
         const int64_t t = (static_cast<int64_t>(n_img) * p.o_Hl + hq) * p.o_Wl + wq;
         e.pk_row = static_cast<int8_t*>(p.out) +
                    (static_cast<int64_t>(a_ph * p.o_nph_w + b_ph) * p.o_c16 * p.o_plane_len + t) * 16;
-        if (EPI == EPI_PACKED && DT == DT_I8 && p.af_ficw8)
+        if (EPI == EPI_PACKED && DT == DT_I8 && XT != 0 && p.af_ficw8)
           e.af_row = reinterpret_cast<const uint4*>(p.af_ficw8) +
                      (static_cast<int64_t>(a_ph * p.o_nph_w + b_ph) * p.o_c16 * p.af_HlWl +
                       static_cast<int64_t>(hq) * p.o_Wl + wq) * 3;
@@ -1367,7 +1377,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
 
       const int as = u % n_acc;
       const uint32_t uphase = static_cast<uint32_t>(u / n_acc) & 1u;
-      if ((p.dbg & 8) && u < n_units - 2) continue;
+      if ((dbg_of(p) & 8) && u < n_units - 2) continue;
       long long t_proc = 0;
       if (trace) {
         const long long w0 = clock64();
@@ -1395,19 +1405,19 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
           row_sum = p.relu ? epi_columns<DT, EPI, true, FC || FIC, false, false, xtra>(p, e, t_row, k_base, c_lo, c_hi, af_sum)
                            : epi_columns<DT, EPI, false, FC || FIC, false, false, xtra>(p, e, t_row, k_base, c_lo, c_hi, af_sum);
         else
-          row_sum = p.relu ? epi_columns<DT, EPI, true, FC || FIC, true, false, xtra>(p, e, t_row, k_base, c_lo, c_hi, af_sum)
-                           : epi_columns<DT, EPI, false, FC || FIC, true, false, xtra>(p, e, t_row, k_base, c_lo, c_hi, af_sum);
-      } else if (p.dbg & 1) {
-      } else if (!slow) {
-        if (p.dbg & 64)
-          row_sum = epi_columns<DT, EPI, true, false, false>(p, e, t_row, k_base, c_lo, c_hi, af_sum);
-        else if (DT == DT_I8 && (FC || FIC) && e.chunk32)
-          row_sum = p.relu
-                        ? epi_columns<DT, EPI, true, FC || FIC, false, true>(p, e, t_row, k_base, c_lo, c_hi, af_sum)
-                        : epi_columns<DT, EPI, false, FC || FIC, false, true>(p, e, t_row, k_base, c_lo, c_hi, af_sum);
-        else
-          row_sum = p.relu ? epi_columns<DT, EPI, true, FC || FIC, false>(p, e, t_row, k_base, c_lo, c_hi, af_sum)
-                           : epi_columns<DT, EPI, false, FC || FIC, false>(p, e, t_row, k_base, c_lo, c_hi, af_sum);
+          row_sum = epi_columns<DT, EPI, false, FC || FIC, true, false, xtra>(p, e, t_row, k_base, c_lo, c_hi, af_sum);
+      } else if (dbg_of(p) & 1) {
+      } else if (dbg_of(p) & 64) {
+        row_sum = epi_columns<DT, EPI, true, false, false>(p, e, t_row, k_base, c_lo, c_hi, af_sum);
+      } else if (!slow && !(DT == DT_I8 && (FC || FIC) && !e.chunk32)) {
+        // ONE fast copy of the drain loop per activation (int8 checked plans: int32
+        // chunk sums, exact for CRS < 8192; larger CRS take the general path) --
+        // every extra copy of this loop in the kernel cost instruction-cache misses
+        constexpr bool kC32 = DT == DT_I8 && (FC || FIC);
+        row_sum = p.relu ? epi_columns<DT, EPI, true, FC || FIC, false, kC32>(p, e, t_row, k_base, c_lo, c_hi, af_sum)
+                         : epi_columns<DT, EPI, false, FC || FIC, false, kC32>(p, e, t_row, k_base, c_lo, c_hi, af_sum);
+      } else if constexpr (DT == DT_I8) {
+        row_sum = epi_columns<DT, EPI, false, FC || FIC, true>(p, e, t_row, k_base, c_lo, c_hi, af_sum);
       } else {
         row_sum = p.relu ? epi_columns<DT, EPI, true, FC || FIC, true>(p, e, t_row, k_base, c_lo, c_hi, af_sum)
                          : epi_columns<DT, EPI, false, FC || FIC, true>(p, e, t_row, k_base, c_lo, c_hi, af_sum);
@@ -1494,7 +1504,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
         if (!alt) named_bar(kBarQuarter0 + quarter, 32 * kEpiParts);
       }
     }
-    if (EPI == EPI_PACKED && DT == DT_I8 && p.af_ficw8) {
+    if (EPI == EPI_PACKED && DT == DT_I8 && XT != 0 && p.af_ficw8) {
       // FIC-AF partial of this warp straight into the next layer's accumulator
       // (fire-and-forget reduction; the next layer's verdict reads and resets it)
       const long long w = warp_sum(af_sum);
@@ -1606,7 +1616,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
         }
         for (int ks = 0; ks < p.k_stages; ++ks) {
           mbar_wait(&full[stage], sphase);
-          if (own && !(p.dbg & 128)) {  // dbg bit 7: timing experiment, stages released unread
+          if (own && !(dbg_of(p) & 128)) {  // dbg bit 7: timing experiment, stages released unread
             const uint8_t* sa = sA + stage * L.a_stage_bytes;
             int32_t d0 = 0, d1 = 0, d2 = 0;  // <= 4 phases * 4 groups * kPx chunks: |d| < 2^27
 #pragma unroll
@@ -1709,7 +1719,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_i8_tc_kernel(const __gri
   // (one small launch per plan, or per pass of many layers) reduces them.  A
   // last-CTA reduction in this kernel would hold every CTA at exit for a ticket
   // atomic round trip (measured: ~2.5 us per layer on the critical path).
-  if ((FC || FIC) && !(p.dbg & 32) && threadIdx.x == 0) {
+  if ((FC || FIC) && !(dbg_of(p) & 32) && threadIdx.x == 0) {
     int64_t* rec = p.cta_rec + static_cast<int64_t>(blockIdx.x) * kCtaRec;
     if (FC) {
       FcRec r{0, kNoKey, 0, 0};
@@ -1783,12 +1793,18 @@ cudaError_t launch_variant(const ConvTcParams& p, int grid, bool pdl, cudaStream
   return cudaLaunchKernelEx(&cfg, kern, p);
 }
 
-// XT: 0 = no per-channel extras, 1 = IC column sums, 2 = ICBatch batch sums
+// XT: 0 = no per-channel extras, 1 = IC column sums, 2 = ICBatch batch sums,
+// 3 = FIC-AF producer (the next layer's rhs dotted from the stored outputs),
+// 4 = FIC with the staged input-checksum source (FIC-SM)
 // (int8 only; separate kernel instances so the FC / FIC / unprotected kernels
-// carry none of their code or registers)
+// carry none of their code or registers: instruction-cache footprint is time)
 template <int DT, int EPI, int XT>
 cudaError_t launch_epi(const ConvTcParams& p, int grid, bool pdl, cudaStream_t st) {
   const bool fc = (p.check & abed_dev::CHECK_FC) != 0, fic = (p.check & abed_dev::CHECK_FIC) != 0;
+  if constexpr (XT == 4) {  // FIC with the staged input-checksum source
+    if (fc) return launch_variant<DT, EPI, true, true, XT>(p, grid, pdl, st);
+    return launch_variant<DT, EPI, false, true, XT>(p, grid, pdl, st);
+  }
   if (fc && fic) return launch_variant<DT, EPI, true, true, XT>(p, grid, pdl, st);
   if (fc) return launch_variant<DT, EPI, true, false, XT>(p, grid, pdl, st);
   if (fic) return launch_variant<DT, EPI, false, true, XT>(p, grid, pdl, st);

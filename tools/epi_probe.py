@@ -1,5 +1,7 @@
 """Attribute one bench layer's kernel time with the conv kernel's timing-experiment
-flags (abed_debug_set_conv_trace flags; results are NOT valid outputs):
+flags (abed_debug_set_conv_trace flags; results are NOT valid outputs).  The flags
+exist only in a diagnostics build: rm -rf build && ABED_NVCC_EXTRA=-DABED_CONV_DEBUG=1
+python -c "from paper_2006_04984_b200 import _build; _build.build()".  Flags:
   0 normal, 1 epilogue skips the TMEM->register->store work, 16 skips only the
   requantise math, 8 MMA-only (epilogue / commits of all but the last 2 units
   skipped).  Per flag: graph of R back-to-back launches after an L2 flush, CUDA
