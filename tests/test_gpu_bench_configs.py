@@ -8,10 +8,10 @@ reference headers, detail::conv_fast_i8 + epilog, convolution.hpp:224,353):
 * BASELINE configs[1]: all 16 ResNet-50 3x3 layers at batch 32, SplitMix64 data
   with the bench's seeds, scale 0.05, bias linspace(-2, 2), ReLU, int8 written
   into the packed layout (OUT_I8_PACKED) -- unprotected, FC, FIC (FR), FIC-SM
-  (staged source) and ICBatch; FC/FIC/ICBatch verdicts must pass and FIC's
+  (staged source), IC and ICBatch; FC/FIC/IC/ICBatch verdicts must pass and FIC's
   lhs = rhs = the reference's sum of the ConvOut;
-* BASELINE configs[4] at one GPU: three layers (stride 2, two N tiles, eight N
-  tiles / streamed filters) at batch 1024;
+* BASELINE configs[4] at one GPU: four layers (64 channels, stride 2, two N
+  tiles, eight N tiles / streamed filters) at batch 1024;
 * BASELINE configs[2]: VGG-16 conv1_2 / conv3_1 / conv5_1 at batch 64 in fp16
   and bf16 against an f64 conv of the rounded operands within the stated
   tolerance (|y - y_ref| <= 2^(1-p) |y_ref| + 2^-19 sum|x f|, p = 11 for fp16,
@@ -118,6 +118,7 @@ VARIANTS = {
     "fic": (abi.CHECK_FIC, abi.RHS_REREAD),
     "fic_sm": (abi.CHECK_FIC, abi.RHS_STAGED),
     "icbatch": (abi.CHECK_ICBATCH, None),
+    "ic": (abi.CHECK_IC, None),
 }
 
 
@@ -151,7 +152,7 @@ def check_variants(res, want_y, conv_sum):
             assert oc[0].status == 0, name
         if checks & abi.CHECK_FIC:
             assert oc[1].status == 0 and oc[1].lhs == oc[1].rhs == conv_sum, (name, oc[1].lhs, oc[1].rhs, conv_sum)
-        if checks & abi.CHECK_ICBATCH:
+        if checks & (abi.CHECK_ICBATCH | abi.CHECK_IC):
             assert oc[2].status == 0 and oc[2].error_count == 0, name
 
 
@@ -168,7 +169,9 @@ def test_resnet50_b32_layer(ref, li):
     check_variants(res, want, int(conv.astype(np.int64).sum()))
 
 
-B1024 = [3, 8, 14]  # layer2.0 (stride 2, 4 phases), layer3.1 (2 N tiles), layer4.1 (streamed B, 8 N tiles)
+# layer1.0 (64 channels: unit-interleaved epilogue), layer2.0 (stride 2, 4 phases),
+# layer3.1 (2 N tiles), layer4.1 (streamed B, 8 N tiles)
+B1024 = [0, 3, 8, 14]
 
 
 @pytest.mark.parametrize("li", B1024, ids=[f"{RESNET50_3X3[i][0]}-b1024" for i in B1024])
@@ -180,7 +183,7 @@ def test_resnet50_b1024_layer(ref, li):
     xh, fh = x.cpu().numpy(), f.cpu().numpy()
     conv = ref_conv(ref, xh, fh, ls)
     want = ref_epilog(ref, conv, 0.05, np.asarray(bias, np.float32))
-    res = run_bench_variants(ls, x, f, bias, ("unprotected", "fic", "icbatch"))
+    res = run_bench_variants(ls, x, f, bias, ("unprotected", "fc", "fic", "icbatch"))
     check_variants(res, want, int(conv.astype(np.int64).sum()))
 
 

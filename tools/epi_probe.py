@@ -31,6 +31,8 @@ def main():
     ap.add_argument("--checks", type=int, default=0)
     ap.add_argument("--flags", default="0,1,16,8")
     ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--reuse", action="store_true",
+                    help="FIC: keep the first run's input checksum (no in-kernel input pass)")
     a = ap.parse_args()
     name, c, h, w, k, st = RESNET50_3X3[a.layer]
     ls = api.layer_shape(a.batch, c, h, w, k, 3, 3, st, st, 1, 1)
@@ -48,6 +50,10 @@ def main():
         abi.call("abed_debug_set_conv_trace", plan.handle, None, fl)
         with torch.cuda.stream(stream):
             plan.run(packed, out, abi.OUT_I8_PACKED, ep=ep)
+            if a.checks:
+                plan.finalize()
+            if a.reuse:
+                abi.call("abed_conv_plan_set_reuse_input_checksum", plan.handle, 1)
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=stream):
@@ -65,7 +71,7 @@ def main():
                 ts.append(e0.elapsed_time(e1) * 1e3 / a.reps)
         res[fl] = round(statistics.mean(ts), 2)
     ops = 2.0 * ls.n * ls.k * ls.p * ls.q * ls.c * 9
-    print(name, "batch", a.batch, "checks", a.checks, {f"flags{k_}": v for k_, v in res.items()},
+    print(name, "batch", a.batch, "checks", a.checks, "reuse" if a.reuse else "", {f"flags{k_}": v for k_, v in res.items()},
           "TOPS@flags0", round(ops / (res[min(res)] * 1e-6) / 1e12, 1) if 0 in res else None)
 
 
