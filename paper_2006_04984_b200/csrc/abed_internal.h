@@ -69,13 +69,12 @@ __global__ void fc_finalize_part2_kernel(const int64_t* part, abed_dev::ActGeom 
                                          const unsigned long long* scratch, abed_verify_outcome* out);
 __global__ void fic_finalize_kernel(const int64_t* part, int n, const unsigned long long* rhs_p,
                                     abed_verify_outcome* out);
-// IC: ic[c,r,s] (and FIC's rhs when fic_rhs != nullptr) from the in-kernel class sums
-void ic_from_classes_launch(const int64_t* S, const uint64_t* rowmask, const uint64_t* colmask,
-                            const abed_dev::ActGeom& g, int nrc, int ncc, const int32_t* fsum, int32_t* ic,
-                            unsigned long long* fic_rhs, cudaStream_t st);
 // IC verdicts of many plans (two launches): ic from the class sums (S == nullptr:
 // computed ahead), FIC rhs when fic_rhs != nullptr, then ic_verify_k
 struct IcVerdictJob {
+  int copy_only;                  // finalize again without a run: repeat the stored outcome
+  abed_verify_outcome* last;      // plan-owned copy of the last outcome
+  int64_t S_len;                  // class sums to zero after use (S != nullptr)
   const int64_t* S;
   const uint64_t* rowmask;
   const uint64_t* colmask;
@@ -83,7 +82,7 @@ struct IcVerdictJob {
   const int32_t* fsum;
   int32_t* ic;
   unsigned long long* fic_rhs;
-  const unsigned long long* ksum;
+  unsigned long long* ksum;        // consumed and zeroed
   const int8_t* f;
   int64_t K, crs;
   unsigned long long* scr;
@@ -94,9 +93,6 @@ struct IcVerdictBatch {
   IcVerdictJob job[kMaxIcJobs];
 };
 void ic_verdict_many_launch(const IcVerdictJob* jobs, int n, cudaStream_t st);
-// ic_verify_k verdict: scr = plan-owned {count, first k (init ~0), ticket, -, dot[K]}
-void ic_finalize_launch(const unsigned long long* ksum, const int8_t* f, const int32_t* ic, int64_t K, int64_t crs,
-                        unsigned long long* scr, abed_verify_outcome* out, cudaStream_t st);
 
 // conv_tc.cu
 uint32_t conv_tc_smem_bytes(const abed_dev::ConvTcParams& p);
@@ -190,6 +186,9 @@ struct abed_conv_plan {
   // the pristine input, faults.hpp:111-115)
   int reuse_input_checksum = 0;
   int last_rhs_mode = 0;
+  int ic_pending = 0;                      // IC: a run's in-kernel sums await their verdict
+  abed_verify_outcome* d_ic_last = nullptr;  // IC: last verdict (repeated by a second finalize)
+  unsigned long long cmp_seen = 0;         // compare runs: mismatches already reported
   int last_grid = 0;            // CTAs of the last conv launch (records the verdict reduces)        // rhs_mode of the last run (its verdict reduction needs it)
   // FIC-AF: this layer's FIC rhs is accumulated by the previous layer's epilogue
   // (which is run with next = this plan); the verdict consumes and resets it

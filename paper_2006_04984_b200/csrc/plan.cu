@@ -754,105 +754,12 @@ __global__ void fic_finalize_kernel(const int64_t* __restrict__ part, int n, con
   }
 }
 
-// IC input checksum from the in-kernel class sums (rhs_mode 4): thread per
-// (c, r, s) of gen_input_checksum (checksum.hpp:248-266): ic[c,r,s] = sum of
-// S[phase(r,s)][rc][cc][c] over the row classes whose filter-row mask holds r and
-// the column classes whose mask holds s; also FIC's rhs = sum fsum * ic (fic_dot,
-// :275-285) into *fic_rhs (zeroed by the caller).
-__global__ void ic_from_classes_kernel(const int64_t* __restrict__ S, const uint64_t* __restrict__ rowmask,
-                                       const uint64_t* __restrict__ colmask, ActGeom g, int nrc, int ncc,
-                                       const int32_t* __restrict__ fsum, int32_t* __restrict__ ic,
-                                       unsigned long long* fic_rhs) {
-  const int64_t crs = (int64_t)g.c * g.r * g.s;
-  const int c256 = g.c16 * 16;
-  long long dot = 0;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < crs; t += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(t / (g.r * g.s)), r = (int)((t / g.s) % g.r), sc = (int)(t % g.s);
-    const int a = r % g.sh, b = sc % g.sw, phase = a * g.nph_w + b;
-    long long v = 0;
-    for (int rc = 0; rc < nrc; ++rc) {
-      if (!((rowmask[a * nrc + rc] >> r) & 1ull)) continue;
-      for (int cc = 0; cc < ncc; ++cc)
-        if ((colmask[b * ncc + cc] >> sc) & 1ull) v += S[((int64_t)(phase * nrc + rc) * ncc + cc) * c256 + c];
-    }
-    ic[t] = (int32_t)v;
-    if (fsum) dot += (long long)fsum[t] * v;
-  }
-  if (fic_rhs) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-    if ((threadIdx.x & 31) == 0 && dot != 0) atomicAdd(fic_rhs, (unsigned long long)dot);
-  }
-}
-
-void ic_from_classes_launch(const int64_t* S, const uint64_t* rowmask, const uint64_t* colmask, const ActGeom& g,
-                            int nrc, int ncc, const int32_t* fsum, int32_t* ic, unsigned long long* fic_rhs,
-                            cudaStream_t st) {
-  const int64_t crs = (int64_t)g.c * g.r * g.s;
-  ic_from_classes_kernel<<<(int)std::min<int64_t>((crs + 127) / 128, 4 * num_sms()), 128, 0, st>>>(
-      S, rowmask, colmask, g, nrc, ncc, fsum, ic, fic_rhs);
-}
-
-// IC per-channel (ic_verify_k, checksum.hpp:319-347): out_sum[k] vs
-// dot(f[k,:], ic) in i64, one block per channel (the CRS-long dot split over 256
-// threads); the count and the first mismatching k go to scr = {count, first k,
-// ticket, -, dot[K]}, and the last block writes the outcome and resets scr[0..2].
-__global__ void __launch_bounds__(256) ic_finalize_kernel(const unsigned long long* __restrict__ ksum,
-                                                          const int8_t* __restrict__ f, const int32_t* __restrict__ ic,
-                                                          int64_t K, int64_t crs, unsigned long long* scr,
-                                                          abed_verify_outcome* out) {
-  __shared__ long long s_part[8];
-  __shared__ bool s_last;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int64_t k = blockIdx.x; k < K; k += gridDim.x) {
-    long long dot = 0;
-    for (int64_t i = threadIdx.x; i < crs; i += blockDim.x) dot += (long long)f[k * crs + i] * ic[i];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-    if (lane == 0) s_part[w] = dot;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      long long d = 0;
-      for (int q = 0; q < (int)(blockDim.x >> 5); ++q) d += s_part[q];
-      scr[4 + k] = (unsigned long long)d;
-      if ((long long)ksum[k] != d) {
-        atomicAdd(&scr[0], 1ull);
-        atomicMin(&scr[1], (unsigned long long)k);
-      }
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    __threadfence();
-    s_last = atomicAdd(&scr[2], 1ull) == gridDim.x - 1;
-  }
-  __syncthreads();
-  if (!s_last || threadIdx.x != 0) return;
-  __threadfence();
-  const unsigned long long cnt = __ldcg(&scr[0]);
-  if (cnt == 0) {
-    write_outcome(out, 0, 0, 0, 0, 0, 0, 0, 0);
-  } else {
-    const int64_t k = (int64_t)__ldcg(&scr[1]);
-    write_outcome(out, 1, 1, k, -1, -1, (long long)ksum[k], (long long)__ldcg(&scr[4 + k]), (long long)cnt);
-  }
-  scr[0] = 0ull;
-  scr[1] = ~0ull;
-  scr[2] = 0ull;
-}
-
-void ic_finalize_launch(const unsigned long long* ksum, const int8_t* f, const int32_t* ic, int64_t K, int64_t crs,
-                        unsigned long long* scr, abed_verify_outcome* out, cudaStream_t st) {
-  const int blocks = (int)std::min<int64_t>(K, 4 * num_sms());
-  ic_finalize_kernel<<<blocks, 256, 0, st>>>(ksum, f, ic, K, crs, scr, out);
-}
-
 // IC verdicts of many plans in two launches (blockIdx.y = plan): every plan's
 // ic from its class sums, then every plan's ic_verify_k.  A pass of 16 IC
 // layers was 32 dependent small launches (~25 us per layer of step time).
 __global__ void __launch_bounds__(128) ic_from_classes_many_kernel(const __grid_constant__ IcVerdictBatch b) {
   const IcVerdictJob& j = b.job[blockIdx.y];
-  if (!j.S) return;  // input checksum computed ahead (no class sums)
+  if (j.copy_only || !j.S) return;  // input checksum computed ahead / kept (no class sums)
   const int64_t crs = j.crs;
   const int rs = j.R * j.Sd;
   long long dot = 0;
@@ -880,8 +787,16 @@ __global__ void __launch_bounds__(128) ic_from_classes_many_kernel(const __grid_
 // (ticket) writes the outcome and resets scr
 __global__ void __launch_bounds__(256) ic_finalize_many_kernel(const __grid_constant__ IcVerdictBatch b) {
   const IcVerdictJob& j = b.job[blockIdx.y];
+  if (j.copy_only) {  // a second finalize of the same run
+    if (blockIdx.x == 0 && threadIdx.x == 0) *j.out = *j.last;
+    return;
+  }
   __shared__ bool s_last;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  // the class sums were read by ic_from_classes: zero them for the next run
+  if (j.S)
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < j.S_len; i += (int64_t)gridDim.x * blockDim.x)
+      const_cast<int64_t*>(j.S)[i] = 0;
   const bool vec = (j.crs & 15) == 0 && (reinterpret_cast<uintptr_t>(j.f) & 15) == 0;
   for (int64_t k = (int64_t)blockIdx.x * nw + w; k < j.K; k += (int64_t)gridDim.x * nw) {
     long long dot = 0;
@@ -903,8 +818,11 @@ __global__ void __launch_bounds__(256) ic_finalize_many_kernel(const __grid_cons
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
     if (lane == 0) {
+      const long long lhs = (long long)j.ksum[k];
+      j.ksum[k] = 0ull;  // consumed: the next run accumulates afresh
       j.scr[4 + k] = (unsigned long long)dot;
-      if ((long long)j.ksum[k] != dot) {
+      j.scr[4 + j.K + k] = (unsigned long long)lhs;
+      if (lhs != dot) {
         atomicAdd(&j.scr[0], 1ull);
         atomicMin(&j.scr[1], (unsigned long long)k);
       }
@@ -923,8 +841,10 @@ __global__ void __launch_bounds__(256) ic_finalize_many_kernel(const __grid_cons
     write_outcome(j.out, 0, 0, 0, 0, 0, 0, 0, 0);
   } else {
     const int64_t k = (int64_t)__ldcg(&j.scr[1]);
-    write_outcome(j.out, 1, 1, k, -1, -1, (long long)j.ksum[k], (long long)__ldcg(&j.scr[4 + k]), (long long)cnt);
+    write_outcome(j.out, 1, 1, k, -1, -1, (long long)__ldcg(&j.scr[4 + j.K + k]), (long long)__ldcg(&j.scr[4 + k]),
+                  (long long)cnt);
   }
+  *j.last = *j.out;
   j.scr[0] = 0ull;
   j.scr[1] = ~0ull;
   j.scr[2] = 0ull;
