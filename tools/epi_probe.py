@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--checks", type=int, default=0)
     ap.add_argument("--flags", default="0,1,16,8")
     ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--finalize", action="store_true", help="finalize after every run (inside the timed graph)")
     ap.add_argument("--reuse", action="store_true",
                     help="FIC: keep the first run's input checksum (no in-kernel input pass)")
     a = ap.parse_args()
@@ -59,6 +60,8 @@ def main():
         with torch.cuda.graph(g, stream=stream):
             for _ in range(a.reps):
                 plan.run(packed, out, abi.OUT_I8_PACKED, ep=ep)
+                if a.finalize and a.checks:
+                    plan.finalize()
         ts = []
         for i in range(5):
             flush.zero_()
