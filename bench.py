@@ -686,6 +686,53 @@ def measure_abft_gemm(dev, stream, flush):
             "gemms": out}
 
 
+def measure_dropin_calls(dev):
+    """The reference-facing one-shot call a drop-in caller makes per layer
+    (conv_fast_i8 / conv_direct -> abed_conv_i8, convolution.hpp:224,237): device
+    tensors in / out, synchronous like the reference.  First call (plan built and
+    cached), then the mean of 20 cached calls, against the plan API's one kernel
+    launch for the same layer (ResNet-50 layer1.0.conv2, batch 32).  Host wall
+    clock around each synchronous call (the call itself synchronizes)."""
+    import time
+
+    import torch
+
+    from paper_2006_04984_b200 import abi, api
+
+    ls = api.layer_shape(32, 64, 56, 56, 64, 3, 3, 1, 1, 1, 1)
+    x = api.fill_random_i8(ls.n * ls.c * ls.h * ls.w, api.derive_seed(91, 1)).view(ls.input_dims())
+    f = api.fill_random_i8(ls.k * ls.c * ls.r * ls.s, api.derive_seed(91, 2)).view(ls.filter_dims())
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    y = api.conv_direct(x, f, ls)
+    first = (time.perf_counter() - t0) * 1e3
+    ts = []
+    for _ in range(20):
+        t0 = time.perf_counter()
+        api.conv_direct(x, f, ls)
+        ts.append((time.perf_counter() - t0) * 1e3)
+    plan = api.ConvPlan(ls, f, 0)
+    packed = plan.pack(x)
+    out = torch.empty(ls.output_dims(), dtype=torch.int32, device=dev)
+    plan.run(packed, out, abi.OUT_I32_NCHW, ep=None)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(20):
+        plan.run(packed, out, abi.OUT_I32_NCHW, ep=None)
+    e1.record()
+    torch.cuda.synchronize()
+    assert torch.equal(out, y)
+    ops = 2.0 * ls.n * ls.k * ls.p * ls.q * ls.c * 9
+    cached = statistics.mean(ts)
+    return {"call": "abed_conv_i8 (conv_fast_i8 / conv_direct drop-in), layer1.0.conv2 b32, int32 NCHW out",
+            "first_call_ms": round(first, 3), "cached_call_ms": round(cached, 3),
+            "cached_call_tops": round(ops / (cached * 1e-3) / 1e12, 2),
+            "plan_api_kernel_ms": round(e0.elapsed_time(e1) / 20, 4),
+            "note": "one-shot calls pack the filters and the input, run the tensor-core conv and synchronize; "
+                    "the plan and its buffers are cached per (device, shape)"}
+
+
 def measure_campaign_cfg5(args, dev, world, rank, dist):
     """BASELINE configs[4]'s fault-injection campaign: ResNet-50 layer1.0.conv2
     (64 -> 64, 3x3, 56x56) at batch 1024, the batch sharded over the ranks
@@ -1074,6 +1121,7 @@ def run_ours(args, world, rank, local):
                      "coverage": round((c[0] + c[1]) / trials, 4)}
 
     camp5 = None if args.skip_campaign5 else measure_campaign_cfg5(args, dev, world, rank, dist)
+    dropin = measure_dropin_calls(dev) if rank == 0 else None
 
     if rank != 0:
         if dist:
@@ -1130,6 +1178,7 @@ def run_ours(args, world, rank, local):
         "resnet50_network_int8": r50,
         "abft_gemm_int8": abft,
         "cfg5_campaign_b1024": camp5,
+        "dropin_one_shot": dropin,
     }
     print(json.dumps(line), flush=True)
     if dist:

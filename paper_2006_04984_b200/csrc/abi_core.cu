@@ -1,6 +1,9 @@
 // C ABI: library utilities, the protected-conv plan (hot path) and the
 // reference-facing convolution entry points built on it.
 #include <cuda_runtime.h>
+#include <memory>
+#include <list>
+#include <mutex>
 
 #include <algorithm>
 #include <vector>
@@ -329,6 +332,72 @@ void build_fic_classes(abed_conv_plan* pl) {
   cuda_check(cudaMemcpy(pl->d_colcls, pl->h_colcls.data(), pl->h_colcls.size(), cudaMemcpyHostToDevice), "colcls h2d");
   cuda_check(cudaDeviceSynchronize(), "fic classes sync");
   cudaFree(d_rep);
+}
+
+// ---------------------------------------------------------------- one-shot plan cache
+// abed_conv_i8 (the reference's conv_fast_i8 / conv_direct, called once per
+// layer by reference code) keeps an unchecked plan + packed-input buffer per
+// (device, shape); at most kOneShotCap entries per device (oldest evicted).
+struct OneShot {
+  abed_layer_shape shape{};
+  int device = -1;
+  abed_conv_plan* plan = nullptr;
+  int8_t* packed = nullptr;
+  std::mutex mu;
+};
+constexpr size_t kOneShotCap = 8;
+static std::mutex g_one_shot_mu;
+static std::list<std::unique_ptr<OneShot>> g_one_shot;
+
+static bool same_shape(const abed_layer_shape& a, const abed_layer_shape& b) {
+  return a.n == b.n && a.c == b.c && a.h == b.h && a.w == b.w && a.k == b.k && a.r == b.r && a.s == b.s &&
+         a.stride_h == b.stride_h && a.stride_w == b.stride_w && a.pad_h == b.pad_h && a.pad_w == b.pad_w;
+}
+
+// returns the entry with its mutex held by `hold` (taken under the cache mutex, so
+// an entry in use is never evicted)
+OneShot& one_shot_acquire(const abed_layer_shape& shape, std::unique_lock<std::mutex>& hold) {
+  int dev = 0;
+  cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+  std::lock_guard<std::mutex> lock(g_one_shot_mu);
+  for (auto it = g_one_shot.begin(); it != g_one_shot.end(); ++it)
+    if ((*it)->device == dev && same_shape((*it)->shape, shape)) {
+      g_one_shot.splice(g_one_shot.begin(), g_one_shot, it);  // most recent first
+      hold = std::unique_lock<std::mutex>(g_one_shot.front()->mu);
+      return *g_one_shot.front();
+    }
+  auto e = std::make_unique<OneShot>();
+  e->shape = shape;
+  e->device = dev;
+  int8_t* zeros = nullptr;
+  const int64_t fbytes = shape.k * shape.c * shape.r * shape.s;
+  cuda_check(cudaMalloc(&zeros, (size_t)fbytes), "cudaMalloc(filters)");
+  cuda_check(cudaMemset(zeros, 0, (size_t)fbytes), "memset filters");
+  try {
+    e->plan = plan_create(shape, zeros, 0, 0);
+    cuda_check(cudaMalloc(&e->packed, geom_packed_bytes(e->plan->g)), "cudaMalloc(packed)");
+  } catch (...) {
+    cudaFree(zeros);
+    if (e->plan) abed_conv_plan_destroy(e->plan);
+    throw;
+  }
+  cudaFree(zeros);
+  if (g_one_shot.size() >= kOneShotCap) {
+    // evict the oldest entry of this device that no call is using
+    for (auto it = std::prev(g_one_shot.end());; --it) {
+      if ((*it)->device == dev && (*it)->mu.try_lock()) {
+        (*it)->mu.unlock();
+        abed_conv_plan_destroy((*it)->plan);
+        cudaFree((*it)->packed);
+        g_one_shot.erase(it);
+        break;
+      }
+      if (it == g_one_shot.begin()) break;
+    }
+  }
+  g_one_shot.push_front(std::move(e));
+  hold = std::unique_lock<std::mutex>(g_one_shot.front()->mu);
+  return *g_one_shot.front();
 }
 
 abed_conv_plan* plan_create(const abed_layer_shape& shape, const int8_t* filters, int checks, int force_bn) {
@@ -728,20 +797,20 @@ int abed_conv_i8(const int8_t* input, const int8_t* filters, const abed_layer_sh
     if (shape->c * shape->r * shape->s > 65536)
       throw_invalid("conv_direct: CRS > 65536 exceeds the int32 accumulator plan");
     cudaStream_t st = (cudaStream_t)stream;
-    abed_conv_plan* pl = plan_create(*shape, filters, 0, 0);
-    int8_t* packed = nullptr;
-    try {
-      cuda_check(cudaMalloc(&packed, geom_packed_bytes(pl->g)), "cudaMalloc(packed)");
-      launch_pack_input(input, pl->g, packed, st);
-      plan_run(pl, packed, nullptr, ABED_OUT_I32_NCHW, convout, nullptr, -1, 0, st);
-      cuda_check(cudaStreamSynchronize(st), "conv_i8 sync");
-    } catch (...) {
-      cudaFree(packed);
-      abed_conv_plan_destroy(pl);
-      throw;
-    }
-    cudaFree(packed);
-    abed_conv_plan_destroy(pl);
+    // one-shot reference call (conv_fast_i8 / conv_direct): the plan and its
+    // packed-input buffer come from a small per-device cache keyed by the layer
+    // shape, so repeated calls pay neither plan construction nor cudaMalloc; only
+    // the filters are re-packed (they may change between calls)
+    std::unique_lock<std::mutex> hold;
+    OneShot& o = one_shot_acquire(*shape, hold);
+    abed_conv_plan* pl = o.plan;
+    const ConvTcParams& p = pl->base;
+    const int64_t rows = (int64_t)p.n_tiles * p.k_stages * p.ntaps * p.gps * p.block_n_tot;
+    pack_filters_kernel<<<grid_for(rows, 256), 256, 0, st>>>(filters, pl->g, p.block_n, p.block_n_tot, p.n_tiles,
+                                                             p.gps, p.k_stages, 0, pl->d_wpk);
+    launch_pack_input(input, pl->g, o.packed, st);
+    plan_run(pl, o.packed, nullptr, ABED_OUT_I32_NCHW, convout, nullptr, -1, 0, st);
+    cuda_check(cudaStreamSynchronize(st), "conv_i8 sync");
   });
 }
 
