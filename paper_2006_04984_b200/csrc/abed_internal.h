@@ -131,6 +131,10 @@ void plan_init_common(abed_conv_plan* pl, const abed_layer_shape& shape, int che
 void plan_run(abed_conv_plan* pl, const int8_t* packed, const abed_epilog_params* ep, int out_mode, void* out,
               const abed_conv_plan* next, int64_t fault_key, int fault_bit, cudaStream_t st);
 void plan_finalize(abed_conv_plan* pl, abed_verify_outcome* out_dev, cudaStream_t st);
+// one reference-style conv call on a plan cached per (device, shape, checks)
+void one_shot_run(const abed_layer_shape& shape, int checks, const int8_t* input, const int8_t* filters,
+                  const abed_epilog_params* ep, int out_mode, void* out, abed_verify_outcome* outcomes_dev,
+                  cudaStream_t st);
 abed_dev::VerdictJob plan_verdict_job(const abed_conv_plan* pl, abed_verify_outcome* out_dev);
 // ref_kernels.cu
 void dev_gen_input_checksum(const int8_t* x, const abed_layer_shape& s, int32_t* sums, cudaStream_t st);

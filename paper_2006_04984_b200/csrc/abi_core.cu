@@ -341,6 +341,7 @@ void build_fic_classes(abed_conv_plan* pl) {
 struct OneShot {
   abed_layer_shape shape{};
   int device = -1;
+  int checks = 0;
   abed_conv_plan* plan = nullptr;
   int8_t* packed = nullptr;
   std::mutex mu;
@@ -356,12 +357,12 @@ static bool same_shape(const abed_layer_shape& a, const abed_layer_shape& b) {
 
 // returns the entry with its mutex held by `hold` (taken under the cache mutex, so
 // an entry in use is never evicted)
-OneShot& one_shot_acquire(const abed_layer_shape& shape, std::unique_lock<std::mutex>& hold) {
+OneShot& one_shot_acquire(const abed_layer_shape& shape, int checks, std::unique_lock<std::mutex>& hold) {
   int dev = 0;
   cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
   std::lock_guard<std::mutex> lock(g_one_shot_mu);
   for (auto it = g_one_shot.begin(); it != g_one_shot.end(); ++it)
-    if ((*it)->device == dev && same_shape((*it)->shape, shape)) {
+    if ((*it)->device == dev && (*it)->checks == checks && same_shape((*it)->shape, shape)) {
       g_one_shot.splice(g_one_shot.begin(), g_one_shot, it);  // most recent first
       hold = std::unique_lock<std::mutex>(g_one_shot.front()->mu);
       return *g_one_shot.front();
@@ -369,12 +370,16 @@ OneShot& one_shot_acquire(const abed_layer_shape& shape, std::unique_lock<std::m
   auto e = std::make_unique<OneShot>();
   e->shape = shape;
   e->device = dev;
+  e->checks = checks;
   int8_t* zeros = nullptr;
   const int64_t fbytes = shape.k * shape.c * shape.r * shape.s;
   cuda_check(cudaMalloc(&zeros, (size_t)fbytes), "cudaMalloc(filters)");
   cuda_check(cudaMemset(zeros, 0, (size_t)fbytes), "memset filters");
   try {
-    e->plan = plan_create(shape, zeros, 0, 0);
+    e->plan = plan_create(shape, zeros, checks, 0);
+    // one-shot FIC plans serve the output-checksum tap only (fused_conv_epilog):
+    // the kernel skips the input pass
+    e->plan->reuse_input_checksum = 1;
     cuda_check(cudaMalloc(&e->packed, geom_packed_bytes(e->plan->g)), "cudaMalloc(packed)");
   } catch (...) {
     cudaFree(zeros);
@@ -398,6 +403,25 @@ OneShot& one_shot_acquire(const abed_layer_shape& shape, std::unique_lock<std::m
   g_one_shot.push_front(std::move(e));
   hold = std::unique_lock<std::mutex>(g_one_shot.front()->mu);
   return *g_one_shot.front();
+}
+
+// One reference-style call on the cached plan: re-pack the filters (they may
+// change between calls), pack the input, run; with outcomes_dev the plan's
+// verdicts (FIC: lhs = the sum of the ConvOut) follow.  Stream-ordered.
+void one_shot_run(const abed_layer_shape& shape, int checks, const int8_t* input, const int8_t* filters,
+                  const abed_epilog_params* ep, int out_mode, void* out, abed_verify_outcome* outcomes_dev,
+                  cudaStream_t st) {
+  std::unique_lock<std::mutex> hold;
+  OneShot& o = one_shot_acquire(shape, checks, hold);
+  abed_conv_plan* pl = o.plan;
+  const ConvTcParams& p = pl->base;
+  const int64_t rows = (int64_t)p.n_tiles * p.k_stages * p.ntaps * p.gps * p.block_n_tot;
+  pack_filters_kernel<<<grid_for(rows, 256), 256, 0, st>>>(filters, pl->g, p.block_n, p.block_n_tot, p.n_tiles, p.gps,
+                                                           p.k_stages, 0, pl->d_wpk);
+  launch_pack_input(input, pl->g, o.packed, st);
+  plan_run(pl, o.packed, ep, out_mode, out, nullptr, -1, 0, st);
+  if (outcomes_dev) plan_finalize(pl, outcomes_dev, st);
+  cuda_check(cudaGetLastError(), "one-shot conv");
 }
 
 abed_conv_plan* plan_create(const abed_layer_shape& shape, const int8_t* filters, int checks, int force_bn) {
@@ -797,19 +821,7 @@ int abed_conv_i8(const int8_t* input, const int8_t* filters, const abed_layer_sh
     if (shape->c * shape->r * shape->s > 65536)
       throw_invalid("conv_direct: CRS > 65536 exceeds the int32 accumulator plan");
     cudaStream_t st = (cudaStream_t)stream;
-    // one-shot reference call (conv_fast_i8 / conv_direct): the plan and its
-    // packed-input buffer come from a small per-device cache keyed by the layer
-    // shape, so repeated calls pay neither plan construction nor cudaMalloc; only
-    // the filters are re-packed (they may change between calls)
-    std::unique_lock<std::mutex> hold;
-    OneShot& o = one_shot_acquire(*shape, hold);
-    abed_conv_plan* pl = o.plan;
-    const ConvTcParams& p = pl->base;
-    const int64_t rows = (int64_t)p.n_tiles * p.k_stages * p.ntaps * p.gps * p.block_n_tot;
-    pack_filters_kernel<<<grid_for(rows, 256), 256, 0, st>>>(filters, pl->g, p.block_n, p.block_n_tot, p.n_tiles,
-                                                             p.gps, p.k_stages, 0, pl->d_wpk);
-    launch_pack_input(input, pl->g, o.packed, st);
-    plan_run(pl, o.packed, nullptr, ABED_OUT_I32_NCHW, convout, nullptr, -1, 0, st);
+    one_shot_run(*shape, 0, input, filters, nullptr, ABED_OUT_I32_NCHW, convout, nullptr, st);
     cuda_check(cudaStreamSynchronize(st), "conv_i8 sync");
   });
 }

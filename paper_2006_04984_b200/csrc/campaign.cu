@@ -90,10 +90,7 @@ struct PlanGuard {
 
 // run the tcgen05 conv over NCHW device tensors, int32 NCHW out
 void tc_conv_nchw(const abed_layer_shape& s, const int8_t* x, const int8_t* f, int32_t* out, cudaStream_t st) {
-  PlanGuard pl{plan_create(s, f, 0, 0)};
-  Dev<int8_t> packed((size_t)geom_packed_bytes(pl.p->g));
-  abed_pack_input(pl.p, x, packed.p, st);
-  plan_run(pl.p, packed.p, nullptr, ABED_OUT_I32_NCHW, out, nullptr, -1, 0, st);
+  one_shot_run(s, 0, x, f, nullptr, ABED_OUT_I32_NCHW, out, nullptr, st);
   cuda_check(cudaStreamSynchronize(st), "tc_conv sync");
 }
 
@@ -591,15 +588,13 @@ int abed_fused_conv_epilog(const int8_t* x, const int8_t* f, const abed_layer_sh
         for (float v : hb) if (!std::isfinite(v)) throw_invalid("epilog: non-finite bias");
       }
       if (ep->output_kind != ABED_I8 && ep->output_kind != ABED_F32) throw_invalid("epilog: output kind must be i8 or f32");
-      PlanGuard pl{plan_create(*s, f, out_checksum ? ABED_CHECK_FIC : 0, 0)};
-      pl.p->reuse_input_checksum = 1;  // only the output reduction is needed for the tap
-      Dev<int8_t> packed((size_t)geom_packed_bytes(pl.p->g));
-      abed_pack_input(pl.p, x, packed.p, st);
-      plan_run(pl.p, packed.p, ep, ep->output_kind == ABED_F32 ? ABED_OUT_F32_NCHW : ABED_OUT_I8_NCHW, out, nullptr, -1, 0, st);
+      // cached plan (FIC on only for the output-checksum tap: the FIC lhs is the
+      // sum of the ConvOut before the epilog)
+      Dev<abed_verify_outcome> oc(out_checksum ? 3 : 1);
+      one_shot_run(*s, out_checksum ? ABED_CHECK_FIC : 0, x, f, ep,
+                   ep->output_kind == ABED_F32 ? ABED_OUT_F32_NCHW : ABED_OUT_I8_NCHW, out,
+                   out_checksum ? oc.p : nullptr, st);
       if (out_checksum) {
-        Dev<abed_verify_outcome> oc(3);
-        cuda_check(cudaMemsetAsync(pl.p->d_acc, 0, 8, st), "memset");
-        plan_finalize(pl.p, oc.p, st);
         abed_verify_outcome h;
         cuda_check(cudaMemcpyAsync(&h, oc.p + 1, sizeof(h), cudaMemcpyDeviceToHost, st), "d2h");
         cuda_check(cudaStreamSynchronize(st), "sync");
