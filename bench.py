@@ -316,6 +316,7 @@ def measure_vgg16_fp16(args, dev, stream, flush, world, dist):
         res[v] = {"tflops": round(flops * world / (ms * 1e-3) / 1e12, 2), "ms_per_step": round(ms, 4)}
     fails = sum(o.status for v in ("fc", "fic") for oc in sets[v].outcomes() for o in oc[:2])
     u = res["unprotected"]["ms_per_step"]
+    vgg_peak = measured_peaks().get("bf16_tflops") or 1590.0
     return {"workload": "vgg16-3x3-convs-fp16-b64 (12 layers, C>=64; f32 accumulate, ReLU, fp16 packed out)",
             "dtype": "fp16 operands, f32 accumulation (tcgen05 kind::f16)", "global_batch": VGG_BATCH * world,
             "gflop_per_step": round(flops * world / 1e9, 1), "variants": res,
@@ -324,6 +325,13 @@ def measure_vgg16_fp16(args, dev, stream, flush, world, dist):
                              "duplication_vs_unprotected": round(100 * (res["dup"]["ms_per_step"] / u - 1), 2)},
             "tau": "absolute, (CRS+32)*2^-22*max|x|*sum|f| (FC per pixel; FIC x N*P*Q)",
             "fault_free_verdicts_failed": fails,
+            "roofline": {"bound": "tensor", "peak_tflops": vgg_peak,
+                         "peak_source": "MEASURED_PEAKS.json bf16_tflops" if measured_peaks().get("bf16_tflops")
+                         else "fallback 1590 (B200_PROFILING.md)",
+                         "frac_unprotected": round(res["unprotected"]["tflops"] / vgg_peak, 3),
+                         "frac_fic": round(res["fic"]["tflops"] / vgg_peak, 3),
+                         "frac_fic_of_sustained": (round(res["fic"]["tflops"] / measured_peaks()["bf16_tflops_sustained"], 3)
+                                                   if measured_peaks().get("bf16_tflops_sustained") else None)},
             "peak_note": "fp16 dense peak = MEASURED_PEAKS bf16_tflops (or the 1590 fallback)"}
 
 
@@ -336,6 +344,7 @@ def measure_mobilenetv2_int8(args, dev, stream, flush, world, dist):
 
     from paper_2006_04984_b200 import abi, api
     layers, ops, seed = [], 0, 900
+    hbm_bytes = 0  # algorithmic: every layer reads its input + filters once and writes its output once
     for ci, hw, t, co, st in MBV2_BLOCKS:
         e = ci * t
         ho = (hw + 2 - 3) // st + 1
@@ -345,14 +354,17 @@ def measure_mobilenetv2_int8(args, dev, stream, flush, world, dist):
         block = []
         for kind, ls in shapes:
             seed += 1
+            hbm_bytes += ls.n * ls.c * ls.h * ls.w + ls.n * ls.k * ls.p * ls.q
             if kind == "pw":
                 f = api.fill_random_i8(ls.k * ls.c, api.derive_seed(seed, 2)).view(ls.filter_dims())
                 mk = lambda ch, ls=ls, f=f: api.ConvPlan(ls, f, ch)  # noqa: E731
                 ops += 2 * ls.n * ls.k * ls.p * ls.q * ls.c
+                hbm_bytes += ls.k * ls.c
             else:
                 f = api.fill_random_i8(ls.c * 9, api.derive_seed(seed, 2)).view(ls.c, 1, 3, 3)
                 mk = lambda ch, ls=ls, f=f: api.ConvPlanDW(ls, f, ch)  # noqa: E731
                 ops += 2 * ls.n * ls.k * ls.p * ls.q * 9
+                hbm_bytes += ls.c * 9
             L = {"kind": kind, "ls": ls, "plans": {"unprotected": mk(0), "fic": mk(abi.CHECK_FIC),
                                                     "fic_af": mk(abi.CHECK_FIC)}}
             if block:  # FIC-AF: rhs accumulated by the producing layer's epilogue
@@ -427,6 +439,16 @@ def measure_mobilenetv2_int8(args, dev, stream, flush, world, dist):
             "fic_af": "FIC with each in-block layer's input checksum accumulated by the producing epilogue",
             "blocks": [list(b) for b in MBV2_BLOCKS], "global_batch": BATCH * world,
             "gop_per_step": round(ops * world / 1e9, 2), "variants": res,
+            # HBM-bound stress config: algorithmic bytes (each layer's int8 input, output and
+            # filters once) per step over the step time, against the measured copy bandwidth
+            "roofline": {"bound": "hbm", "algorithmic_bytes_per_step": int(hbm_bytes * world),
+                         "achieved_gbs_fic": round(hbm_bytes * world / (res["fic"]["ms_per_step"] * 1e-3) / 1e9, 1),
+                         "achieved_gbs_unprotected": round(hbm_bytes * world / (u * 1e-3) / 1e9, 1),
+                         "peak_gbs": measured_peaks().get("hbm_gbs") or 7700.0,
+                         "frac_fic": round(hbm_bytes * world / (res["fic"]["ms_per_step"] * 1e-3) / 1e9 /
+                                           (measured_peaks().get("hbm_gbs") or 7700.0), 3),
+                         "note": "15 chained launches of small layers: per-launch latency, not bandwidth, sets "
+                                 "the step time"},
             "overhead_pct": {"fic_vs_unprotected": round(100 * (res["fic"]["ms_per_step"] / u - 1), 2),
                              "fic_af_vs_unprotected": round(100 * (res["fic_af"]["ms_per_step"] / u - 1), 2),
                              "duplication_vs_unprotected": round(100 * (res["dup"]["ms_per_step"] / u - 1), 2)},
