@@ -864,6 +864,8 @@ def run_ours(args, world, rank, local):
         # FIC with the input checksum dotted from the staged shared-memory tiles
         # instead of the default second read of the stored input (FR)
         L["plans"]["fic_sm"].set_input_checksum_source(abi.RHS_STAGED)
+        # the captured pass finalizes every IC run it contains
+        L["plans"]["ic"].set_paired_finalize(True)
         L["packed"] = L["plans"]["unprotected"].pack(x)
         # ICBatch: the packed input also holds the batch-sum digit images (written in-kernel)
         L["packed_icb"] = L["plans"]["icbatch"].pack(x)

@@ -327,6 +327,12 @@ int abed_conv_plan_finalize_many(abed_conv_plan* const* plans, int32_t n, abed_v
  * an earlier run instead of recomputing it from the (possibly corrupted) input;
  * the run is then exactly one kernel launch (fault campaigns, kernel timing). */
 int abed_conv_plan_set_reuse_input_checksum(abed_conv_plan* plan, int32_t reuse);
+/* IC plans: a run's in-kernel sums are consumed (and cleared) by the finalize of
+ * that run, so eager run/finalize pairs need no per-run memsets.  A run captured
+ * into a CUDA graph clears them itself (the host cannot see how replays and
+ * finalizes interleave) unless paired = 1 declares that every captured run is
+ * followed by its finalize in the same graph (the PlanSet pass pattern). */
+int abed_conv_plan_set_paired_finalize(abed_conv_plan* plan, int32_t paired);
 /* Where an int8 FIC plan's in-kernel input checksum (the FIC right-hand side,
  * gen_input_checksum + fic_dot, checksum.hpp:248-285) reads the input from:
  * ABED_RHS_REREAD (default) reads the stored input a second time (the cost

@@ -194,6 +194,7 @@ SIGNATURES = {
     "abed_conv_plan_create_dw": (C.c_int, [SHP, P, i32, C.POINTER(P)]),
     "abed_conv_plan_set_af_input": (C.c_int, [P, i32]),
     "abed_conv_plan_set_reuse_input_checksum": (C.c_int, [P, i32]),
+    "abed_conv_plan_set_paired_finalize": (C.c_int, [P, i32]),
     "abed_conv_plan_set_input_checksum_source": (C.c_int, [P, i32]),
     "abed_probe_mma_i8_peak": (C.c_int, [i32, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "abed_verdict_records": (C.c_int, [P, i32, P, i64, P, P]),

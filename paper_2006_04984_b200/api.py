@@ -475,6 +475,10 @@ class ConvPlan:
         """FIC rhs from the staged activation tiles (default) or a re-read of the input (FR)."""
         call("abed_conv_plan_set_input_checksum_source", self.handle, source)
 
+    def set_paired_finalize(self, on: bool = True):
+        """IC plans: captured graphs finalize every run they contain (no clearing memsets)."""
+        call("abed_conv_plan_set_paired_finalize", self.handle, 1 if on else 0)
+
     def set_af_input(self, on: bool = True):
         """FIC-AF: this layer's FIC rhs comes from the previous layer's epilogue."""
         call("abed_conv_plan_set_af_input", self.handle, 1 if on else 0)

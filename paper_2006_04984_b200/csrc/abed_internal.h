@@ -191,6 +191,7 @@ struct abed_conv_plan {
   int reuse_input_checksum = 0;
   int last_rhs_mode = 0;
   int ic_pending = 0;                      // IC: a run's in-kernel sums await their verdict
+  int paired_finalize = 0;                 // IC: captured graphs finalize every run they contain
   abed_verify_outcome* d_ic_last = nullptr;  // IC: last verdict (repeated by a second finalize)
   unsigned long long cmp_seen = 0;         // compare runs: mismatches already reported
   int last_grid = 0;            // CTAs of the last conv launch (records the verdict reduces)        // rhs_mode of the last run (its verdict reduction needs it)

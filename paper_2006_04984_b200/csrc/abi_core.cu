@@ -545,8 +545,14 @@ void plan_run(abed_conv_plan* pl, const int8_t* packed, const abed_epilog_params
   p.fault_key = fault_key;
   p.fault_bit = fault_bit;
   // IC: the per-channel sums (and class sums) of a run are zeroed by its verdict;
-  // only a run whose predecessor was never finalized needs them cleared here
-  const bool ic_dirty = (pl->checks & ABED_CHECK_IC) && pl->ic_pending;
+  // a run whose predecessor was never finalized clears them here.  Under stream
+  // capture the host cannot see how replays interleave with finalizes, so captured
+  // runs clear them too -- unless the caller declared that its graphs pair every
+  // run with a finalize (abed_conv_plan_set_paired_finalize)
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cuda_check(cudaStreamIsCapturing(st, &cap), "capture status");
+  const bool ic_dirty = (pl->checks & ABED_CHECK_IC) &&
+                        (pl->ic_pending || (cap != cudaStreamCaptureStatusNone && !pl->paired_finalize));
   if (ic_dirty) cuda_check(cudaMemsetAsync(pl->d_acc + 4, 0, pl->shape.k * 8, st), "memset ic");
   if (pl->checks & ABED_CHECK_IC) pl->ic_pending = 1;
   // compare runs accumulate mismatches; compare_count reports the increase
@@ -799,6 +805,12 @@ int abed_conv_plan_set_input_checksum_source(abed_conv_plan* pl, int32_t source)
     if (!pl) throw_invalid("plan is null");
     if (source != ABED_RHS_STAGED && source != ABED_RHS_REREAD) throw_invalid("input checksum source must be 0 or 1");
     pl->rhs_src = source;
+  });
+}
+int abed_conv_plan_set_paired_finalize(abed_conv_plan* pl, int32_t paired) {
+  return guarded([&] {
+    if (!pl) throw_invalid("plan is null");
+    pl->paired_finalize = paired ? 1 : 0;
   });
 }
 int abed_conv_plan_set_reuse_input_checksum(abed_conv_plan* pl, int32_t reuse) {

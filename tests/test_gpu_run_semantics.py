@@ -96,6 +96,30 @@ def test_ic_graph_replays_of_run_and_finalize(ora):
         assert _same(plan.outcomes()[2], good)
 
 
+def test_ic_captured_runs_without_finalize_clear_their_sums(ora):
+    """A graph that contains only the run, replayed several times, then one eager
+    finalize: the verdict is the last run's (captured runs clear the sums unless the
+    plan declared paired finalizes)."""
+    ls = api.layer_shape(2, 16, 12, 12, 32, 3, 3, 1, 1, 1, 1)
+    x, f = _data(ls, 14)
+    plan = api.ConvPlan(ls, f.cuda(), abi.CHECK_IC)
+    packed = plan.pack(x.cuda())
+    out = torch.empty(ls.output_dims(), dtype=torch.int32, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        plan.run(packed, out, abi.OUT_I32_NCHW, ep=None)
+        plan.finalize()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        plan.run(packed, out, abi.OUT_I32_NCHW, ep=None)
+    for _ in range(3):
+        g.replay()
+    plan.finalize()
+    torch.cuda.synchronize()
+    assert _same(plan.outcomes()[2], _ic_ref(ora, x, f, ls))
+
+
 def test_compare_count_reports_the_increase():
     ls = api.layer_shape(2, 16, 10, 10, 16, 3, 3, 1, 1, 1, 1)
     x, f = _data(ls, 13)
