@@ -19,7 +19,10 @@ reference headers, detail::conv_fast_i8 + epilog, convolution.hpp:224,353):
   accumulation bound);
 * BASELINE configs[3]: the five MobileNetV2 blocks at batch 32 chained through
   the packed layout, FIC on every layer; the block output equals the reference
-  pointwise convs + epilogs around the depthwise restatement.
+  pointwise convs + epilogs around the depthwise restatement;
+* the whole-network block: one ResNet-50 bottleneck chain per stage (1x1 -> 3x3
+  -> 1x1 through the packed layout) with FIC and with FIC-AF, chain output and
+  every layer's FIC lhs / rhs against the reference.
 
 Integer outputs are bit-exact.  The packed output is unpacked from the identity
 consumer's strip planes (conv_tc.cuh layout, Hl = P, Wl = Q, one phase).
@@ -264,5 +267,52 @@ def test_mobilenetv2_block_b32(ref, ora, bi):
     for (kind, ls), fh in zip(shapes, filt):
         conv = ref_conv(ref, h, fh, ls) if kind == "pw" else ora.dwconv_i8(h, fh, ls)
         h = ref_epilog(ref, conv, 0.02, zero(ls))
+    got = unpack_identity(out, last).squeeze(-1).cpu().numpy()
+    assert np.array_equal(got, h)
+
+
+# whole-network block (bench.py resnet50_network_int8): one bottleneck chain per
+# stage -- conv1 1x1 -> conv2 3x3 (stride 2 at a stage's first block) -> conv3 1x1
+# through the packed layout, FIC on every layer and FIC-AF (each in-chain layer's
+# rhs accumulated by the producing epilogue); batch 4 keeps the CPU reference fast
+CHAIN_PICK = [0, 4, 9, 16]  # layer1.0, layer2.0, layer3.0, layer4.0 bottlenecks
+
+
+@pytest.mark.parametrize("variant", ["fic", "fic_af"])
+@pytest.mark.parametrize("ci", CHAIN_PICK, ids=lambda i: f"chain{i}")
+def test_resnet50_bottleneck_chain(ref, ci, variant):
+    from bench import resnet50_chains
+    chain = resnet50_chains(4)[ci]
+    assert len(chain) == 3
+    plans, filt = [], []
+    bias = []
+    for li, ls in enumerate(chain):
+        f = api.fill_random_i8(ls.k * ls.c * ls.r * ls.s, api.derive_seed(700 + 7 * ci + li, 2)).view(ls.filter_dims())
+        pl = api.ConvPlan(ls, f, abi.CHECK_FIC)
+        if variant == "fic_af" and li > 0:
+            pl.set_af_input(True)
+        plans.append(pl)
+        filt.append(f.cpu().numpy())
+        bias.append(np.linspace(-1.0, 1.0, ls.k).astype(np.float32))
+    ls0 = chain[0]
+    x = api.fill_random_i8(ls0.n * ls0.c * ls0.h * ls0.w, api.derive_seed(700 + 7 * ci, 1)).view(ls0.input_dims())
+    bufs = [plans[0].pack(x), plans[1].packed_buffer(), plans[2].packed_buffer()]
+    last = chain[2]
+    out = torch.zeros(identity_out_bytes(last), dtype=torch.int8, device="cuda")
+    for i, pl in enumerate(plans):
+        pl.run(bufs[i], bufs[i + 1] if i < 2 else out, abi.OUT_I8_PACKED,
+               ep=pl.epilog_params(0.02, bias[i].tolist(), True), next_plan=plans[i + 1] if i < 2 else None)
+    ps = api.PlanSet(plans)
+    ps.finalize()
+    torch.cuda.synchronize()
+    h = x.cpu().numpy()
+    sums = []
+    for ls, fh, b in zip(chain, filt, bias):
+        conv = ref_conv(ref, h, fh, ls)
+        sums.append(int(conv.astype(np.int64).sum()))
+        h = ref_epilog(ref, conv, 0.02, b)
+    oc = ps.outcomes()
+    for i in range(3):  # FIC of every layer: pass, lhs = rhs = the reference's ConvOut sum
+        assert oc[i][1].status == 0 and oc[i][1].lhs == oc[i][1].rhs == sums[i], (i, oc[i][1].lhs, sums[i])
     got = unpack_identity(out, last).squeeze(-1).cpu().numpy()
     assert np.array_equal(got, h)
