@@ -834,6 +834,12 @@ def run_ours(args, world, rank, local):
 
     from paper_2006_04984_b200 import abi, api
 
+    # ABED_BENCH_SHARED_GPU=1: code-path check of the multi-rank bench on a box with
+    # fewer GPUs than ranks (ranks share devices, gloo instead of NCCL); its
+    # timings are not measurements
+    shared = os.environ.get("ABED_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     # per-GPU batch: BASELINE configs[1] (32 per GPU, weak scaling) by default;
     # --global-batch B shards a fixed batch over the ranks (configs[4]: 1024, strong)
@@ -844,7 +850,10 @@ def run_ours(args, world, rank, local):
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     stream = torch.cuda.Stream()
     peaks = measured_peaks()
