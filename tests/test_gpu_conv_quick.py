@@ -65,3 +65,43 @@ def test_pack_input_vector_path_equals_byte_path(dims):
     plan.run(a, out, abi.OUT_I32_NCHW)
     torch.cuda.synchronize()
     assert torch.equal(out.cpu().to(torch.int64), ref_conv(x.cpu(), f.cpu(), ls))
+
+
+def _random_shapes(count, seed):
+    g = torch.Generator().manual_seed(seed)
+    out = []
+    while len(out) < count:
+        r = [1, 3, 5][int(torch.randint(0, 3, (1,), generator=g))]
+        st = int(torch.randint(1, 3, (1,), generator=g))
+        pad = int(torch.randint(0, r // 2 + 1, (1,), generator=g))
+        h = int(torch.randint(max(r - 2 * pad, 1), 21, (1,), generator=g))
+        w = int(torch.randint(max(r - 2 * pad, 1), 23, (1,), generator=g))
+        c = int(torch.randint(1, 41, (1,), generator=g))
+        k = int(torch.randint(1, 40, (1,), generator=g))
+        n = int(torch.randint(1, 4, (1,), generator=g))
+        out.append((n, c, h, w, k, r, r, st, st, pad, pad))
+    return out
+
+
+@pytest.mark.parametrize("dims", _random_shapes(24, 2026), ids=lambda d: "x".join(map(str, d)))
+def test_pack_input_random_geometries(dims):
+    """pack_input's staged transpose on random geometries (odd widths -> byte
+    loads, widths % 4 == 0 -> word loads, stride 2 phases, 1x1 / 3x3 / 5x5, filler
+    channels): both source paths give the same planes and the conv on them is exact."""
+    from paper_2006_04984_b200 import api
+    ls = abi.layer_shape(*dims)
+    g = torch.Generator().manual_seed(sum(dims))
+    x = torch.randint(-128, 128, ls.input_dims(), dtype=torch.int8, generator=g)
+    f = torch.randint(-128, 128, ls.filter_dims(), dtype=torch.int8, generator=g)
+    plan = api.ConvPlan(ls, f.cuda(), 0)
+    a = plan.pack(x.cuda(), plan.packed_buffer())
+    raw = torch.empty(x.numel() + 1, dtype=torch.int8, device="cuda")
+    raw[1:].copy_(x.flatten().cuda())
+    b = plan.packed_buffer()
+    abi.call("abed_pack_input", plan.handle, raw.data_ptr() + 1, b.data_ptr(), None)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    out = torch.empty(ls.output_dims(), dtype=torch.int32, device="cuda")
+    plan.run(a, out, abi.OUT_I32_NCHW)
+    torch.cuda.synchronize()
+    assert torch.equal(out.cpu().to(torch.int64), ref_conv(x, f, ls))
