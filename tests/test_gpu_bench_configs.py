@@ -276,14 +276,16 @@ def test_mobilenetv2_block_b32(ref, ora, bi):
 # through the packed layout, FIC on every layer and FIC-AF (each in-chain layer's
 # rhs accumulated by the producing epilogue); batch 4 keeps the CPU reference fast
 CHAIN_PICK = [0, 4, 9, 16]  # layer1.0, layer2.0, layer3.0, layer4.0 bottlenecks
+PROJ_PICK = [1, 5, 10, 17]   # the 1x1 projections (stride 2 from layer2 on, up to 2048 channels)
 
 
 @pytest.mark.parametrize("variant", ["fic", "fic_af"])
-@pytest.mark.parametrize("ci", CHAIN_PICK, ids=lambda i: f"chain{i}")
+@pytest.mark.parametrize("ci", CHAIN_PICK + PROJ_PICK, ids=lambda i: f"chain{i}")
 def test_resnet50_bottleneck_chain(ref, ci, variant):
     from bench import resnet50_chains
     chain = resnet50_chains(4)[ci]
-    assert len(chain) == 3
+    if len(chain) == 1 and variant == "fic_af":
+        pytest.skip("a single-layer chain has no producer epilogue to tap")
     plans, filt = [], []
     bias = []
     for li, ls in enumerate(chain):
@@ -296,12 +298,13 @@ def test_resnet50_bottleneck_chain(ref, ci, variant):
         bias.append(np.linspace(-1.0, 1.0, ls.k).astype(np.float32))
     ls0 = chain[0]
     x = api.fill_random_i8(ls0.n * ls0.c * ls0.h * ls0.w, api.derive_seed(700 + 7 * ci, 1)).view(ls0.input_dims())
-    bufs = [plans[0].pack(x), plans[1].packed_buffer(), plans[2].packed_buffer()]
-    last = chain[2]
+    nl = len(chain)
+    bufs = [plans[0].pack(x)] + [plans[i].packed_buffer() for i in range(1, nl)]
+    last = chain[-1]
     out = torch.zeros(identity_out_bytes(last), dtype=torch.int8, device="cuda")
     for i, pl in enumerate(plans):
-        pl.run(bufs[i], bufs[i + 1] if i < 2 else out, abi.OUT_I8_PACKED,
-               ep=pl.epilog_params(0.02, bias[i].tolist(), True), next_plan=plans[i + 1] if i < 2 else None)
+        pl.run(bufs[i], bufs[i + 1] if i < nl - 1 else out, abi.OUT_I8_PACKED,
+               ep=pl.epilog_params(0.02, bias[i].tolist(), True), next_plan=plans[i + 1] if i < nl - 1 else None)
     ps = api.PlanSet(plans)
     ps.finalize()
     torch.cuda.synchronize()
@@ -312,7 +315,7 @@ def test_resnet50_bottleneck_chain(ref, ci, variant):
         sums.append(int(conv.astype(np.int64).sum()))
         h = ref_epilog(ref, conv, 0.02, b)
     oc = ps.outcomes()
-    for i in range(3):  # FIC of every layer: pass, lhs = rhs = the reference's ConvOut sum
+    for i in range(nl):  # FIC of every layer: pass, lhs = rhs = the reference's ConvOut sum
         assert oc[i][1].status == 0 and oc[i][1].lhs == oc[i][1].rhs == sums[i], (i, oc[i][1].lhs, sums[i])
     got = unpack_identity(out, last).squeeze(-1).cpu().numpy()
     assert np.array_equal(got, h)
