@@ -212,147 +212,282 @@ __global__ void __launch_bounds__(256) pack_input_v4_kernel(const int8_t* __rest
   }
 }
 
-// Shared-memory staged transpose (NCHW -> strip planes): block = (plane, image,
-// band of rb M-space rows); smem holds the band in the OUTPUT layout
-// [rb][Wl][16 channels].  Phase 0 zeroes it (halo, filler channels); phase 1:
-// work item = (channel quad, band row, input word of 4 columns), 4 coalesced
-// 32-bit loads (the quad's channels), a 4 x 4 byte transpose (__byte_perm) and
-// one 32-bit smem store per pixel of this stride phase; phase 2 copies the band
-// out with 16-byte loads / stores.  Every input byte read once per stride phase,
-// every output byte written once; ~20 instructions per 16-byte pixel (the
-// byte-gather version was issue-bound at 0.25 of HBM).  Rows that are not a
-// multiple of 4 bytes (or an unaligned base) use byte loads in phase 1.  The zero
-// tail of each plane (after the last image) is written by one extra block per plane.
-template <int SW>  // horizontal stride 1 or 2 (0: any, with divisions)
-__global__ void __launch_bounds__(256) pack_input_smem_kernel(const int8_t* __restrict__ x, ActGeom g, int lrb,
-                                                              int nbands, int words_ok, int8_t* __restrict__ out) {
-  extern __shared__ __align__(16) uint8_t tile[];  // [rb][Wl][16]
+// Shared-memory staged transpose (NCHW -> strip planes): block = (plane, band of
+// rb M-space rows, group of ipb images); smem holds one image's band in the
+// OUTPUT layout (two buffers, alternating over the images): rows of wp 16-byte
+// pixel slots, output pixel j of band row ii at slot ii * wp + pad0 + j, slot s
+// stored at s ^ ((s >> 3) & 7) (an XOR swizzle inside each 8-slot group).
+// Phase 1: work item = (band row, channel quad, input word of WB bytes = WB
+// columns): 4 coalesced WB-byte loads (the quad's channels), WB/4 4 x 4 byte
+// transposes (__byte_perm) and one 32-bit smem store per column.  Lanes of a warp
+// cover (channel quad, word) pairs of one row; the swizzle spreads a store
+// instruction over distinct banks.  With stride 1, pad0 aligns every input word
+// to a slot group, so the stores need no bounds checks (slots outside the output
+// row are never read) and their addresses are one XOR apart.  Phase 2 writes the
+// band out with 16-byte stores; halo pixels (rows / columns outside the input)
+// and filler channel quads are written as zeros there, so there is no zeroing
+// pass.  Every input byte read once per stride phase, every output byte written
+// once.  WB = 0: rows that are not a multiple of 4 bytes (or an unaligned base)
+// use byte loads.  The zero tail of each plane (after the last image) is written
+// by one extra block per plane.
+#ifndef ABED_PACK_MINB
+#define ABED_PACK_MINB 5  // resident 256-thread blocks per SM the register budget allows
+#endif
+__device__ __forceinline__ int pack_slot(int s) { return s ^ ((s >> 3) & 7); }
+
+// n / d for 0 <= n < 2^31 with a multiply-high (the divisor fixed per launch)
+struct PackDiv {
+  uint32_t m, l, d;
+  __device__ __forceinline__ int div(int n) const { return (int)((__umulhi((uint32_t)n, m) + (uint32_t)n) >> l); }
+};
+static PackDiv pack_div(uint32_t d) {
+  uint32_t l = 0;
+  while ((1ull << l) < d) ++l;
+  return PackDiv{(uint32_t)(((1ull << 32) * ((1ull << l) - d)) / d + 1), l, d};
+}
+
+// one (band row, channel quad, input word) item of phase 1: load, transpose, store
+template <int SW, int WB>
+__device__ __forceinline__ void pack_item(const int8_t* src, int HW, uint32_t lm, int cq, uint8_t* buf, int q, int ii,
+                                          int wp, int pad0, int off, int sw, int Wl, int fixed_base) {
+  constexpr int NW = WB >= 4 ? WB / 4 : 1;  // 32-bit words per load
+  constexpr int NP = 4 * NW;                // columns per word
+  uint32_t v[4][NW];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    if ((lm >> e) & 1u) {  // channel 4cq + e exists
+      if (NW == 2) {
+        const uint2 t = __ldg(reinterpret_cast<const uint2*>(src + e * HW));
+        v[e][0] = t.x;
+        v[e][NW - 1] = t.y;
+      } else {
+        v[e][0] = __ldg(reinterpret_cast<const uint32_t*>(src + e * HW));
+      }
+    } else {
+#pragma unroll
+      for (int h = 0; h < NW; ++h) v[e][h] = 0u;
+    }
+  }
+  // 4 x 4 byte transposes: pw[4h + t] = channels 4cq..4cq+3 of column WB*q + 4h + t
+  uint32_t pw[NP];
+#pragma unroll
+  for (int h = 0; h < NW; ++h) {
+    const uint32_t t01lo = __byte_perm(v[0][h], v[1][h], 0x5140), t01hi = __byte_perm(v[0][h], v[1][h], 0x7362);
+    const uint32_t t23lo = __byte_perm(v[2][h], v[3][h], 0x5140), t23hi = __byte_perm(v[2][h], v[3][h], 0x7362);
+    pw[4 * h + 0] = __byte_perm(t01lo, t23lo, 0x5410);
+    pw[4 * h + 1] = __byte_perm(t01lo, t23lo, 0x7632);
+    pw[4 * h + 2] = __byte_perm(t01hi, t23hi, 0x5410);
+    pw[4 * h + 3] = __byte_perm(t01hi, t23hi, 0x7632);
+  }
+  if (SW == 1) {
+    // slots s0 .. s0 + NP - 1 (s0 a multiple of NP): the swizzled byte address of
+    // column t is base ^ (t << 4)
+    const uint32_t base = fixed_base >= 0 ? (uint32_t)fixed_base
+                                          : (uint32_t)pack_slot(ii * wp + pad0 + off + q * NP) * 16u + cq * 4u;
+#pragma unroll
+    for (int t = 0; t < NP; ++t) *reinterpret_cast<uint32_t*>(buf + (base ^ (t << 4))) = pw[t];
+  } else {
+#pragma unroll
+    for (int t = 0; t < NP; ++t) {
+      const int jj = q * NP + t + off;  // = j * sw
+      int j;
+      if (SW == 2) {
+        if (jj & 1) continue;
+        j = jj >> 1;
+      } else {
+        if (jj % sw) continue;
+        j = jj / sw;
+      }
+      if (jj < 0 || j >= Wl) continue;
+      *reinterpret_cast<uint32_t*>(buf + pack_slot(ii * wp + pad0 + j) * 16 + cq * 4) = pw[t];
+    }
+  }
+}
+
+template <int SW, int WB>  // SW: horizontal stride 1 or 2 (0: any); WB: 8, 4 or 0 (bytes)
+__global__ void __launch_bounds__(256, ABED_PACK_MINB) pack_input_smem_kernel(const int8_t* __restrict__ x, ActGeom g, int lrb,
+                                                                 PackDiv div_bands, int ipb, int pad0, int wp,
+                                                                 int8_t* __restrict__ out) {
+  extern __shared__ __align__(128) uint8_t tile[];  // 2 x [rb][wp][16]
   const int rb = 1 << lrb;
-  const int plane = blockIdx.y;
-  const int grp = plane % g.c16, phase = plane / g.c16;
-  const int a = phase / g.nph_w, b = phase % g.nph_w;
+  const int grp = blockIdx.y, phase = blockIdx.z;
+  const int plane = phase * g.c16 + grp;
+  int a = phase, b = 0;
+  if (SW == 2 && g.nph_w == 2) a = phase >> 1, b = phase & 1;
+  if (SW == 0) a = phase / g.nph_w, b = phase - a * g.nph_w;
   uint4* const pbase = reinterpret_cast<uint4*>(out) + (int64_t)plane * g.plane_len;
-  if (blockIdx.x == (unsigned)(g.n * nbands)) {  // zero tail of this plane
+  if (blockIdx.x == gridDim.x - 1) {  // zero tail of this plane
     for (int64_t t = g.m_total + threadIdx.x; t < g.plane_len; t += blockDim.x) pbase[t] = make_uint4(0, 0, 0, 0);
     return;
   }
-  const int n = blockIdx.x / nbands, i0 = (blockIdx.x - n * nbands) * rb;
+  const int ng = div_bands.div(blockIdx.x);
+  const int i0 = (blockIdx.x - ng * (int)div_bands.d) * rb;
   const int rows = min(rb, g.Hl - i0);
   const int nch = max(0, min(16, g.c - grp * 16));  // 0: a filler group (c16 is even)
+  const int nq = (nch + 3) >> 2;
   const int npix = rows * g.Wl;
-  uint4* const st4 = reinterpret_cast<uint4*>(tile);
-  for (int i = threadIdx.x; i < npix; i += blockDim.x) st4[i] = make_uint4(0, 0, 0, 0);
-  __syncthreads();
-  const int64_t HW = (int64_t)g.h * g.w;
-  const int8_t* xg = x + ((int64_t)n * g.c + grp * 16) * HW;
+  const int HW = g.h * g.w;
   const int off = g.pw - b;  // output column j holds input column j * sw - off
   const int sw = SW ? SW : g.sw;
-  uint32_t* const t32 = reinterpret_cast<uint32_t*>(tile);
-  if (words_ok) {
-    // lanes split into row groups of lpr lanes (lane -> word q of a row); warps and
-    // row groups walk the (channel quad, band row) pairs: no divisions per item
-    const int wq = g.w >> 2;
-    const int lpr = wq <= 4 ? 4 : wq <= 8 ? 8 : wq <= 16 ? 16 : 32;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int sub = lane / lpr, ql = lane - sub * lpr;
-    const int gpw = 32 / lpr;  // row groups per warp
-    const int nq = (nch + 3) >> 2;
-    const int npairs = nq << lrb;
-    // U row-pair iterations per batch (4U loads in flight per thread; U = 4 cost
-    // registers and occupancy and measured no faster on B200, so U = 1)
-    constexpr int U = 1;
-    for (int rb0 = warp * gpw; rb0 < npairs; rb0 += U * 8 * gpw) {
-      for (int q0 = 0; q0 < wq; q0 += lpr) {
-        const int q = q0 + ql;
-        uint32_t v[U][4];
-        bool okr[U];
+  // valid output columns [jlo, jhi): 0 <= j * sw - off < w
+  int jlo, jhi;
+  if (SW == 1) {
+    jlo = max(off, 0);
+    jhi = min(g.Wl, g.w + off);
+  } else {
+    jlo = off <= 0 ? 0 : (off + sw - 1) / sw;
+    jhi = min(g.Wl, g.w - 1 + off < 0 ? 0 : (g.w - 1 + off) / sw + 1);
+  }
+  // valid band rows [ilo, ihi): 0 <= r0 + ii * sh < h
+  const int r0 = i0 * g.sh + a - g.ph;
+  int ilo = 0, ihi = rows;
+  while (ilo < rows && r0 + ilo * g.sh < 0) ++ilo;
+  while (ihi > ilo && r0 + (ihi - 1) * g.sh >= g.h) --ihi;
+  // phase-1 lane roles (fixed for the block): lanes split into groups of lpr lanes
+  // (lane -> input word q of a row); a group is one (row, channel quad) pair
+  // rp = 4 * ii + cq; warps and groups walk the pairs
+  const int wq = WB ? g.w / WB : 0;
+  const int lpr = wq <= 4 ? 4 : wq <= 8 ? 8 : wq <= 16 ? 16 : 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int sub = lane / lpr, ql = lane - sub * lpr;
+  const int gpw = 32 / lpr;
+  const int npairs = ihi << 2;
+  const int rp0 = ilo * 4 + warp * gpw + sub;
+  // common case: every thread has at most one item; its source offset and smem
+  // address are fixed for all images of the block
+  const bool one = WB != 0 && (ihi - ilo) * 4 <= 8 * gpw && wq <= lpr;
+  // (pinned in registers: the compiler would otherwise recompute them per image)
+  uint32_t lm0 = 0;
+  if (one && rp0 < npairs && ql < wq) lm0 = (1u << max(0, min(4, nch - 4 * (rp0 & 3)))) - 1u;
+  int src0 = (rp0 & 3) * 4 * HW + (r0 + (rp0 >> 2) * g.sh) * g.w + ql * WB;
+  int base0 = SW == 1 ? pack_slot((rp0 >> 2) * wp + pad0 + off + ql * 4 * (WB >= 4 ? WB / 4 : 1)) * 16 + (rp0 & 3) * 4
+                      : -1;
+  asm volatile("" : "+r"(lm0), "+r"(src0), "+r"(base0));
+  // phase 2: the (up to 4) pixels of this thread and their smem slots, packed
+  // two per register (0xffff: halo, stored as zeros; 0xfffe: no pixel)
+  const bool p2fast = npix <= 4 * 256 && nq == 4;
+  uint32_t slots[2] = {0xfffefffeu, 0xfffefffeu};
+  if (p2fast) {
+    const float rwl = 1.0f / (float)g.Wl;
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int r = rb0 + u * 8 * gpw + sub;
-          const int cq = r >> lrb, ii = r & (rb - 1);
-          const int hh = (i0 + ii) * g.sh + a - g.ph;
-          okr[u] = r < npairs && ii < rows && hh >= 0 && hh < g.h && q < wq;
-          const int8_t* src = xg + (int64_t)(cq * 4) * HW + (int64_t)hh * g.w;
-#pragma unroll
-          for (int e = 0; e < 4; ++e)
-            v[u][e] = (okr[u] && cq * 4 + e < nch) ? __ldg(reinterpret_cast<const uint32_t*>(src + e * HW) + q) : 0u;
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          if (!okr[u]) continue;
-          const int r = rb0 + u * 8 * gpw + sub;
-          const int cq = r >> lrb, ii = r & (rb - 1);
-          // 4 x 4 byte transpose: p[t] = channels 4cq..4cq+3 of input column 4q + t
-          const uint32_t t01lo = __byte_perm(v[u][0], v[u][1], 0x5140), t01hi = __byte_perm(v[u][0], v[u][1], 0x7362);
-          const uint32_t t23lo = __byte_perm(v[u][2], v[u][3], 0x5140), t23hi = __byte_perm(v[u][2], v[u][3], 0x7362);
-          uint32_t pw4[4] = {__byte_perm(t01lo, t23lo, 0x5410), __byte_perm(t01lo, t23lo, 0x7632),
-                             __byte_perm(t01hi, t23hi, 0x5410), __byte_perm(t01hi, t23hi, 0x7632)};
-          // rotate by q & 3 so one store instruction of the warp spreads over the
-          // banks: lane writes column 4q + ((t + q) & 3) at step t
-          const int rot = q & 3;
-          if (rot & 1) {
-            const uint32_t t0 = pw4[0];
-            pw4[0] = pw4[1]; pw4[1] = pw4[2]; pw4[2] = pw4[3]; pw4[3] = t0;
-          }
-          if (rot & 2) {
-            const uint32_t t0 = pw4[0], t1 = pw4[1];
-            pw4[0] = pw4[2]; pw4[1] = pw4[3]; pw4[2] = t0; pw4[3] = t1;
-          }
-          uint32_t* const trow = t32 + ii * g.Wl * 4 + cq;
-#pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            const int jj = q * 4 + ((t + rot) & 3) + off;  // = j * sw
-            int j;
-            if (SW == 1) {
-              j = jj;
-            } else if (SW == 2) {
-              if (jj & 1) continue;
-              j = jj >> 1;
-            } else {
-              if (jj % sw) continue;
-              j = jj / sw;
-            }
-            if (jj < 0 || j >= g.Wl) continue;
-            trow[j * 4] = pw4[t];
-          }
+    for (int k = 0; k < 4; ++k) {
+      const int i = threadIdx.x + 256 * k;
+      const int ii = __float2int_rz(((float)i + 0.5f) * rwl);
+      const int j = i - ii * g.Wl;
+      uint32_t sl = 0xfffeu;
+      if (i < npix)
+        sl = (ii >= ilo && ii < ihi && j >= jlo && j < jhi) ? (uint32_t)pack_slot(ii * wp + pad0 + j) : 0xffffu;
+      slots[k >> 1] = (slots[k >> 1] & ~(0xffffu << (16 * (k & 1)))) | (sl << (16 * (k & 1)));
+    }
+    asm volatile("" : "+r"(slots[0]), "+r"(slots[1]));
+  }
+  const int n_end = min(g.n, (ng + 1) * ipb);
+  // per-image pointers advance by one image: this thread's item source, the band's output
+  const int64_t xstep = (int64_t)g.c * HW, dstep = (int64_t)g.Hl * g.Wl;
+  const int8_t* xg = x + ((int64_t)ng * ipb * g.c + grp * 16) * HW;
+  uint4* dst = pbase + ((int64_t)ng * ipb * g.Hl + i0) * g.Wl;
+  for (int n = ng * ipb; n < n_end; ++n, xg += xstep, dst += dstep) {
+    uint8_t* const buf = tile + (size_t)((n - ng * ipb) & 1) * 16 * rb * wp;
+    if (WB != 0) {
+      if (one) {
+        if (lm0) pack_item<SW, WB>(xg + src0, HW, lm0, rp0 & 3, buf, ql, rp0 >> 2, wp, pad0, off, sw, g.Wl, base0);
+      } else {
+        for (int rp = rp0; rp < npairs; rp += 8 * gpw) {
+          const int cq = rp & 3, ii = rp >> 2;
+          if (cq >= nq) continue;
+          const uint32_t lm = (1u << min(4, nch - 4 * cq)) - 1u;
+          const int8_t* const src = xg + cq * 4 * HW + (r0 + ii * g.sh) * g.w;
+          for (int q = ql; q < wq; q += lpr)
+            pack_item<SW, WB>(src + q * WB, HW, lm, cq, buf, q, ii, wp, pad0, off, sw, g.Wl, -1);
         }
       }
+    } else {
+      const int total = nch * rows * g.w;
+      for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+        const int e = idx / (rows * g.w), rem = idx - e * rows * g.w, ii = rem / g.w, ww = rem - ii * g.w;
+        if (ii < ilo || ii >= ihi) continue;
+        const int jj = ww + off;
+        if (jj < 0 || jj % sw) continue;
+        const int j = jj / sw;
+        if (j >= g.Wl) continue;
+        buf[pack_slot(ii * wp + pad0 + j) * 16 + e] = (uint8_t)xg[e * HW + (r0 + ii * g.sh) * g.w + ww];
+      }
+      // channels nch..4nq-1 of the last quad: zero (phase 2 masks whole quads only)
+      if (nch & 3)
+        for (int i = threadIdx.x; i < rows * wp; i += blockDim.x)
+          for (int e = nch; e < 4 * nq; ++e) buf[i * 16 + e] = 0;
     }
-  } else {
-    const int total = nch * rows * g.w;
-    for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
-      const int e = idx / (rows * g.w), rem = idx - e * rows * g.w, ii = rem / g.w, ww = rem - ii * g.w;
-      const int hh = (i0 + ii) * g.sh + a - g.ph;
-      const int jj = ww + off;
-      if (hh < 0 || hh >= g.h || jj < 0 || jj % sw) continue;
-      const int j = jj / sw;
-      if (j >= g.Wl) continue;
-      tile[(ii * g.Wl + j) * 16 + e] = (uint8_t)xg[e * HW + (int64_t)hh * g.w + ww];
+    __syncthreads();
+    const uint4* const st4 = reinterpret_cast<const uint4*>(buf);
+    if (p2fast) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t sl = (slots[k >> 1] >> (16 * (k & 1))) & 0xffffu;
+        if (sl != 0xfffeu) dst[threadIdx.x + 256 * k] = sl != 0xffffu ? st4[sl] : make_uint4(0, 0, 0, 0);
+      }
+    } else {
+      const float rwl = 1.0f / (float)g.Wl;
+      for (int i = threadIdx.x; i < npix; i += blockDim.x) {
+        const int ii = __float2int_rz(((float)i + 0.5f) * rwl);  // exact: i < 8 Wl, Wl <= 1536
+        const int j = i - ii * g.Wl;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (ii >= ilo && ii < ihi && j >= jlo && j < jhi && nq > 0) {
+          v = st4[pack_slot(ii * wp + pad0 + j)];
+          if (nq < 4) {
+            if (nq < 2) v.y = 0;
+            if (nq < 3) v.z = 0;
+            v.w = 0;
+          }
+        }
+        dst[i] = v;
+      }
     }
+    // the next image writes the other buffer; the one after this reuses this one
+    // only after the next barrier, which every thread reaches after its phase 2
   }
-  __syncthreads();
-  uint4* const dst = pbase + ((int64_t)n * g.Hl + i0) * g.Wl;
-  for (int i = threadIdx.x; i < npix; i += blockDim.x) dst[i] = st4[i];
 }
 
 void launch_pack_input(const int8_t* x, const ActGeom& g, int8_t* packed, cudaStream_t st) {
   const int planes = g.n_phase * g.c16;
   const int64_t x_bytes = (int64_t)g.n * g.c * g.h * g.w;
-  // band height: a power of two <= 8 M-space rows, <= 24 KB of staged output pixels
+  // smem rows: wp 16-byte slots, output pixel j at slot pad0 + j; with stride 1
+  // pad0 makes input column 0 land on a multiple of 8 slots
+  const int pad0 = g.sw == 1 ? (8 - (g.pw & 7)) & 7 : 0;
+  const int wp = (std::max(pad0 + g.Wl, g.sw == 1 ? pad0 + g.pw + g.w : 0) + 7) & ~7;
+  // band height: a power of two <= 8 M-space rows, <= 24 KB of staged pixels (x2 buffers)
   int lrb = 3;
-  while (lrb > 0 && (16 << lrb) * g.Wl > 24 * 1024) --lrb;
-  if (16 * g.Wl <= 48 * 1024) {
+  while (lrb > 0 && (16 << lrb) * wp > 24 * 1024) --lrb;
+  if (16 * wp <= 24 * 1024) {
     const int rb = 1 << lrb;
     const int nbands = (g.Hl + rb - 1) / rb;
-    const int words_ok = (g.w % 4 == 0) && (reinterpret_cast<uintptr_t>(x) & 3) == 0;
-    const size_t smem = (size_t)16 * rb * g.Wl;
-    const dim3 grid((unsigned)(g.n * nbands + 1), (unsigned)planes);
+    const uintptr_t xa = reinterpret_cast<uintptr_t>(x);
+    const int wb = (g.w % 8 == 0 && (xa & 7) == 0) ? 8 : (g.w % 4 == 0 && (xa & 3) == 0) ? 4 : 0;
+    // images per block: amortise the per-block setup while keeping >= ~4 waves
+    const char* ipb_s = getenv("ABED_PACK_IPB");  // tuning / test override
+    const int ipb_env = ipb_s ? atoi(ipb_s) : 0;
+    int ipb = ipb_env > 0 ? ipb_env : 1;
+    if (ipb_env <= 0)
+      while (ipb < 4 && (int64_t)((g.n + 2 * ipb - 1) / (2 * ipb)) * nbands * planes >= (int64_t)num_sms() * 8) ipb *= 2;
+    const int ngroups = (g.n + ipb - 1) / ipb;
+    const size_t smem = (size_t)2 * 16 * rb * wp;
+    const dim3 grid((unsigned)(ngroups * nbands + 1), (unsigned)g.c16, (unsigned)g.n_phase);
+    const PackDiv div_bands = pack_div((uint32_t)nbands);
+#define ABED_PACK_LAUNCH(SWV)                                                                     \
+  do {                                                                                             \
+    if (wb == 8)                                                                                   \
+      pack_input_smem_kernel<SWV, 8><<<grid, 256, smem, st>>>(x, g, lrb, div_bands, ipb, pad0, wp, packed);     \
+    else if (wb == 4)                                                                              \
+      pack_input_smem_kernel<SWV, 4><<<grid, 256, smem, st>>>(x, g, lrb, div_bands, ipb, pad0, wp, packed);     \
+    else                                                                                           \
+      pack_input_smem_kernel<SWV, 0><<<grid, 256, smem, st>>>(x, g, lrb, div_bands, ipb, pad0, wp, packed);     \
+  } while (0)
     if (g.sw == 1)
-      pack_input_smem_kernel<1><<<grid, 256, smem, st>>>(x, g, lrb, nbands, words_ok, packed);
+      ABED_PACK_LAUNCH(1);
     else if (g.sw == 2)
-      pack_input_smem_kernel<2><<<grid, 256, smem, st>>>(x, g, lrb, nbands, words_ok, packed);
+      ABED_PACK_LAUNCH(2);
     else
-      pack_input_smem_kernel<0><<<grid, 256, smem, st>>>(x, g, lrb, nbands, words_ok, packed);
+      ABED_PACK_LAUNCH(0);
+#undef ABED_PACK_LAUNCH
     return;
   }
   // very wide rows: the register-transpose kernel

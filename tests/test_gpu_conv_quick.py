@@ -43,24 +43,35 @@ def test_conv_i8_matches_exact(dims):
     assert bad.numel() == 0, f"{bad.shape[0]} mismatches, first {bad[:4].tolist()} got {got.flatten()[:8]} want {want.flatten()[:8]}"
 
 
-@pytest.mark.parametrize("dims", SHAPES + [(2, 20, 13, 17, 16, 3, 3, 1, 1, 1, 1), (1, 16, 9, 6, 16, 1, 1, 1, 1, 0, 0)])
-def test_pack_input_vector_path_equals_byte_path(dims):
-    """abed_pack_input's 4-pixel vector path (aligned source) and its per-pixel
-    gather (the same tensor at an odd address) give identical strip planes, and the
-    conv on them is exact."""
+PACK_SHAPES = SHAPES + [(2, 20, 13, 17, 16, 3, 3, 1, 1, 1, 1), (1, 16, 9, 6, 16, 1, 1, 1, 1, 0, 0),
+                        (5, 6, 11, 24, 8, 3, 3, 2, 2, 1, 1), (3, 40, 9, 16, 16, 5, 5, 1, 1, 2, 2),
+                        (4, 17, 6, 32, 8, 3, 3, 2, 1, 0, 1)]
+
+
+@pytest.mark.parametrize("ipb", [None, 2, 3])
+@pytest.mark.parametrize("dims", PACK_SHAPES)
+def test_pack_input_vector_path_equals_byte_path(dims, ipb, monkeypatch):
+    """abed_pack_input's 8-column and 4-column word paths (source aligned to 8 / to
+    4 bytes only) and its per-pixel gather (the same tensor at an odd address) give
+    identical strip planes, also with several images per block (ABED_PACK_IPB), and
+    the conv on them is exact."""
     from paper_2006_04984_b200 import api
+    if ipb is not None:
+        monkeypatch.setenv("ABED_PACK_IPB", str(ipb))
     ls = abi.layer_shape(*dims)
     g = torch.Generator().manual_seed(7 + sum(dims))
     x = torch.randint(-128, 128, ls.input_dims(), dtype=torch.int8, generator=g).cuda()
     f = torch.randint(-128, 128, ls.filter_dims(), dtype=torch.int8, generator=g).cuda()
     plan = api.ConvPlan(ls, f, 0)
     a = plan.pack(x, plan.packed_buffer())
-    raw = torch.empty(x.numel() + 1, dtype=torch.int8, device="cuda")
-    raw[1:].copy_(x.flatten())
-    b = plan.packed_buffer()
-    abi.call("abed_pack_input", plan.handle, raw.data_ptr() + 1, b.data_ptr(), None)
-    torch.cuda.synchronize()
-    assert torch.equal(a, b)
+    for shift in (4, 1):
+        raw = torch.empty(x.numel() + 8, dtype=torch.int8, device="cuda")
+        raw[shift:shift + x.numel()].copy_(x.flatten())
+        b = plan.packed_buffer()
+        b.fill_(77)  # the pack writes every byte (halo, filler channels, plane tails)
+        abi.call("abed_pack_input", plan.handle, raw.data_ptr() + shift, b.data_ptr(), None)
+        torch.cuda.synchronize()
+        assert torch.equal(a, b), shift
     out = torch.empty(ls.output_dims(), dtype=torch.int32, device="cuda")
     plan.run(a, out, abi.OUT_I32_NCHW)
     torch.cuda.synchronize()
