@@ -246,13 +246,11 @@ static PackDiv pack_div(uint32_t d) {
   return PackDiv{(uint32_t)(((1ull << 32) * ((1ull << l) - d)) / d + 1), l, d};
 }
 
-// one (band row, channel quad, input word) item of phase 1: load, transpose, store
-template <int SW, int WB>
-__device__ __forceinline__ void pack_item(const int8_t* src, int HW, uint32_t lm, int cq, uint8_t* buf, int q, int ii,
-                                          int wp, int pad0, int off, int sw, int Wl, int fixed_base) {
+// one (band row, channel quad, input word) item of phase 1: load (pack_load),
+// transpose and store to the staging rows (pack_store)
+template <int WB>
+__device__ __forceinline__ void pack_load(const int8_t* src, int HW, uint32_t lm, uint32_t (&v)[4][WB >= 4 ? WB / 4 : 1]) {
   constexpr int NW = WB >= 4 ? WB / 4 : 1;  // 32-bit words per load
-  constexpr int NP = 4 * NW;                // columns per word
-  uint32_t v[4][NW];
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
     if ((lm >> e) & 1u) {  // channel 4cq + e exists
@@ -268,6 +266,13 @@ __device__ __forceinline__ void pack_item(const int8_t* src, int HW, uint32_t lm
       for (int h = 0; h < NW; ++h) v[e][h] = 0u;
     }
   }
+}
+
+template <int SW, int WB>
+__device__ __forceinline__ void pack_store(const uint32_t (&v)[4][WB >= 4 ? WB / 4 : 1], int cq, uint8_t* buf, int q,
+                                           int ii, int wp, int pad0, int off, int sw, int Wl, int fixed_base) {
+  constexpr int NW = WB >= 4 ? WB / 4 : 1;  // 32-bit words per load
+  constexpr int NP = 4 * NW;                // columns per word
   // 4 x 4 byte transposes: pw[4h + t] = channels 4cq..4cq+3 of column WB*q + 4h + t
   uint32_t pw[NP];
 #pragma unroll
@@ -386,19 +391,27 @@ __global__ void __launch_bounds__(256, ABED_PACK_MINB) pack_input_smem_kernel(co
   const int64_t xstep = (int64_t)g.c * HW, dstep = (int64_t)g.Hl * g.Wl;
   const int8_t* xg = x + ((int64_t)ng * ipb * g.c + grp * 16) * HW;
   uint4* dst = pbase + ((int64_t)ng * ipb * g.Hl + i0) * g.Wl;
+  constexpr int NW = WB >= 4 ? WB / 4 : 1;
+  uint32_t v[4][NW];  // common case: the next image's item, loaded before this image's phase 2
+  if (WB != 0 && one && lm0) pack_load<WB>(xg + src0, HW, lm0, v);
   for (int n = ng * ipb; n < n_end; ++n, xg += xstep, dst += dstep) {
     uint8_t* const buf = tile + (size_t)((n - ng * ipb) & 1) * 16 * rb * wp;
     if (WB != 0) {
       if (one) {
-        if (lm0) pack_item<SW, WB>(xg + src0, HW, lm0, rp0 & 3, buf, ql, rp0 >> 2, wp, pad0, off, sw, g.Wl, base0);
+        if (lm0) {
+          pack_store<SW, WB>(v, rp0 & 3, buf, ql, rp0 >> 2, wp, pad0, off, sw, g.Wl, base0);
+          if (n + 1 < n_end) pack_load<WB>(xg + xstep + src0, HW, lm0, v);
+        }
       } else {
         for (int rp = rp0; rp < npairs; rp += 8 * gpw) {
           const int cq = rp & 3, ii = rp >> 2;
           if (cq >= nq) continue;
           const uint32_t lm = (1u << min(4, nch - 4 * cq)) - 1u;
           const int8_t* const src = xg + cq * 4 * HW + (r0 + ii * g.sh) * g.w;
-          for (int q = ql; q < wq; q += lpr)
-            pack_item<SW, WB>(src + q * WB, HW, lm, cq, buf, q, ii, wp, pad0, off, sw, g.Wl, -1);
+          for (int q = ql; q < wq; q += lpr) {
+            pack_load<WB>(src + q * WB, HW, lm, v);
+            pack_store<SW, WB>(v, cq, buf, q, ii, wp, pad0, off, sw, g.Wl, -1);
+          }
         }
       }
     } else {
