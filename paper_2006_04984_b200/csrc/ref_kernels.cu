@@ -283,6 +283,88 @@ __global__ void __launch_bounds__(kColsumWarps * 32) colsum_i8_cluster_kernel(co
   cluster.sync();  // keep this CTA's partials alive until every peer has read them
 }
 
+// Wide variant for long rows (the batch checksum: 256 images x 200704 bytes): a
+// CTA owns 4096 adjacent columns (256 threads x one 16-byte vector, so one load
+// instruction of the CTA reads 4 KB contiguous of one row -- whole DRAM pages,
+// where the 512-column tiles above touch 512 bytes per row and page) and a row
+// range; each thread sums its 16 columns over the rows (no cross-warp reduction).
+// Row splits of a tile form a cluster and are summed through DSMEM as above.
+constexpr int kColsumWideCols = 4096;
+__global__ void __launch_bounds__(256, 4) colsum_i8_wide_kernel(const int8_t* __restrict__ x, int64_t rows,
+                                                                int64_t len, int64_t rows_per,
+                                                                int32_t* __restrict__ out) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  __shared__ __align__(16) int32_t s_part[kColsumWideCols];
+  const int cs = static_cast<int>(cluster.num_blocks());
+  const int rank = static_cast<int>(cluster.block_rank());
+  const int64_t cols16 = len >> 4;
+  const int64_t tile = blockIdx.x / cs;
+  const int64_t c16 = tile * 256 + threadIdx.x;
+  const int64_t r0 = rank * rows_per, r1 = r0 + rows_per < rows ? r0 + rows_per : rows;
+  int32_t acc[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) acc[j] = 0;
+  if (c16 < cols16 && r1 > r0) {
+    const uint4* ptr = reinterpret_cast<const uint4*>(x) + c16 + r0 * cols16;
+    const int64_t mine = r1 - r0;
+    int64_t done = 0;
+    while (done < mine) {
+      uint32_t ev[4] = {0u, 0u, 0u, 0u}, od[4] = {0u, 0u, 0u, 0u};
+      const int64_t batch_end = done + 256 < mine ? done + 256 : mine;  // 16-bit lanes: <= 256 rows per flush
+      while (done < batch_end) {  // batches of 16 rows, every load issued before use
+        const int rem = batch_end - done < 16 ? static_cast<int>(batch_end - done) : 16;
+        uint4 v[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+          v[u] = u < rem ? __ldcs(ptr + u * cols16) : make_uint4(0x80808080u, 0x80808080u, 0x80808080u, 0x80808080u);
+        ptr += rem * cols16;
+        done += rem;
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {  // padding slots add (0x80 ^ 0x80) = 0
+          const uint32_t w[4] = {v[u].x ^ 0x80808080u, v[u].y ^ 0x80808080u, v[u].z ^ 0x80808080u,
+                                 v[u].w ^ 0x80808080u};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            ev[q] += w[q] & 0x00FF00FFu;
+            od[q] += (w[q] >> 8) & 0x00FF00FFu;
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        acc[4 * q] += static_cast<int32_t>(ev[q] & 0xFFFFu);
+        acc[4 * q + 1] += static_cast<int32_t>(od[q] & 0xFFFFu);
+        acc[4 * q + 2] += static_cast<int32_t>(ev[q] >> 16);
+        acc[4 * q + 3] += static_cast<int32_t>(od[q] >> 16);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) acc[j] -= static_cast<int32_t>(128 * mine);
+  }
+  if (cs == 1) {
+    if (c16 < cols16) {
+      int4* o = reinterpret_cast<int4*>(out + c16 * 16);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) o[j] = make_int4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
+    }
+    return;
+  }
+  int4* sp = reinterpret_cast<int4*>(s_part + threadIdx.x * 16);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) sp[j] = make_int4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
+  cluster.sync();
+  const int per = (kColsumWideCols + cs - 1) / cs;
+  for (int cl = rank * per + threadIdx.x; cl < (rank + 1) * per && cl < kColsumWideCols; cl += 256) {
+    const int64_t col = tile * kColsumWideCols + cl;
+    if (col >= len) continue;
+    int32_t sum = 0;
+    for (int q = 0; q < cs; ++q) sum += cluster.map_shared_rank(s_part, q)[cl];
+    out[col] = sum;
+  }
+  cluster.sync();  // keep this CTA's partials alive until every peer has read them
+}
+
 // any length / alignment: one column per thread, the same row split
 __global__ void colsum_i8_kernel(const int8_t* __restrict__ x, int64_t rows, int64_t len, int64_t rows_per,
                                  int32_t* __restrict__ out) {
@@ -530,6 +612,42 @@ int guarded2(Fn&& fn) {
 void dev_colsum_i8(const int8_t* x, int64_t rows, int64_t len, int32_t* out, cudaStream_t st) {
   const bool v16 = (len % 16 == 0) && (reinterpret_cast<uintptr_t>(x) % 16 == 0);
   if (v16) {
+    const int64_t wide_tiles = (len + kColsumWideCols - 1) / kColsumWideCols;
+    const char* force_s = getenv("ABED_COLSUM_KERNEL");  // tuning / tests: 1 wide, 2 narrow
+    const int force = force_s ? atoi(force_s) : 0;
+    if (force != 2 && (force == 1 || wide_tiles * 16 >= num_sms())) {
+      // row splits: a power-of-two cluster <= 8 (measured on the 256 x 200704 batch
+      // checksum: cs 8 13.3 us, 4 15.4, 16 17.9, 12 20.5), one wave of <= 4 CTAs
+      // per SM, >= 8 rows per split
+      int64_t cs = 8;
+      while (cs > 1 && (wide_tiles * cs > (int64_t)num_sms() * 4 || (rows + cs - 1) / cs < 8)) cs >>= 1;
+      const char* cs_s = getenv("ABED_COLSUM_CS");  // tuning experiments
+      if (cs_s && atoi(cs_s) > 0) cs = atoi(cs_s);
+      if (cs < 1) cs = 1;
+      const int64_t rows_per = (rows + cs - 1) / cs;
+      static bool wattr[64] = {};
+      int dev = 0;
+      cudaGetDevice(&dev);
+      if (dev < 0 || dev >= 64 || !wattr[dev]) {
+        cuda_check(cudaFuncSetAttribute(colsum_i8_wide_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
+                   "colsum cluster attr");
+        if (dev >= 0 && dev < 64) wattr[dev] = true;
+      }
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)(wide_tiles * cs));
+      cfg.blockDim = dim3(256);
+      cfg.stream = st;
+      cudaLaunchAttribute la[1];
+      la[0].id = cudaLaunchAttributeClusterDimension;
+      la[0].val.clusterDim.x = (unsigned)cs;
+      la[0].val.clusterDim.y = 1;
+      la[0].val.clusterDim.z = 1;
+      cfg.attrs = la;
+      cfg.numAttrs = 1;
+      cuda_check(cudaLaunchKernelEx(&cfg, colsum_i8_wide_kernel, x, rows, len, rows_per, out), "colsum launch");
+      launched("colsum_i8");
+      return;
+    }
     // row splits of a 512-column tile = one cluster (<= 16 CTAs, DSMEM reduction):
     // about 8 resident CTAs per SM in one wave, at least one row per warp
     const int64_t col_tiles = (len / 16 + 31) / 32;

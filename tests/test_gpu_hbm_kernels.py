@@ -36,6 +36,23 @@ def test_batch_checksum(nchw):
     assert torch.equal(got, x.to(torch.int32).sum(0, keepdim=True))
 
 
+@pytest.mark.parametrize("kernel", ["1", "2"], ids=["wide", "narrow"])
+@pytest.mark.parametrize("nchw", [(40, 64, 56, 56), (300, 4, 32, 32), (17, 3, 100, 100), (1, 16, 16, 16),
+                                  (513, 1, 4, 4)])
+@pytest.mark.parametrize("fill", [None, 127, -128])
+def test_batch_checksum_kernels(nchw, kernel, fill, monkeypatch):
+    """Both 16-byte-vector column-sum kernels (4096-column tiles reading whole
+    pages per row, and 512-column tiles), forced by ABED_COLSUM_KERNEL, with and
+    without row-split clusters, more than 256 rows (the 16-bit lane flush) and the
+    extreme values of both signs."""
+    monkeypatch.setenv("ABED_COLSUM_KERNEL", kernel)
+    g = torch.Generator().manual_seed(sum(nchw))
+    x = torch.full(nchw, fill, dtype=torch.int8) if fill is not None else \
+        torch.randint(-128, 128, nchw, dtype=torch.int8, generator=g)
+    got = api.ic_batch_checksum(x.cuda()).cpu()
+    assert torch.equal(got, x.to(torch.int32).sum(0, keepdim=True))
+
+
 @pytest.mark.parametrize("nkpq", [(2, 64, 56, 56), (1, 3, 5, 7), (2, 16, 4, 4), (1, 8, 3, 16)])
 @pytest.mark.parametrize("relu", [True, False])
 @pytest.mark.parametrize("kind", [abi.I8, abi.F32])
