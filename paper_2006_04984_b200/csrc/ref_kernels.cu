@@ -365,6 +365,77 @@ __global__ void __launch_bounds__(256, 4) colsum_i8_wide_kernel(const int8_t* __
   cluster.sync();  // keep this CTA's partials alive until every peer has read them
 }
 
+// Tall variant for short rows (the filter checksum: 512 filters x 4608 bytes): a
+// CTA owns 32 adjacent columns of EVERY row (128 row groups x two 16-byte
+// vectors), so ~one CTA per SM covers the matrix with all its loads in flight at
+// once and no row split, cluster or atomic: the rows are summed in registers
+// (16-bit lanes), then across the 128 row groups in shared memory.
+__global__ void __launch_bounds__(256) colsum_i8_tall_kernel(const int8_t* __restrict__ x, int64_t rows, int64_t len,
+                                                             int32_t* __restrict__ out) {
+  __shared__ int32_t part[128][33];
+  __shared__ int32_t red2[8][32];
+  const int64_t cols16 = len >> 4;
+  const int vec = threadIdx.x & 1, g = threadIdx.x >> 1;
+  const int64_t c16 = (int64_t)blockIdx.x * 2 + vec;
+  int32_t acc[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) acc[j] = 0;
+  if (c16 < cols16 && g < rows) {
+    const int64_t mine = (rows - g + 127) / 128;  // rows g, g + 128, ...
+    const uint4* ptr = reinterpret_cast<const uint4*>(x) + c16 + g * cols16;
+    const int64_t step = 128 * cols16;
+    int64_t done = 0;
+    while (done < mine) {
+      uint32_t ev[4] = {0u, 0u, 0u, 0u}, od[4] = {0u, 0u, 0u, 0u};
+      const int64_t batch_end = done + 256 < mine ? done + 256 : mine;  // 16-bit lanes: <= 256 rows per flush
+      while (done < batch_end) {  // batches of 8 rows, every load issued before use
+        const int rem = batch_end - done < 8 ? static_cast<int>(batch_end - done) : 8;
+        uint4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          v[u] = u < rem ? __ldcs(ptr + u * step) : make_uint4(0x80808080u, 0x80808080u, 0x80808080u, 0x80808080u);
+        ptr += rem * step;
+        done += rem;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {  // padding slots add (0x80 ^ 0x80) = 0
+          const uint32_t w[4] = {v[u].x ^ 0x80808080u, v[u].y ^ 0x80808080u, v[u].z ^ 0x80808080u,
+                                 v[u].w ^ 0x80808080u};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            ev[q] += w[q] & 0x00FF00FFu;
+            od[q] += (w[q] >> 8) & 0x00FF00FFu;
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        acc[4 * q] += static_cast<int32_t>(ev[q] & 0xFFFFu);
+        acc[4 * q + 1] += static_cast<int32_t>(od[q] & 0xFFFFu);
+        acc[4 * q + 2] += static_cast<int32_t>(ev[q] >> 16);
+        acc[4 * q + 3] += static_cast<int32_t>(od[q] >> 16);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) acc[j] -= static_cast<int32_t>(128 * mine);
+  }
+#pragma unroll
+  for (int j = 0; j < 16; ++j) part[g][vec * 16 + j] = acc[j];
+  __syncthreads();
+  const int c = threadIdx.x & 31, sl = threadIdx.x >> 5;
+  int32_t sum = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) sum += part[sl * 16 + i][c];
+  red2[sl][c] = sum;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    int32_t tot = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) tot += red2[i][c];
+    const int64_t col = (int64_t)blockIdx.x * 32 + c;
+    if (col < len) out[col] = tot;
+  }
+}
+
 // any length / alignment: one column per thread, the same row split
 __global__ void colsum_i8_kernel(const int8_t* __restrict__ x, int64_t rows, int64_t len, int64_t rows_per,
                                  int32_t* __restrict__ out) {
@@ -613,9 +684,10 @@ void dev_colsum_i8(const int8_t* x, int64_t rows, int64_t len, int32_t* out, cud
   const bool v16 = (len % 16 == 0) && (reinterpret_cast<uintptr_t>(x) % 16 == 0);
   if (v16) {
     const int64_t wide_tiles = (len + kColsumWideCols - 1) / kColsumWideCols;
-    const char* force_s = getenv("ABED_COLSUM_KERNEL");  // tuning / tests: 1 wide, 2 narrow
+    // tuning / tests: 1 wide, 2 not wide, 3 tall, 4 cluster (2 and 4: the 512-column tiles)
+    const char* force_s = getenv("ABED_COLSUM_KERNEL");
     const int force = force_s ? atoi(force_s) : 0;
-    if (force != 2 && (force == 1 || wide_tiles * 16 >= num_sms())) {
+    if (force == 1 || (force == 0 && wide_tiles * 16 >= num_sms())) {
       // row splits: a power-of-two cluster <= 8 (measured on the 256 x 200704 batch
       // checksum: cs 8 13.3 us, 4 15.4, 16 17.9, 12 20.5), one wave of <= 4 CTAs
       // per SM, >= 8 rows per split
@@ -645,6 +717,14 @@ void dev_colsum_i8(const int8_t* x, int64_t rows, int64_t len, int32_t* out, cud
       cfg.attrs = la;
       cfg.numAttrs = 1;
       cuda_check(cudaLaunchKernelEx(&cfg, colsum_i8_wide_kernel, x, rows, len, rows_per, out), "colsum launch");
+      launched("colsum_i8");
+      return;
+    }
+    // short rows: 32-column CTAs over all rows when they fill the SMs without
+    // more than ~4 CTAs per SM
+    const int64_t tall_tiles = (len / 16 + 1) / 2;
+    if (force != 4 && (force == 3 || (tall_tiles <= (int64_t)num_sms() * 4 && tall_tiles * 2 >= num_sms() && rows >= 64))) {
+      colsum_i8_tall_kernel<<<(unsigned)tall_tiles, 256, 0, st>>>(x, rows, len, out);
       launched("colsum_i8");
       return;
     }

@@ -18,9 +18,11 @@ def ora():
 
 
 @pytest.mark.parametrize("kcrs", [(64, 64, 3, 3), (512, 512, 3, 3), (3, 5, 3, 3), (300, 3, 3, 3), (1, 16, 1, 1),
-                                  (7, 1, 1, 1), (1000, 16, 1, 1)])
+                                  (7, 1, 1, 1), (1000, 16, 1, 1), (40000, 16, 1, 1), (2048, 512, 1, 1)])
 @pytest.mark.parametrize("extreme", [False, True])
-def test_filter_checksum(ora, kcrs, extreme):
+@pytest.mark.parametrize("kernel", ["0", "3", "4"], ids=["auto", "tall", "cluster"])
+def test_filter_checksum(ora, kcrs, extreme, kernel, monkeypatch):
+    monkeypatch.setenv("ABED_COLSUM_KERNEL", kernel)
     g = torch.Generator().manual_seed(sum(kcrs))
     f = torch.full(kcrs, -128, dtype=torch.int8) if extreme else torch.randint(-128, 128, kcrs, dtype=torch.int8,
                                                                                 generator=g)
@@ -36,15 +38,15 @@ def test_batch_checksum(nchw):
     assert torch.equal(got, x.to(torch.int32).sum(0, keepdim=True))
 
 
-@pytest.mark.parametrize("kernel", ["1", "2"], ids=["wide", "narrow"])
+@pytest.mark.parametrize("kernel", ["1", "3", "4"], ids=["wide", "tall", "cluster"])
 @pytest.mark.parametrize("nchw", [(40, 64, 56, 56), (300, 4, 32, 32), (17, 3, 100, 100), (1, 16, 16, 16),
                                   (513, 1, 4, 4)])
 @pytest.mark.parametrize("fill", [None, 127, -128])
 def test_batch_checksum_kernels(nchw, kernel, fill, monkeypatch):
-    """Both 16-byte-vector column-sum kernels (4096-column tiles reading whole
-    pages per row, and 512-column tiles), forced by ABED_COLSUM_KERNEL, with and
-    without row-split clusters, more than 256 rows (the 16-bit lane flush) and the
-    extreme values of both signs."""
+    """The three 16-byte-vector column-sum kernels (4096-column tiles reading
+    whole pages per row, 32-column tiles over all rows, 512-column tiles with
+    row-split clusters), forced by ABED_COLSUM_KERNEL, with more than 256 rows per
+    thread lane (the 16-bit flush) and the extreme values of both signs."""
     monkeypatch.setenv("ABED_COLSUM_KERNEL", kernel)
     g = torch.Generator().manual_seed(sum(nchw))
     x = torch.full(nchw, fill, dtype=torch.int8) if fill is not None else \
