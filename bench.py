@@ -1090,6 +1090,11 @@ def run_ours(args, world, rank, local):
         h2d = sum(t.numel() for t in host_in)
         d2h = sum(t.numel() for t in host_out) + oc_host.numel()
 
+        # issue order: the smallest input first and the smallest output last, so the
+        # pipeline's lone first H2D and lone last D2H are short
+        first = min(range(len(layers)), key=lambda i: host_in[i].numel())
+        last = min((i for i in range(len(layers)) if i != first), key=lambda i: host_out[i].numel())
+        order = [first] + [i for i in range(len(layers)) if i not in (first, last)] + [last]
         # three streams pipelined across the 16 layers: the copy engines move layer
         # i+1's input in and layer i-1's output out while layer i computes (each
         # layer owns its device buffers, so there are no hazards inside a step)
@@ -1100,7 +1105,8 @@ def run_ours(args, world, rank, local):
             cur = torch.cuda.current_stream()
             for st_ in (s_in, s_cmp, s_out):
                 st_.wait_stream(cur)
-            for i, L in enumerate(layers):
+            for i in order:
+                L = layers[i]
                 pl = L["plans"]["fic"]
                 with torch.cuda.stream(s_in):
                     dev_in[i].copy_(host_in[i], non_blocking=True)
@@ -1146,8 +1152,29 @@ def run_ours(args, world, rank, local):
             t = torch.tensor([e_ms], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = t.item()
+        # the PCIe floor of the same bytes: one H2D of the step's inputs and one D2H of
+        # its outputs + verdicts, concurrently on two streams, nothing else
+        fl_in = torch.empty(int(h2d), dtype=torch.int8).pin_memory()
+        fl_out = torch.empty(int(d2h), dtype=torch.int8).pin_memory()
+        fl_din = torch.empty(int(h2d), dtype=torch.int8, device=dev)
+        fl_dout = torch.empty(int(d2h), dtype=torch.int8, device=dev)
+
+        def copies_only():
+            cur = torch.cuda.current_stream()
+            s_in.wait_stream(cur)
+            s_out.wait_stream(cur)
+            with torch.cuda.stream(s_in):
+                fl_din.copy_(fl_in, non_blocking=True)
+            with torch.cuda.stream(s_out):
+                fl_out.copy_(fl_dout, non_blocking=True)
+            cur.wait_stream(s_in)
+            cur.wait_stream(s_out)
+
+        copies_only()
+        floor_ms = time_e2e(copies_only)
         e2e = {"value": round(ops_step / (e_ms * 1e-3) / 1e12, 3), "unit": "TOPS", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": round(e_ms, 3), "eager_ms_per_step": round(eager_ms, 3),
+               "pcie_floor_ms": round(floor_ms, 3), "frac_of_pcie_floor": round(floor_ms / e_ms, 3),
                "path": "per layer: pinned H2D NCHW -> abed_pack_input -> abed_conv_plan_run(FIC, OUT_I8_NCHW) -> "
                        "abed_conv_plan_finalize -> D2H output + verdicts; H2D / compute / D2H on three streams, "
                        "pipelined across the 16 layers; the step's calls captured once as a CUDA graph and replayed "
