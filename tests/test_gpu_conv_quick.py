@@ -45,7 +45,8 @@ def test_conv_i8_matches_exact(dims):
 
 PACK_SHAPES = SHAPES + [(2, 20, 13, 17, 16, 3, 3, 1, 1, 1, 1), (1, 16, 9, 6, 16, 1, 1, 1, 1, 0, 0),
                         (5, 6, 11, 24, 8, 3, 3, 2, 2, 1, 1), (3, 40, 9, 16, 16, 5, 5, 1, 1, 2, 2),
-                        (4, 17, 6, 32, 8, 3, 3, 2, 1, 0, 1)]
+                        (4, 17, 6, 32, 8, 3, 3, 2, 1, 0, 1), (2, 16, 20, 24, 16, 3, 3, 3, 3, 1, 1),
+                        (1, 8, 17, 32, 8, 5, 5, 3, 2, 2, 2)]
 
 
 @pytest.mark.parametrize("ipb", [None, 2, 3])
