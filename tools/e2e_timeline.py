@@ -27,6 +27,9 @@ for li, (name, c, h, w, k, st) in enumerate(bench.RESNET50_3X3):
                    "hin": x.cpu().pin_memory(), "din": torch.empty_like(x),
                    "dout": torch.empty(ls.output_dims(), dtype=torch.int8, device=dev),
                    "hout": torch.empty(ls.output_dims(), dtype=torch.int8).pin_memory()})
+groups = int(os.environ.get("E2E_GROUPS", "0"))  # >0: copies per group of consecutive layers
+if groups:
+    os.environ["E2E_ONE_PINNED"] = "1"
 if os.environ.get("E2E_ONE_PINNED"):  # carve every host buffer from one pinned block per direction
     tot_in = sum(L["hin"].numel() for L in layers)
     tot_out = sum(L["hout"].numel() for L in layers)
@@ -39,6 +42,17 @@ if os.environ.get("E2E_ONE_PINNED"):  # carve every host buffer from one pinned 
         L["hin"] = v
         oi += v.numel()
         L["hout"] = big_out[oo:oo + L["hout"].numel()].view(L["hout"].shape)
+        oo += L["hout"].numel()
+    # matching contiguous device blocks
+    dbig_in = torch.empty(tot_in, dtype=torch.int8, device=dev)
+    dbig_out = torch.empty(tot_out, dtype=torch.int8, device=dev)
+    oi = oo = 0
+    for L in layers:
+        L["din"] = dbig_in[oi:oi + L["hin"].numel()].view(L["hin"].shape)
+        L["in_off"] = oi
+        oi += L["hin"].numel()
+        L["dout"] = dbig_out[oo:oo + L["hout"].numel()].view(L["hout"].shape)
+        L["out_off"] = oo
         oo += L["hout"].numel()
 oc_dev = torch.empty(216 * len(layers), dtype=torch.uint8, device=dev)
 oc_host = torch.empty(216 * len(layers), dtype=torch.uint8).pin_memory()
@@ -54,7 +68,38 @@ def ev(stream):
     return e
 
 
+def step_grouped(marks):
+    cur = torch.cuda.current_stream()
+    for st_ in (s_in, s_cmp, s_out):
+        st_.wait_stream(cur)
+    n = len(layers)
+    bounds = [round(i * n / groups) for i in range(groups + 1)]
+    for gi in range(groups):
+        ls_ = list(range(bounds[gi], bounds[gi + 1]))
+        a, b = layers[ls_[0]], layers[ls_[-1]]
+        i0, i1 = a["in_off"], b["in_off"] + b["hin"].numel()
+        o0, o1 = a["out_off"], b["out_off"] + b["hout"].numel()
+        with torch.cuda.stream(s_in):
+            dbig_in[i0:i1].copy_(big_in[i0:i1], non_blocking=True)
+        s_cmp.wait_stream(s_in)
+        for i in ls_:
+            L = layers[i]
+            L["plan"].pack(L["din"], L["packed"], stream=sp)
+            L["plan"].run(L["packed"], L["dout"], abi.OUT_I8_NCHW, ep=L["ep"], stream=sp)
+            abi.call("abed_conv_plan_finalize", L["plan"].handle, oc_dev[i * 216:].data_ptr(), sp)
+        s_out.wait_stream(s_cmp)
+        with torch.cuda.stream(s_out):
+            big_out[o0:o1].copy_(dbig_out[o0:o1], non_blocking=True)
+    with torch.cuda.stream(s_out):
+        s_out.wait_stream(s_cmp)
+        oc_host.copy_(oc_dev, non_blocking=True)
+    for st_ in (s_in, s_cmp, s_out):
+        cur.wait_stream(st_)
+
+
 def step(marks):
+    if groups:
+        return step_grouped(marks)
     cur = torch.cuda.current_stream()
     for st_ in (s_in, s_cmp, s_out):
         st_.wait_stream(cur)
