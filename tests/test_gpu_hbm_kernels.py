@@ -67,3 +67,15 @@ def test_epilog(ora, nkpq, relu, kind):
     got = api.epilog(acc.cuda(), scale, bias, relu, kind).cpu().numpy()
     want = ora.epilog(acc.numpy(), scale, bias, relu=relu, out_f32=kind == abi.F32)
     assert np.array_equal(got.view(np.uint8), np.asarray(want).view(np.uint8))
+
+
+@pytest.mark.parametrize("nv", ["1", "2", "4", "8"])
+@pytest.mark.parametrize("kcrs", [(512, 512, 3, 3), (300, 3, 3, 3), (1000, 16, 1, 1), (70, 9, 5, 5)])
+def test_filter_checksum_tall_widths(ora, kcrs, nv, monkeypatch):
+    """The tall column-sum kernel at every column width per CTA (16 * NV)."""
+    monkeypatch.setenv("ABED_COLSUM_KERNEL", "3")
+    monkeypatch.setenv("ABED_COLSUM_TALL_NV", nv)
+    g = torch.Generator().manual_seed(sum(kcrs) + int(nv))
+    f = torch.randint(-128, 128, kcrs, dtype=torch.int8, generator=g)
+    got = api.gen_filter_checksum(f.cuda()).cpu().numpy()
+    assert np.array_equal(got, ora.gen_filter_checksum(f.numpy()))
