@@ -226,8 +226,11 @@ __global__ void __launch_bounds__(256) pack_input_v4_kernel(const int8_t* __rest
 // row are never read) and their addresses are one XOR apart.  Phase 2 writes the
 // band out with 16-byte stores; halo pixels (rows / columns outside the input)
 // and filler channel quads are written as zeros there, so there is no zeroing
-// pass.  Every input byte read once per stride phase, every output byte written
-// once.  WB = 0: rows that are not a multiple of 4 bytes (or an unaligned base)
+// pass.  When every thread has at most one item (the common case) its source
+// offset, smem address and copy-out slots are computed once per block and pinned
+// in registers, and the next image's words are loaded before the current image's
+// barrier and copy-out.  Every input byte read once per stride phase, every output
+// byte written once.  WB = 0: rows that are not a multiple of 4 bytes (or an unaligned base)
 // use byte loads.  The zero tail of each plane (after the last image) is written
 // by one extra block per plane.
 #ifndef ABED_PACK_MINB
