@@ -23,7 +23,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
          "-diag-suppress", "177", "-I", os.path.join(ROOT, "include")]
 # diagnostics builds only (e.g. ABED_NVCC_EXTRA=-DABED_CONV_DEBUG=1 for the conv
-# kernel's timing-experiment flags used by tools/epi_probe.py; rebuild from clean)
+# kernel's timing-experiment flags used by tools/epi_probe.py); a change of flags
+# rebuilds every object
 FLAGS += os.environ.get("ABED_NVCC_EXTRA", "").split()
 
 
@@ -41,6 +42,14 @@ def build(verbose: bool = False) -> str:
     headers = glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h")) + \
         glob.glob(os.path.join(ROOT, "include", "*.h"))
     hdr_mtime = max((os.path.getmtime(h) for h in headers), default=0)
+    # objects built with other flags (ABED_NVCC_EXTRA, a different nvcc) are stale
+    stamp = os.path.join(BUILD, "flags.txt")
+    flags_now = " ".join([NVCC, *ARCH, *FLAGS])
+    if not os.path.exists(stamp) or open(stamp).read() != flags_now:
+        for o in glob.glob(os.path.join(BUILD, "*.o")):
+            os.remove(o)
+        with open(stamp, "w") as fh:
+            fh.write(flags_now)
     objs, cmds = [], []
     for src in sources:
         obj = os.path.join(BUILD, os.path.basename(src).replace(".cu", ".o"))
