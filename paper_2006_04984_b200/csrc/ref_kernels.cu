@@ -290,7 +290,13 @@ __global__ void __launch_bounds__(kColsumWarps * 32) colsum_i8_cluster_kernel(co
 // range; each thread sums its 16 columns over the rows (no cross-warp reduction).
 // Row splits of a tile form a cluster and are summed through DSMEM as above.
 constexpr int kColsumWideCols = 4096;
-__global__ void __launch_bounds__(256, 4) colsum_i8_wide_kernel(const int8_t* __restrict__ x, int64_t rows,
+#ifndef ABED_COLSUM_WIDE_U
+#define ABED_COLSUM_WIDE_U 16  // rows (16-byte loads) in flight per thread
+#endif
+#ifndef ABED_COLSUM_WIDE_MINB
+#define ABED_COLSUM_WIDE_MINB 4
+#endif
+__global__ void __launch_bounds__(256, ABED_COLSUM_WIDE_MINB) colsum_i8_wide_kernel(const int8_t* __restrict__ x, int64_t rows,
                                                                 int64_t len, int64_t rows_per,
                                                                 int32_t* __restrict__ out) {
   namespace cg = cooperative_groups;
@@ -312,16 +318,17 @@ __global__ void __launch_bounds__(256, 4) colsum_i8_wide_kernel(const int8_t* __
     while (done < mine) {
       uint32_t ev[4] = {0u, 0u, 0u, 0u}, od[4] = {0u, 0u, 0u, 0u};
       const int64_t batch_end = done + 256 < mine ? done + 256 : mine;  // 16-bit lanes: <= 256 rows per flush
-      while (done < batch_end) {  // batches of 16 rows, every load issued before use
-        const int rem = batch_end - done < 16 ? static_cast<int>(batch_end - done) : 16;
-        uint4 v[16];
+      while (done < batch_end) {  // batches of U rows, every load issued before use
+        constexpr int U = ABED_COLSUM_WIDE_U;
+        const int rem = batch_end - done < U ? static_cast<int>(batch_end - done) : U;
+        uint4 v[U];
 #pragma unroll
-        for (int u = 0; u < 16; ++u)
+        for (int u = 0; u < U; ++u)
           v[u] = u < rem ? __ldcs(ptr + u * cols16) : make_uint4(0x80808080u, 0x80808080u, 0x80808080u, 0x80808080u);
         ptr += rem * cols16;
         done += rem;
 #pragma unroll
-        for (int u = 0; u < 16; ++u) {  // padding slots add (0x80 ^ 0x80) = 0
+        for (int u = 0; u < U; ++u) {  // padding slots add (0x80 ^ 0x80) = 0
           const uint32_t w[4] = {v[u].x ^ 0x80808080u, v[u].y ^ 0x80808080u, v[u].z ^ 0x80808080u,
                                  v[u].w ^ 0x80808080u};
 #pragma unroll
@@ -694,7 +701,8 @@ void dev_colsum_i8(const int8_t* x, int64_t rows, int64_t len, int32_t* out, cud
       // checksum: cs 8 13.3 us, 4 15.4, 16 17.9, 12 20.5), one wave of <= 4 CTAs
       // per SM, >= 8 rows per split
       int64_t cs = 8;
-      while (cs > 1 && (wide_tiles * cs > (int64_t)num_sms() * 4 || (rows + cs - 1) / cs < 8)) cs >>= 1;
+      while (cs > 1 && (wide_tiles * cs > (int64_t)num_sms() * ABED_COLSUM_WIDE_MINB || (rows + cs - 1) / cs < 8))
+        cs >>= 1;
       const char* cs_s = getenv("ABED_COLSUM_CS");  // tuning experiments
       if (cs_s && atoi(cs_s) > 0) cs = atoi(cs_s);
       if (cs < 1) cs = 1;
