@@ -893,6 +893,7 @@ def run_ours(args, world, rank, local):
         L["plans"]["fic_sm"].set_input_checksum_source(abi.RHS_STAGED)
         # the captured pass finalizes every IC run it contains
         L["plans"]["ic"].set_paired_finalize(True)
+        L["plans"]["icbatch"].set_paired_finalize(True)
         L["packed"] = L["plans"]["unprotected"].pack(x)
         # ICBatch: the packed input also holds the batch-sum digit images (written in-kernel)
         L["packed_icb"] = L["plans"]["icbatch"].pack(x)

@@ -101,8 +101,7 @@ int mma_pattern_of(const abed_dev::ActGeom& g, int gps);
 // pdl: launch with programmatic stream serialization (griddepcontrol in the kernel)
 cudaError_t conv_tc_launch(const abed_dev::ConvTcParams& p, int num_sms, bool pdl, cudaStream_t stream);
 // ICBatch: compare and reset after a fused run (p.icb_ready = {writer counter, ticket})
-cudaError_t icb_scan_launch(const abed_dev::ConvTcParams& p, int64_t* rec, abed_verify_outcome* out,
-                            cudaStream_t stream);
+cudaError_t icb_scan_launch(const abed_dev::IcbScanJob* jobs, int n, cudaStream_t stream);
 // reduces the per-CTA verdict records of n plans (one block each)
 cudaError_t verdict_launch(const abed_dev::VerdictJob* jobs, int n, cudaStream_t stream);
 
@@ -191,6 +190,7 @@ struct abed_conv_plan {
   int reuse_input_checksum = 0;
   int last_rhs_mode = 0;
   int ic_pending = 0;                      // IC: a run's in-kernel sums await their verdict
+  int icb_pending = 0;                     // ICBatch: a run's batch sums await their scan
   int paired_finalize = 0;                 // IC: captured graphs finalize every run they contain
   abed_verify_outcome* d_ic_last = nullptr;  // IC: last verdict (repeated by a second finalize)
   unsigned long long cmp_seen = 0;         // compare runs: mismatches already reported

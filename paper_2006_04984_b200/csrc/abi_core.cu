@@ -555,6 +555,16 @@ void plan_run(abed_conv_plan* pl, const int8_t* packed, const abed_epilog_params
                         (pl->ic_pending || (cap != cudaStreamCaptureStatusNone && !pl->paired_finalize));
   if (ic_dirty) cuda_check(cudaMemsetAsync(pl->d_acc + 4, 0, pl->shape.k * 8, st), "memset ic");
   if (pl->checks & ABED_CHECK_IC) pl->ic_pending = 1;
+  // ICBatch: the same for the batch sums and the digit-writer counter, which the
+  // scan at finalize consumes and resets
+  const bool icb_dirty = (pl->checks & ABED_CHECK_ICBATCH) &&
+                         (pl->icb_pending || (cap != cudaStreamCaptureStatusNone && !pl->paired_finalize));
+  if (icb_dirty) {
+    cuda_check(cudaMemsetAsync(pl->d_icb_lhs, 0, (size_t)pl->shape.k * pl->shape.p * pl->shape.q * 8, st),
+               "memset icb_lhs");
+    cuda_check(cudaMemsetAsync(pl->d_icb_ctl, 0, 8, st), "memset icb_ctl");
+  }
+  if (pl->checks & ABED_CHECK_ICBATCH) pl->icb_pending = 1;
   // compare runs accumulate mismatches; compare_count reports the increase
   p.rhs_mode = 0;
   p.conv_grid = conv_tc_grid(p, num_sms());
@@ -644,7 +654,23 @@ void plan_run(abed_conv_plan* pl, const int8_t* packed, const abed_epilog_params
   pl->last_rhs_mode = p.rhs_mode;
   pl->last_grid = p.conv_grid + p.ic_ctas;
   cuda_check(conv_tc_launch(p, num_sms(), pl->pdl != 0, st), "conv_i8_tc launch");
-  if (p.icb_d) cuda_check(icb_scan_launch(p, pl->d_icb_rec, pl->d_icb_out, st), "icb_scan launch");
+}
+
+// ICBatch scan of the plan's last run (ic_batch_verify, checksum.hpp:398-421) --
+// launched by the finalize that first follows the run, batched over the pass
+static abed_dev::IcbScanJob icb_scan_job(abed_conv_plan* pl) {
+  abed_dev::IcbScanJob j{};
+  j.lhs = pl->d_icb_lhs;
+  j.dig = pl->d_icb_dig;
+  j.D = pl->g.n_extra;
+  j.Q = (int)pl->g.q;
+  j.PQ = (int64_t)pl->g.p * pl->g.q;
+  j.kpq = (int64_t)pl->shape.k * j.PQ;
+  j.rec = pl->d_icb_rec;
+  j.ctl = pl->d_icb_ctl;
+  j.out = pl->d_icb_out;
+  pl->icb_pending = 0;
+  return j;
 }
 
 abed_dev::VerdictJob plan_verdict_job(const abed_conv_plan* pl, abed_verify_outcome* out_dev) {
@@ -678,6 +704,10 @@ abed_dev::VerdictJob plan_verdict_job(const abed_conv_plan* pl, abed_verify_outc
 void plan_finalize(abed_conv_plan* pl, abed_verify_outcome* out_dev, cudaStream_t st) {
   // IC first: with FIC its input checksum also gives FIC's rhs
   if (pl->checks & ABED_CHECK_IC) ic_verdict(pl, out_dev + 2, st);
+  if ((pl->checks & ABED_CHECK_ICBATCH) && pl->icb_pending) {
+    const abed_dev::IcbScanJob j = icb_scan_job(pl);
+    cuda_check(icb_scan_launch(&j, 1, st), "icb_scan");
+  }
   // FC / FIC: reduce the conv kernel's per-CTA records into VerifyOutcomes
   if (pl->checks & (ABED_CHECK_FC | ABED_CHECK_FIC | ABED_CHECK_ICBATCH)) {
     const abed_dev::VerdictJob j = plan_verdict_job(pl, out_dev);
@@ -789,14 +819,19 @@ int abed_conv_plan_finalize_many(abed_conv_plan* const* plans, int32_t n, abed_v
     if (n < 0) throw_invalid("finalize_many: negative plan count");
     std::vector<abed_dev::VerdictJob> jobs;
     std::vector<IcVerdictJob> ic_jobs;
+    std::vector<abed_dev::IcbScanJob> icb_jobs;
     for (int i = 0; i < n; ++i) {
       abed_conv_plan* pl = plans[i];
+      if ((pl->checks & ABED_CHECK_ICBATCH) && pl->icb_pending) icb_jobs.push_back(icb_scan_job(pl));
       if (pl->checks & (ABED_CHECK_FC | ABED_CHECK_FIC | ABED_CHECK_ICBATCH))
         jobs.push_back(plan_verdict_job(pl, outcomes_dev + 3 * i));
       if (pl->checks & ABED_CHECK_IC) ic_jobs.push_back(ic_verdict_job(pl, outcomes_dev + 3 * i + 2, (cudaStream_t)stream));
     }
     // IC first (with FIC its input checksum also gives FIC's rhs): two launches for all plans
     if (!ic_jobs.empty()) ic_verdict_many_launch(ic_jobs.data(), (int)ic_jobs.size(), (cudaStream_t)stream);
+    // ICBatch: one scan launch for every plan of the pass (its outcome goes to slot 2 in the verdict)
+    if (!icb_jobs.empty())
+      cuda_check(icb_scan_launch(icb_jobs.data(), (int)icb_jobs.size(), (cudaStream_t)stream), "icb_scan");
     if (!jobs.empty()) cuda_check(verdict_launch(jobs.data(), (int)jobs.size(), (cudaStream_t)stream), "verdict");
   });
 }

@@ -1,6 +1,8 @@
 // tcgen05 implicit-GEMM convolution: host launcher, verdict reduction kernel.
 // The conv kernel itself lives in conv_tc_kernel.cuh (see its header comment);
 // its (dtype, output flavour) variants are compiled in conv_inst_*.cu.
+#include <algorithm>
+
 #include "conv_tc_kernel.cuh"
 
 namespace abed_host {
@@ -176,12 +178,15 @@ __global__ void __launch_bounds__(256) verdict_kernel(const __grid_constant__ Ve
 // digit images' rows); mismatch count and the first mismatch in the reference's
 // (k, p, q) order with its lhs / rhs.  Resets icb_lhs and the writer counter for
 // the next run; the last block (ticket) folds the per-block records.
-__global__ void __launch_bounds__(256) icb_scan_kernel(unsigned long long* __restrict__ lhs,
-                                                       const int32_t* __restrict__ dig, int D, int64_t kpq,
-                                                       int64_t PQ, int Q, int64_t* __restrict__ rec,
-                                                       unsigned int* __restrict__ ctl, abed_verify_outcome* out) {
-  pdl_launch_dependents();  // the next layer's prologue may overlap this scan
-  pdl_wait();
+__global__ void __launch_bounds__(256) icb_scan_kernel(const __grid_constant__ IcbScanBatch b) {
+  const IcbScanJob& j = b.job[blockIdx.y];
+  unsigned long long* const lhs = j.lhs;
+  const int32_t* const dig = j.dig;
+  const int D = j.D, Q = j.Q;
+  const int64_t kpq = j.kpq, PQ = j.PQ;
+  int64_t* const rec = j.rec;
+  unsigned int* const ctl = j.ctl;
+  abed_verify_outcome* const out = static_cast<abed_verify_outcome*>(j.out);
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   FcRec r{0, kNoKey, 0, 0};
   // 4 consecutive (k, p, q) per thread, every load of a group issued before use
@@ -317,24 +322,24 @@ cudaError_t verdict_launch(const abed_dev::VerdictJob* jobs, int n, cudaStream_t
   return cudaSuccess;
 }
 
-cudaError_t icb_scan_launch(const ConvTcParams& p, int64_t* rec, abed_verify_outcome* out, cudaStream_t stream) {
-  const int64_t kpq = static_cast<int64_t>(p.K) * p.P * p.Q;
-  int blocks = static_cast<int>((kpq + 1023) / 1024);
-  if (blocks > abed_dev::kIcbScanBlocks) blocks = abed_dev::kIcbScanBlocks;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(blocks);
-  cfg.blockDim = dim3(256);
-  cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  // plain launch (as the verdict): the programmatic-dependent launch measured
-  // 1.5-2.8 us slower per ICBatch layer
-  cfg.numAttrs = 0;
-  return cudaLaunchKernelEx(&cfg, abed_dev::icb_scan_kernel, p.icb_lhs, static_cast<const int32_t*>(p.icb_dig),
-                            p.icb_d, kpq, static_cast<int64_t>(p.P) * p.Q, p.Q, rec, p.icb_ready, out);
+cudaError_t icb_scan_launch(const abed_dev::IcbScanJob* jobs, int n, cudaStream_t stream) {
+  for (int i = 0; i < n; i += abed_dev::kMaxIcbScanJobs) {
+    abed_dev::IcbScanBatch b{};
+    const int m = std::min(abed_dev::kMaxIcbScanJobs, n - i);
+    int64_t max_kpq = 1;
+    for (int q = 0; q < m; ++q) {
+      b.job[q] = jobs[i + q];
+      max_kpq = std::max(max_kpq, jobs[i + q].kpq);
+    }
+    int blocks = static_cast<int>((max_kpq + 1023) / 1024);
+    if (blocks > abed_dev::kIcbScanBlocks) blocks = abed_dev::kIcbScanBlocks;
+    // plain launch (as the verdict): one per finalize, for every ICBatch plan of the
+    // pass (was one per run: 16 launches on the b32 step)
+    abed_dev::icb_scan_kernel<<<dim3(blocks, m), 256, 0, stream>>>(b);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 cudaError_t conv_tc_launch(const ConvTcParams& p_in, int num_sms, bool pdl, cudaStream_t stream) {

@@ -213,6 +213,21 @@ struct VerdictJob {
 constexpr int kMaxVerdictJobs = 32;
 // ICBatch verdict (icb_scan_kernel): per-block records {count, first key, lhs, rhs}
 constexpr int kIcbScanBlocks = 296;
+// one ICBatch plan's scan inputs; a pass scans every ICBatch plan in one launch
+// (blockIdx.y = job) at its finalize
+struct IcbScanJob {
+  unsigned long long* lhs;  // [K][P][Q] batch sums of the outputs (consumed: zeroed by the scan)
+  const int32_t* dig;       // [D][K][P][Q] conv of the batch-sum digit images
+  int D, Q;
+  int64_t kpq, PQ;
+  int64_t* rec;             // [kIcbScanBlocks][4] per-block records
+  unsigned int* ctl;        // {icb_ready, ticket}: reset by the last block
+  void* out;                // abed_verify_outcome of the run
+};
+constexpr int kMaxIcbScanJobs = 32;
+struct IcbScanBatch {
+  IcbScanJob job[kMaxIcbScanJobs];
+};
 struct VerdictBatch {
   int n;
   VerdictJob job[kMaxVerdictJobs];

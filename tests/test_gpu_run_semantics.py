@@ -166,3 +166,73 @@ def test_fused_conv_epilog_tap_on_the_cached_fic_plan(ora):
         conv = ora.conv_i8(x.numpy(), f.numpy(), ls)
         assert cs == int(conv.astype(np.int64).sum())
         assert np.array_equal(y.cpu().numpy(), ora.epilog(conv, 0.03, bias))
+
+
+def _icb_ref(ora, x, f, ls, fault_key=-1, fault_bit=0):
+    conv = ora.conv_i8(x.numpy(), f.numpy(), ls)
+    if fault_key >= 0:
+        flat = conv.reshape(-1).view(np.uint32)
+        flat[fault_key] ^= np.uint32(1 << fault_bit)
+    extra = ora.conv_batch_checksum(ora.ic_batch_checksum(x.numpy()), f.numpy(), ls)
+    return ora.ic_batch_verify(conv, extra)
+
+
+def test_icbatch_scan_at_finalize_consumes_and_repeats(ora):
+    """ICBatch: the scan of a run happens at the finalize that follows it (one launch
+    for every plan of a pass); a second finalize repeats the outcome; a run that was
+    never finalized is cleared before the next run accumulates (ic_batch_verify,
+    checksum.hpp:398-421)."""
+    ls = api.layer_shape(4, 32, 14, 14, 48, 3, 3, 1, 1, 1, 1)
+    x, f = _data(ls, 15)
+    plan = api.ConvPlan(ls, f.cuda(), abi.CHECK_ICBATCH)
+    packed = plan.pack(x.cuda())
+    out = torch.empty(ls.output_dims(), dtype=torch.int32, device="cuda")
+    key = 1 * ls.k * ls.p * ls.q + 9 * ls.p * ls.q + 4 * ls.q + 2
+    good, bad = _icb_ref(ora, x, f, ls), _icb_ref(ora, x, f, ls, key, 21)
+    assert good.status == 0 and bad.status == 1
+    plan.run(packed, out, abi.OUT_I32_NCHW, ep=None, fault_key=key, fault_bit=21)
+    plan.finalize()
+    assert _same(plan.outcomes()[2], bad)
+    plan.finalize()
+    assert _same(plan.outcomes()[2], bad)
+    plan.run(packed, out, abi.OUT_I32_NCHW, ep=None)
+    plan.finalize()
+    assert _same(plan.outcomes()[2], good)
+    plan.run(packed, out, abi.OUT_I32_NCHW, ep=None, fault_key=key, fault_bit=21)
+    plan.run(packed, out, abi.OUT_I32_NCHW, ep=None)
+    plan.finalize()
+    assert _same(plan.outcomes()[2], good)
+
+
+@pytest.mark.parametrize("paired", [False, True], ids=["run-only-graph", "paired-graph"])
+def test_icbatch_graph_replays(ora, paired):
+    """Captured ICBatch passes: run + finalize graphs (paired: no clearing memsets),
+    and run-only graphs replayed several times before one eager finalize."""
+    ls = api.layer_shape(3, 16, 12, 12, 32, 3, 3, 1, 1, 1, 1)
+    x, f = _data(ls, 16)
+    plans = [api.ConvPlan(ls, f.cuda(), abi.CHECK_ICBATCH) for _ in range(3)]
+    ps = api.PlanSet(plans)
+    for pl in plans:
+        pl.set_paired_finalize(paired)
+    packed = plans[0].pack(x.cuda())
+    outs = [torch.empty(ls.output_dims(), dtype=torch.int32, device="cuda") for _ in plans]
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        for pl, o in zip(plans, outs):
+            pl.run(packed, o, abi.OUT_I32_NCHW, ep=None)
+        ps.finalize()
+    torch.cuda.synchronize()
+    good = _icb_ref(ora, x, f, ls)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        for pl, o in zip(plans, outs):
+            pl.run(packed, o, abi.OUT_I32_NCHW, ep=None)
+        if paired:
+            ps.finalize()
+    for _ in range(4):
+        g.replay()
+    if not paired:
+        ps.finalize()
+    torch.cuda.synchronize()
+    for oc in ps.outcomes():
+        assert _same(oc[2], good)
