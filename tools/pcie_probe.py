@@ -26,3 +26,30 @@ for _ in range(10):
     ts.append(time.perf_counter() - t0)
 res["concurrent_61in_44out_ms"] = round(min(ts) * 1e3, 3)
 print(json.dumps(res))
+
+# write-combined pinned host memory (cudaHostAllocWriteCombined) for the H2D side
+try:
+    import ctypes
+    import numpy as np
+    from cuda.bindings import runtime as rt
+    nbytes = 61 << 20
+    err, ptr = rt.cudaHostAlloc(nbytes, rt.cudaHostAllocWriteCombined)
+    assert err == rt.cudaError_t.cudaSuccess, err
+    arr = np.ctypeslib.as_array((ctypes.c_int8 * nbytes).from_address(int(ptr)))
+    hwc = torch.from_numpy(arr)
+    d = torch.empty(nbytes, dtype=torch.int8, device=dev)
+    hreg = torch.empty(nbytes, dtype=torch.int8).pin_memory()
+    out = {}
+    for name, h in (("pinned", hreg), ("write_combined", hwc)):
+        for _ in range(3):
+            d.copy_(h, non_blocking=True)
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(10):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(); d.copy_(h, non_blocking=True); e1.record(); e1.synchronize(); ts.append(e0.elapsed_time(e1))
+        out[f"h2d_61MB_{name}_GBs"] = round(nbytes / (min(ts) * 1e-3) / 1e9, 1)
+    out["wc_is_pinned"] = bool(hwc.is_pinned())
+    print(json.dumps(out))
+except Exception as exc:  # noqa: BLE001
+    print(json.dumps({"write_combined": f"unavailable: {exc}"}))
