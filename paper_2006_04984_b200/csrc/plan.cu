@@ -918,10 +918,29 @@ __global__ void __launch_bounds__(128) ic_from_classes_many_kernel(const __grid_
     const int c = (int)(t / rs), r = (int)((t / j.Sd) % j.R), sc = (int)(t % j.Sd);
     const int a = r % j.sh, bb = sc % j.sw, phase = a * j.nph_w + bb;
     long long v = 0;
-    for (int rc = 0; rc < j.nrc; ++rc) {
-      if (!((j.rowmask[a * j.nrc + rc] >> r) & 1ull)) continue;
-      for (int cc = 0; cc < j.ncc; ++cc)
-        if ((j.colmask[bb * j.ncc + cc] >> sc) & 1ull) v += j.S[((int64_t)(phase * j.nrc + rc) * j.ncc + cc) * j.c256 + c];
+    if (j.nrc <= 4 && j.ncc <= 4) {
+      // unrolled over at most 4 x 4 classes: the (predicated) class-sum loads are
+      // independent and issue together instead of one L2 round trip each
+      long long part[4][4];
+#pragma unroll
+      for (int rc = 0; rc < 4; ++rc) {
+        const bool rok = rc < j.nrc && ((j.rowmask[a * j.nrc + (rc < j.nrc ? rc : 0)] >> r) & 1ull);
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {
+          const bool ok = rok && cc < j.ncc && ((j.colmask[bb * j.ncc + (cc < j.ncc ? cc : 0)] >> sc) & 1ull);
+          part[rc][cc] = ok ? j.S[((int64_t)(phase * j.nrc + rc) * j.ncc + cc) * j.c256 + c] : 0ll;
+        }
+      }
+#pragma unroll
+      for (int rc = 0; rc < 4; ++rc)
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) v += part[rc][cc];
+    } else {
+      for (int rc = 0; rc < j.nrc; ++rc) {
+        if (!((j.rowmask[a * j.nrc + rc] >> r) & 1ull)) continue;
+        for (int cc = 0; cc < j.ncc; ++cc)
+          if ((j.colmask[bb * j.ncc + cc] >> sc) & 1ull) v += j.S[((int64_t)(phase * j.nrc + rc) * j.ncc + cc) * j.c256 + c];
+      }
     }
     j.ic[t] = (int32_t)v;
     if (j.fsum) dot += (long long)j.fsum[t] * v;
@@ -953,6 +972,9 @@ __global__ void __launch_bounds__(256) ic_finalize_many_kernel(const __grid_cons
     long long dot = 0;
     const int8_t* fk = j.f + k * j.crs;
     if (vec) {
+      // unrolled: the loads of several 512-element steps in flight (layer4's
+      // 4608-element rows were 9 dependent L2 round trips per channel)
+#pragma unroll 4
       for (int64_t i = (int64_t)lane * 16; i < j.crs; i += 32 * 16) {
         const int4 fv = __ldg(reinterpret_cast<const int4*>(fk + i));
         const int4 c0 = __ldg(reinterpret_cast<const int4*>(j.ic + i)), c1 = __ldg(reinterpret_cast<const int4*>(j.ic + i + 4));
