@@ -972,9 +972,6 @@ __global__ void __launch_bounds__(256) ic_finalize_many_kernel(const __grid_cons
     long long dot = 0;
     const int8_t* fk = j.f + k * j.crs;
     if (vec) {
-      // unrolled: the loads of several 512-element steps in flight (layer4's
-      // 4608-element rows were 9 dependent L2 round trips per channel)
-#pragma unroll 4
       for (int64_t i = (int64_t)lane * 16; i < j.crs; i += 32 * 16) {
         const int4 fv = __ldg(reinterpret_cast<const int4*>(fk + i));
         const int4 c0 = __ldg(reinterpret_cast<const int4*>(j.ic + i)), c1 = __ldg(reinterpret_cast<const int4*>(j.ic + i + 4));
