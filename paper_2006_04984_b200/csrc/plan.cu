@@ -261,6 +261,8 @@ __device__ __forceinline__ void pack_load(const int8_t* src, int HW, uint32_t lm
         const uint2 t = __ldg(reinterpret_cast<const uint2*>(src + e * HW));
         v[e][0] = t.x;
         v[e][NW - 1] = t.y;
+      } else if (WB == 2) {
+        v[e][0] = __ldg(reinterpret_cast<const uint16_t*>(src + e * HW));
       } else {
         v[e][0] = __ldg(reinterpret_cast<const uint32_t*>(src + e * HW));
       }
@@ -275,9 +277,9 @@ template <int SW, int WB>
 __device__ __forceinline__ void pack_store(const uint32_t (&v)[4][WB >= 4 ? WB / 4 : 1], int cq, uint8_t* buf, int q,
                                            int ii, int wp, int pad0, int off, int sw, int Wl, int fixed_base) {
   constexpr int NW = WB >= 4 ? WB / 4 : 1;  // 32-bit words per load
-  constexpr int NP = 4 * NW;                // columns per word
+  constexpr int NP = WB >= 2 ? WB : 1;      // columns per word (WB = 2: the low two of a transpose)
   // 4 x 4 byte transposes: pw[4h + t] = channels 4cq..4cq+3 of column WB*q + 4h + t
-  uint32_t pw[NP];
+  uint32_t pw[4 * NW];
 #pragma unroll
   for (int h = 0; h < NW; ++h) {
     const uint32_t t01lo = __byte_perm(v[0][h], v[1][h], 0x5140), t01hi = __byte_perm(v[0][h], v[1][h], 0x7362);
@@ -368,7 +370,7 @@ __global__ void __launch_bounds__(256, ABED_PACK_MINB) pack_input_smem_kernel(co
   uint32_t lm0 = 0;
   if (one && rp0 < npairs && ql < wq) lm0 = (1u << max(0, min(4, nch - 4 * (rp0 & 3)))) - 1u;
   int src0 = (rp0 & 3) * 4 * HW + (r0 + (rp0 >> 2) * g.sh) * g.w + ql * WB;
-  int base0 = SW == 1 ? pack_slot((rp0 >> 2) * wp + pad0 + off + ql * 4 * (WB >= 4 ? WB / 4 : 1)) * 16 + (rp0 & 3) * 4
+  int base0 = SW == 1 ? pack_slot((rp0 >> 2) * wp + pad0 + off + ql * WB) * 16 + (rp0 & 3) * 4
                       : -1;
   asm volatile("" : "+r"(lm0), "+r"(src0), "+r"(base0));
   // phase 2: the (up to 4) pixels of this thread and their smem slots, packed
@@ -477,7 +479,10 @@ void launch_pack_input(const int8_t* x, const ActGeom& g, int8_t* packed, cudaSt
     const int rb = 1 << lrb;
     const int nbands = (g.Hl + rb - 1) / rb;
     const uintptr_t xa = reinterpret_cast<uintptr_t>(x);
-    const int wb = (g.w % 8 == 0 && (xa & 7) == 0) ? 8 : (g.w % 4 == 0 && (xa & 3) == 0) ? 4 : 0;
+    const int wb = (g.w % 8 == 0 && (xa & 7) == 0)   ? 8
+                   : (g.w % 4 == 0 && (xa & 3) == 0) ? 4
+                   : (g.w % 2 == 0 && (xa & 1) == 0) ? 2
+                                                     : 0;
     // images per block: amortise the per-block setup while keeping >= ~4 waves
     const char* ipb_s = getenv("ABED_PACK_IPB");  // tuning / test override
     const int ipb_env = ipb_s ? atoi(ipb_s) : 0;
@@ -494,6 +499,8 @@ void launch_pack_input(const int8_t* x, const ActGeom& g, int8_t* packed, cudaSt
       pack_input_smem_kernel<SWV, 8><<<grid, 256, smem, st>>>(x, g, lrb, div_bands, ipb, pad0, wp, packed);     \
     else if (wb == 4)                                                                              \
       pack_input_smem_kernel<SWV, 4><<<grid, 256, smem, st>>>(x, g, lrb, div_bands, ipb, pad0, wp, packed);     \
+    else if (wb == 2)                                                                              \
+      pack_input_smem_kernel<SWV, 2><<<grid, 256, smem, st>>>(x, g, lrb, div_bands, ipb, pad0, wp, packed);     \
     else                                                                                           \
       pack_input_smem_kernel<SWV, 0><<<grid, 256, smem, st>>>(x, g, lrb, div_bands, ipb, pad0, wp, packed);     \
   } while (0)

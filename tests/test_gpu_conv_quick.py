@@ -46,14 +46,15 @@ def test_conv_i8_matches_exact(dims):
 PACK_SHAPES = SHAPES + [(2, 20, 13, 17, 16, 3, 3, 1, 1, 1, 1), (1, 16, 9, 6, 16, 1, 1, 1, 1, 0, 0),
                         (5, 6, 11, 24, 8, 3, 3, 2, 2, 1, 1), (3, 40, 9, 16, 16, 5, 5, 1, 1, 2, 2),
                         (4, 17, 6, 32, 8, 3, 3, 2, 1, 0, 1), (2, 16, 20, 24, 16, 3, 3, 3, 3, 1, 1),
-                        (1, 8, 17, 32, 8, 5, 5, 3, 2, 2, 2)]
+                        (1, 8, 17, 32, 8, 5, 5, 3, 2, 2, 2), (6, 24, 10, 14, 16, 3, 3, 1, 1, 1, 1),
+                        (3, 36, 9, 10, 8, 3, 3, 2, 2, 1, 1), (2, 16, 7, 6, 16, 1, 1, 1, 1, 0, 0)]
 
 
 @pytest.mark.parametrize("ipb", [None, 2, 3])
 @pytest.mark.parametrize("dims", PACK_SHAPES)
 def test_pack_input_vector_path_equals_byte_path(dims, ipb, monkeypatch):
-    """abed_pack_input's 8-column and 4-column word paths (source aligned to 8 / to
-    4 bytes only) and its per-pixel gather (the same tensor at an odd address) give
+    """abed_pack_input's 8-, 4- and 2-column word paths (source aligned to 8 / 4 / 2
+    bytes, rows a multiple of it) and its per-pixel gather (an odd address) give
     identical strip planes, also with several images per block (ABED_PACK_IPB), and
     the conv on them is exact."""
     from paper_2006_04984_b200 import api
@@ -65,7 +66,7 @@ def test_pack_input_vector_path_equals_byte_path(dims, ipb, monkeypatch):
     f = torch.randint(-128, 128, ls.filter_dims(), dtype=torch.int8, generator=g).cuda()
     plan = api.ConvPlan(ls, f, 0)
     a = plan.pack(x, plan.packed_buffer())
-    for shift in (4, 1):
+    for shift in (4, 2, 1):
         raw = torch.empty(x.numel() + 8, dtype=torch.int8, device="cuda")
         raw[shift:shift + x.numel()].copy_(x.flatten())
         b = plan.packed_buffer()
