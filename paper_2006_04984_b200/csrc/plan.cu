@@ -230,7 +230,9 @@ __global__ void __launch_bounds__(256) pack_input_v4_kernel(const int8_t* __rest
 // offset, smem address and copy-out slots are computed once per block and pinned
 // in registers, and the next image's words are loaded before the current image's
 // barrier and copy-out.  Every input byte read once per stride phase, every output
-// byte written once.  WB = 0: rows that are not a multiple of 4 bytes (or an unaligned base)
+// byte written once.  WB = 2 for rows of an even width (ResNet's 14-wide stages:
+// 12.6 -> 6.1 us per b32 layer, stride 2: 34.7 -> 12.4 us).  WB = 0: odd widths
+// (or an odd base address)
 // use byte loads.  The zero tail of each plane (after the last image) is written
 // by one extra block per plane.
 #ifndef ABED_PACK_MINB
