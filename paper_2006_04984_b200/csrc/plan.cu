@@ -232,8 +232,8 @@ __global__ void __launch_bounds__(256) pack_input_v4_kernel(const int8_t* __rest
 // barrier and copy-out.  Every input byte read once per stride phase, every output
 // byte written once.  WB = 2 for rows of an even width (ResNet's 14-wide stages:
 // 12.6 -> 6.1 us per b32 layer, stride 2: 34.7 -> 12.4 us).  WB = 0: odd widths
-// (or an odd base address)
-// use byte loads.  The zero tail of each plane (after the last image) is written
+// (or an odd base address) use byte loads.  The zero tail of each plane (after
+// the last image) is written
 // by one extra block per plane.
 #ifndef ABED_PACK_MINB
 #define ABED_PACK_MINB 6  // resident 256-thread blocks per SM the register budget allows (40 regs; 5: 48 regs, 0.68 vs 0.71 of HBM)
